@@ -1,0 +1,161 @@
+"""Seeded synthetic workloads (BASELINE.json configs) -- INPUT GENERATION ONLY.
+
+The paper measures on DelBay2km / DelBay125m with hurricane-Sandy forcing
+(Table 1); those meshes and data are not available, so these
+seeded synthetic inputs stand in for them.  Every recipe
+follows SURVEY.md 8(d) and the readings Q19-Q28; nothing here computes any
+part of the FB-LTS method (no tendencies, no labels, no stepping).  The random
+numbers are drawn with ``numpy.random.default_rng(seed)``.
+"""
+from __future__ import annotations
+
+import dataclasses
+import json
+import os
+
+import numpy as np
+
+from .hexmesh import build_periodic_hex_mesh
+from .trisk_mesh import Mesh
+
+G = 9.81              # reading Q28
+F_PLANE = 1.0e-4      # f-plane configs 1, 2, 5
+RHO0 = 1000.0         # reading Q19
+TAU_X = 0.1           # N m^-2, reading Q19
+BETA = (0.531, 0.531, 0.313)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+DT_TABLE = os.path.join(os.path.dirname(_HERE), "configs", "dt.json")
+
+
+def periodic_step(x, L, W, n_images=2):
+    """Smooth periodic plateau: ~1 on [L/2, L), ~0 on [0, L/2) (reading Q20)."""
+    s = np.zeros_like(x)
+    for m in range(-n_images, n_images + 1):
+        s += 0.5 * (np.tanh((x - L / 2 + m * L) / W) - np.tanh((x - L + m * L) / W))
+    return s
+
+
+def grf_periodic(nx, ny, dx, dy, corr_len, rng):
+    """Zero-mean, unit-variance periodic Gaussian random field with Gaussian covariance.
+
+    Spectral synthesis on the (row, column) lattice of the mesh (reading Q22).
+    """
+    kx = 2 * np.pi * np.fft.fftfreq(nx, d=dx)
+    ky = 2 * np.pi * np.fft.fftfreq(ny, d=dy)
+    k2 = ky[:, None] ** 2 + kx[None, :] ** 2
+    amp = np.exp(-k2 * corr_len ** 2 / 8.0)          # sqrt of a Gaussian spectrum
+    noise = rng.standard_normal((ny, nx))
+    f = np.fft.ifft2(np.fft.fft2(noise) * amp).real
+    f -= f.mean()
+    f /= f.std()
+    return f.reshape(-1)
+
+
+def periodic_gaussians(mesh: Mesh, centres, amps, sigma):
+    """Sum of Gaussian bumps with 3x3 periodic images (reading Q23)."""
+    eta = np.zeros(mesh.nCells)
+    for (cx, cy), a in zip(centres, amps):
+        for mx in (-1, 0, 1):
+            for my in (-1, 0, 1):
+                dx = mesh.xCell - (cx + mx * mesh.Lx)
+                dy = mesh.yCell - (cy + my * mesh.Ly)
+                eta += a * np.exp(-(dx * dx + dy * dy) / (2.0 * sigma * sigma))
+    return eta
+
+
+@dataclasses.dataclass
+class Case:
+    name: str
+    mesh: Mesh
+    h0: np.ndarray
+    u0: np.ndarray
+    fine_mask: np.ndarray
+    tau_n: np.ndarray
+    M: int
+    dt: float
+    n_steps: int
+    g: float = G
+    rho0: float = RHO0
+    beta: tuple = BETA
+    slow: bool = True
+    seed: int = 0
+    r: int = 2
+
+
+def load_dt(name, default):
+    try:
+        with open(DT_TABLE) as f:
+            return float(json.load(f)[name]["dt"])
+    except (OSError, KeyError, ValueError):
+        return default
+
+
+def shelf_case(name, nx, ny, dc, seed, *, n_tiles=1, H_lo=10.0, H_hi=4000.0, W=20e3,
+               rough=0.05, corr=20e3, fine_H=250.0, bumps_per_tile=8, sigma=40e3,
+               amp=(0.5, 2.0), forcing=True, M=4, n_steps=200, dt=None, slow=True) -> Case:
+    """Continental-shelf case (configs 2 and 5; reduced sizes for parity tests).
+
+    H(x) = [H_lo + (H_hi - H_lo) S(x mod L_tile; W)] (1 + rough xi), xi a GRF
+    (readings Q20-Q22); fine = H > fine_H (Q21); Gaussian bumps (Q23);
+    tau = (0.1, 0) N m^-2 projected on n_e (Q19).
+    """
+    rng = np.random.default_rng(seed)
+    mesh = build_periodic_hex_mesh(nx, ny, dc)
+    Lt = mesh.Lx / n_tiles
+    S = periodic_step(np.mod(mesh.xCell, Lt), Lt, W)
+    H = H_lo + (H_hi - H_lo) * S
+    if rough:
+        xi = grf_periodic(nx, ny, dc, dc * np.sqrt(3) / 2, corr, rng)
+        H = H * (1.0 + rough * xi)
+    mesh.bottomDepth = H
+    mesh.fVertex = np.full(mesh.nVertices, F_PLANE)
+    centres, amps = [], []
+    for t in range(n_tiles):
+        cx = rng.uniform(t * Lt, (t + 1) * Lt, bumps_per_tile)
+        cy = rng.uniform(0, mesh.Ly, bumps_per_tile)
+        centres += list(zip(cx, cy))
+        amps += list(rng.uniform(amp[0], amp[1], bumps_per_tile))
+    eta = periodic_gaussians(mesh, centres, amps, sigma)
+    h0 = H + eta
+    u0 = np.zeros(mesh.nEdges)
+    tau_n = TAU_X * mesh.edgeNormal[:, 0] if forcing else np.zeros(mesh.nEdges)
+    fine = H > fine_H
+    if dt is None:
+        dt = load_dt(name, 0.5 * dc / np.sqrt(G * H_hi * 1.1))
+    return Case(name=name, mesh=mesh, h0=h0, u0=u0, fine_mask=fine, tau_n=tau_n, M=M,
+                dt=dt, n_steps=n_steps, seed=seed, slow=slow)
+
+
+def config1(seed=1, dt=None, nx=32, ny=32) -> Case:
+    """BASELINE config 1: 32x32 periodic hex, dc = 10 km, 100 m / 4000 m halves joined by a
+    tanh ramp (reading Q20: W = 25 km), fine = H > 2000 m, M = 4, 1 m bump (sigma 40 km)."""
+    rng = np.random.default_rng(seed)
+    dc = 10e3
+    mesh = build_periodic_hex_mesh(nx, ny, dc)
+    H = 100.0 + 3900.0 * periodic_step(mesh.xCell, mesh.Lx, 25e3)
+    mesh.bottomDepth = H
+    mesh.fVertex = np.full(mesh.nVertices, F_PLANE)
+    c = (rng.uniform(0, mesh.Lx), rng.uniform(0, mesh.Ly))
+    h0 = H + periodic_gaussians(mesh, [c], [1.0], 40e3)
+    if dt is None:
+        dt = load_dt("config1", 80.0)
+    return Case(name="config1", mesh=mesh, h0=h0, u0=np.zeros(mesh.nEdges), fine_mask=H > 2000.0,
+                tau_n=np.zeros(mesh.nEdges), M=4, dt=dt, n_steps=100, seed=seed)
+
+
+def config2(seed=2, dt=None) -> Case:
+    """BASELINE config 2: 512x512, dc = 2 km, shelf + 5 % roughness, 8 bumps, forcing, 200 steps."""
+    return shelf_case("config2", 512, 512, 2e3, seed, n_steps=200, dt=dt)
+
+
+def config5(seed=5, dt=None, nx=4096, ny=4096) -> Case:
+    """BASELINE config 5: 4096x4096, dc = 500 m, config 2's profile per 256-km x-tile (8 tiles)."""
+    n_tiles = max(1, int(round(nx * 500.0 / 256e3)))
+    return shelf_case("config5", nx, ny, 500.0, seed, n_tiles=n_tiles, n_steps=50, dt=dt)
+
+
+def small_shelf(seed=7, nx=48, ny=40, dc=2e3, **kw) -> Case:
+    """Reduced shelf case for parity tests: same recipe as config 2 on a small mesh."""
+    kw.setdefault("n_steps", 100)
+    return shelf_case("small_shelf", nx, ny, dc, seed, **kw)

@@ -1,0 +1,176 @@
+"""TRiSK spatial operators, literal fp64 numpy (oracle; test infrastructure only).
+
+Notation: h_i at cell centres, u_e normal velocity at edges
+(eq. semi_discrete_sys).  ``cells``/``edges`` arguments restrict the
+evaluation to an index subset (the LTS phases evaluate on region subsets); the
+result has the length of the subset.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def n_sign(mesh, cells, j):
+    """n_{e,i} for slot j of the given cells: +1 if the cell is cellsOnEdge[e][0].
+
+    P:L961: n_{e,i} in {1,-1} such that n_{e,i} n_e is the outward normal of i;
+    n_e points from cellsOnEdge[e][0] to cellsOnEdge[e][1] (SURVEY c.1).
+    """
+    e = mesh.edgesOnCell[cells, j]
+    return np.where(mesh.cellsOnEdge[e, 0] == cells, 1.0, -1.0)
+
+
+def edge_flux(mesh, U, H, edges):
+    """F_e = h_e u_e with h_e = 0.5 (h[c0] + h[c1]).
+
+    P:L962 ("F_e is the signed value of the thickness flux"); the edge-thickness
+    closure (centred mean) is the reading Q1 (SURVEY c.4).
+    """
+    c0 = mesh.cellsOnEdge[edges, 0]
+    c1 = mesh.cellsOnEdge[edges, 1]
+    h_e = 0.5 * (H[c0] + H[c1])
+    return h_e * U[edges]
+
+
+def thickness_tendency(mesh, U, H, cells):
+    """Psi_i(u, h) = -(1/A_i) sum_{e in E_i} n_{e,i} l_e F_e  (eq. trisk_thickness).
+
+    Evaluated as  -(sum_j n_{e_j,i} * l_{e_j} * F_{e_j}) / A_i,  sum sequential in
+    edgesOnCell slot order from +0.0.
+    """
+    cells = np.asarray(cells)
+    acc = np.zeros(cells.size)
+    nE = mesh.nEdgesOnCell[cells]
+    for j in range(mesh.maxEdges):
+        act = j < nE
+        if not np.any(act):
+            break
+        c = cells[act]
+        e = mesh.edgesOnCell[c, j]
+        F = edge_flux(mesh, U, H, e)
+        term = n_sign(mesh, c, j) * mesh.dvEdge[e] * F
+        acc[act] = acc[act] + term
+    return -acc / mesh.areaCell[cells]
+
+
+def fast_momentum(mesh, H, g, edges):
+    """Phi^fast_e = -g grad(h + z_b) . n_e  (eq. fast_terms).
+
+    Evaluated as  -g * ((h[c1] + z_b[c1]) - (h[c0] + z_b[c0])) / d_e  with
+    z_b = -bottomDepth and d_e = dcEdge (reading Q3, Q15: (h + z_b) per cell first,
+    then the difference; never fold -g grad z_b into a separate term).
+    """
+    c0 = mesh.cellsOnEdge[edges, 0]
+    c1 = mesh.cellsOnEdge[edges, 1]
+    zb = -mesh.bottomDepth
+    t1 = H[c1] + zb[c1]
+    t0 = H[c0] + zb[c0]
+    return -g * (t1 - t0) / mesh.dcEdge[edges]
+
+
+def relative_vorticity(mesh, U):
+    """zeta_v = (1/A_v) sum_{e in E_v} t_{e,v} d_e u_e on every vertex.
+
+    Circulation on the dual cell ("eta = k . curl u + f");
+    t_{e,v} = +1 if v = verticesOnEdge[e][1] (the +t_e side), else -1 (SURVEY c.1,
+    reading Q4).  Sum sequential in edgesOnVertex order.
+    """
+    acc = np.zeros(mesh.nVertices)
+    v = np.arange(mesh.nVertices)
+    for k in range(3):
+        e = mesh.edgesOnVertex[:, k]
+        s = np.where(mesh.verticesOnEdge[e, 1] == v, 1.0, -1.0)
+        acc = acc + s * mesh.dcEdge[e] * U[e]
+    return acc / mesh.areaTriangle
+
+
+def circulation(mesh, U):
+    """sum_{e in E_v} t_{e,v} d_e u_e (un-normalised; used by the Gamma diagnostic)."""
+    acc = np.zeros(mesh.nVertices)
+    v = np.arange(mesh.nVertices)
+    for k in range(3):
+        e = mesh.edgesOnVertex[:, k]
+        s = np.where(mesh.verticesOnEdge[e, 1] == v, 1.0, -1.0)
+        acc = acc + s * mesh.dcEdge[e] * U[e]
+    return acc
+
+
+def vertex_thickness(mesh, H):
+    """h_v = (1/A_v) sum_i kite_{v,i} h_i  (dual thickness by interpolation)."""
+    acc = np.zeros(mesh.nVertices)
+    for k in range(3):
+        acc = acc + mesh.kiteAreasOnVertex[:, k] * H[mesh.cellsOnVertex[:, k]]
+    return acc / mesh.areaTriangle
+
+
+def potential_vorticity(mesh, U, H):
+    """q_v = (zeta_v + f_v) / h_v  (q = eta / h)."""
+    return (relative_vorticity(mesh, U) + mesh.fVertex) / vertex_thickness(mesh, H)
+
+
+def perp_flux(mesh, F_all, edges):
+    """F_perp_e = M_e(F) = sum_j W_{e,j} F_{eoe_j}  (MPAS normalisation, Q6)."""
+    edges = np.asarray(edges)
+    acc = np.zeros(edges.size)
+    nE2 = mesh.nEdgesOnEdge[edges]
+    for j in range(mesh.maxEdges2):
+        act = j < nE2
+        if not np.any(act):
+            break
+        e = edges[act]
+        acc[act] = acc[act] + mesh.weightsOnEdge[e, j] * F_all[mesh.edgesOnEdge[e, j]]
+    return acc
+
+
+def kinetic_energy(mesh, U):
+    """K_i = (1/A_i) sum_{e in E_i} (l_e d_e / 4) u_e^2 on every cell.
+
+    P:L1213 ("K = |u|^2/2"); quadrature reading Q18.  Evaluated as
+    (sum_j 0.25 * l_e * d_e * u_e * u_e) / A_i, left to right.
+    """
+    acc = np.zeros(mesh.nCells)
+    nE = mesh.nEdgesOnCell
+    for j in range(mesh.maxEdges):
+        act = j < nE
+        if not np.any(act):
+            break
+        e = mesh.edgesOnCell[act, j]
+        acc[act] = acc[act] + 0.25 * mesh.dvEdge[e] * mesh.dcEdge[e] * U[e] * U[e]
+    return acc / mesh.areaCell
+
+
+def slow_momentum(mesh, U, H, tau_n, rho0):
+    """Phi^slow_e(u, h) on every edge: the non-gravity-wave momentum terms.
+
+    Split per P:L1548-1561 (the fast part is only -g grad(h + z_b)).  From
+    eq. nonlinear_swe: -(curl u + f k) x u - grad K, written in TRiSK form
+     as  q_hat_e F_perp_e - (K[c1] - K[c0]) / d_e   (sign reading Q5:
+    F_perp along +t_e, so the PV term enters with +), plus the wind-stress-like
+    forcing G_e = (tau . n_e) / (rho0 h_e) (reading Q19; config 2 and 5).
+    q_hat_e = 0.5 (q[v0] + q[v1]) (reading Q2).
+    Evaluated as  (q_hat * F_perp - (K1 - K0) / d_e) + G_e.
+    """
+    e = np.arange(mesh.nEdges)
+    F = edge_flux(mesh, U, H, e)
+    q = potential_vorticity(mesh, U, H)
+    v0 = mesh.verticesOnEdge[:, 0]
+    v1 = mesh.verticesOnEdge[:, 1]
+    q_hat = 0.5 * (q[v0] + q[v1])
+    Fperp = perp_flux(mesh, F, e)
+    K = kinetic_energy(mesh, U)
+    c0 = mesh.cellsOnEdge[:, 0]
+    c1 = mesh.cellsOnEdge[:, 1]
+    h_e = 0.5 * (H[c0] + H[c1])
+    G = tau_n / (rho0 * h_e)
+    return q_hat * Fperp - (K[c1] - K[c0]) / mesh.dcEdge + G
+
+
+def slow_tendency(mesh, U, H, phys):
+    """S_e = Phi^slow_e(u^n, h^n), frozen for the coarse step (Q17).
+
+    ``phys.slow`` False disables every slow term (gravity-wave model,
+    eq. grav_wave_model; "all the slow terms disabled").
+    """
+    if not phys.slow:
+        return np.zeros(mesh.nEdges)
+    return slow_momentum(mesh, U, H, phys.tau_n, phys.rho0)

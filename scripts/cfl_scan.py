@@ -1,0 +1,84 @@
+"""Delta-t selection by bisection on the ORACLE (SURVEY 8(c) reading Q12; the paper's own procedure
+"running the model at increasing time-steps until it becomes unstable").
+
+Calls only inputs/ and oracle/; writes configs/dt.json.  Predicate: 300 coarse steps, unstable if
+any value is non-finite or max|u| > 5 m/s.  Bracket [0.5, 1.0] x the step at which
+nu_loc = nu_max_FBRK = 3.8621532/sqrt(6).  The run uses dt = 0.9 x the largest stable step found.
+
+usage: python scripts/cfl_scan.py config1 [config2 config5]
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from inputs import configs                      # noqa: E402
+from oracle import diagnostics as dg            # noqa: E402
+from oracle import fbrk32, lts                  # noqa: E402
+
+NU_MAX_FBRK = 3.8621532 / np.sqrt(6.0)
+OUT = configs.DT_TABLE
+
+
+def stable(case, lab, dt, steps=300):
+    phys = fbrk32.Phys(g=case.g, beta=case.beta, slow=case.slow, tau_n=case.tau_n, rho0=case.rho0)
+    h, u = case.h0.copy(), case.u0.copy()
+    with np.errstate(all="ignore"):
+        for _ in range(steps):
+            h, u = lts.fblts_step(case.mesh, lab, h, u, dt, case.M, phys)
+            if not (np.all(np.isfinite(u)) and np.all(np.isfinite(h))) or np.max(np.abs(u)) > 5.0:
+                return False
+    return True
+
+
+def scan(name, case, iters=6):
+    lab = lts.label_regions(case.mesh, case.fine_mask)
+    nu1 = dg.rest_courant(case.mesh, lab, 1.0, case.M, case.g)
+    top = NU_MAX_FBRK / nu1
+    lo, hi = 0.5 * top, 1.0 * top
+    t0 = time.time()
+    if not stable(case, lab, lo):
+        raise RuntimeError(f"{name}: unstable at the bracket bottom {lo:.3f} s")
+    if stable(case, lab, hi):
+        lo = hi
+    else:
+        for _ in range(iters):
+            mid = 0.5 * (lo + hi)
+            if stable(case, lab, mid):
+                lo = mid
+            else:
+                hi = mid
+            print(f"  {name}: [{lo:.3f}, {hi:.3f}] s  ({time.time() - t0:.0f} s)", flush=True)
+    dt = 0.9 * lo
+    return {"dt": dt, "stable_dt": lo, "unstable_dt": hi, "nu_loc_limit": lo * nu1,
+            "nu_loc_run": dt * nu1, "bracket_top_dt": top, "predicate": "300 steps, finite, max|u| <= 5",
+            "M": case.M, "nCells": case.mesh.nCells}
+
+
+def main(names):
+    for name in names:
+        if name == "config1":
+            case = configs.config1(dt=1.0)
+        elif name == "config2":
+            case = configs.config2(dt=1.0)
+        elif name == "config5":
+            # proxy: one 256-km tile of config 5 (same dc, profile, roughness recipe, M) in x,
+            # 128 km in y; the full 4096^2 mesh is too large for 300 oracle steps per trial.
+            case = configs.shelf_case("config5_proxy", 512, 296, 500.0, 5, n_tiles=1, n_steps=50, dt=1.0)
+        else:
+            raise SystemExit(f"unknown config {name}")
+        res = scan(name, case)
+        if name == "config5":
+            res["proxy"] = "512x296 cells (one 256-km x-tile, dc = 500 m, seed 5)"
+        print(name, res, flush=True)
+        table = json.load(open(OUT)) if os.path.exists(OUT) else {}
+        table[name] = res
+        json.dump(table, open(OUT, "w"), indent=2, sort_keys=True)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["config1"])
