@@ -1,0 +1,179 @@
+/*
+ * fblts.h -- C ABI of libfblts.so, the B200 (sm_100a) hot path of FB-LTS
+ * (Lilly, Capodaglio, Engwirda, Higdon, Petersen, arXiv 2405.10505).
+ *
+ * What the library computes (PAPER.md line numbers, "P:Lnnn"):
+ *   one FB-LTS coarse step in split mode = the slow tendency frozen at t^n
+ *   (eq. splitting), Coarse Advancement on C u F^l,
+ *   Interface Prediction on IF-1 (eq. preds), M fine FB-RK(3,2)
+ *   subcycles on F (eq. fine_fbrk32) accumulating the interface
+ *   summands, and the Interface Correction (eq. if_correction).
+ *   The spatial operators are TRiSK on a Voronoi C-grid: Psi_i
+ *   (eq. trisk_thickness), Phi^fast = -g grad(h + z_b)
+ *   (eq. fast_terms), and the slow momentum terms
+ *   q_hat F_perp - grad K (+ wind-stress forcing) (eq. nonlinear_swe P:L257-273,
+ *   eq. trisk_vorticity).  FB weights default (0.531, 0.531, 0.313)
+ *   (P:L327-328).  The readings of ambiguous passages are listed in DESIGN.md.
+ *
+ * Conventions
+ *   - All indices are 0-based int32; all floating point is IEEE fp64.
+ *   - Orientation: n_e points from cellsOnEdge[e][0] to cellsOnEdge[e][1];
+ *     t_e = k x n_e; verticesOnEdge[e][1] lies on the +t_e side; edgesOnCell,
+ *     cellsOnVertex are counter-clockwise (Fig. trisk).
+ *   - Host arrays passed in are BORROWED for the duration of the call only; the
+ *     library copies what it needs.  All state I/O is in the caller's ORIGINAL
+ *     order; the library's region-major / space-filling-curve permutation is
+ *     internal.
+ *   - Device memory: the caller owns one workspace buffer (e.g. a torch uint8
+ *     CUDA tensor) that must outlive the context.  The library owns its CUDA
+ *     graphs, events, and (nranks > 1) its NCCL communicator, destroyed by
+ *     fblts_destroy.
+ *   - Streams: every enqueueing call works on cfg.stream (the caller's stream,
+ *     e.g. torch.cuda.current_stream().cuda_stream; NULL = legacy default).
+ *   - Errors: every int function returns 0 on success or a negative FBLTS_ERR_*
+ *     code; fblts_last_error() returns a message naming the field/index/phase.
+ *     fblts_step is asynchronous: device-side failures (h <= 0 or NaN) set a
+ *     device flag that the next synchronising call (fblts_sync, fblts_get_state,
+ *     fblts_diagnostics) reports as FBLTS_ERR_POSITIVITY.
+ *   - Call order: create -> upload_mesh -> set_regions -> workspace_size ->
+ *     bind_workspace -> set_state -> (set_forcing) -> step* -> get_state /
+ *     diagnostics -> destroy.  Out-of-order calls return FBLTS_ERR_ORDER.
+ *   - Determinism: identical inputs give bit-identical outputs.
+ */
+#ifndef FBLTS_H
+#define FBLTS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FBLTS_OK               0
+#define FBLTS_ERR_INVALID_ARG (-1)
+#define FBLTS_ERR_MESH        (-2)
+#define FBLTS_ERR_LABELS      (-3)
+#define FBLTS_ERR_STATE       (-4)
+#define FBLTS_ERR_CUDA        (-5)
+#define FBLTS_ERR_NCCL        (-6)
+#define FBLTS_ERR_POSITIVITY  (-7)
+#define FBLTS_ERR_ORDER       (-8)
+
+/* Region codes returned by fblts_get_labels (cells and edges):
+ *   0 = C^int, 1 = C^IF-2, 2 = C^IF-1, 2+l (l = 1..5) = F^l \ F^(l-1), 8 = F \ F^5.
+ * Cells: IF-1 = coarse cells 1..r hops from F, IF-2 = r+1..2r hops, int = farther;
+ * F^l = fine cells within l*r hops of C.  Edges take the region
+ * "closest to the fine region"; F^l_E = edges touching F^l. */
+#define FBLTS_REGION_INT 0
+#define FBLTS_REGION_IF2 1
+#define FBLTS_REGION_IF1 2
+#define FBLTS_REGION_F1  3
+#define FBLTS_REGION_FDEEP 8
+
+typedef struct fblts_ctx fblts_ctx;
+
+/* TRiSK mesh, host arrays (MPAS field names). */
+typedef struct {
+    int32_t nCells, nEdges, nVertices;
+    int32_t maxEdges;                 /* max edges per cell (row stride of edgesOnCell) */
+    int32_t maxEdges2;                /* row stride of edgesOnEdge / weightsOnEdge */
+    const int32_t *nEdgesOnCell;      /* [nCells] */
+    const int32_t *edgesOnCell;       /* [nCells*maxEdges], CCW; unused slots ignored */
+    const int32_t *cellsOnEdge;       /* [nEdges*2] (c0, c1): n_e points c0 -> c1 */
+    const int32_t *verticesOnEdge;    /* [nEdges*2] (v0, v1): v1 on the +t_e side */
+    const int32_t *nEdgesOnEdge;      /* [nEdges] */
+    const int32_t *edgesOnEdge;       /* [nEdges*maxEdges2] */
+    const double  *weightsOnEdge;     /* [nEdges*maxEdges2]: F_perp_e = sum_j W[e][j] F[eoe[e][j]] */
+    const int32_t *edgesOnVertex;     /* [nVertices*3] */
+    const int32_t *cellsOnVertex;     /* [nVertices*3], CCW */
+    const double  *kiteAreasOnVertex; /* [nVertices*3], aligned with cellsOnVertex */
+    const double  *areaCell;          /* [nCells]    A_i  (m^2) */
+    const double  *areaTriangle;      /* [nVertices] A_v  (m^2) */
+    const double  *dvEdge;            /* [nEdges]    l_e: primal edge length (m) */
+    const double  *dcEdge;            /* [nEdges]    d_e: cell-centre distance (m) */
+    const double  *fVertex;           /* [nVertices] Coriolis parameter (s^-1) */
+    const double  *bottomDepth;       /* [nCells]    H > 0; z_b = -H (m) */
+    const double  *xCell, *yCell, *zCell;  /* [nCells] positions, used only for the SFC order */
+} fblts_mesh;
+
+typedef struct {
+    double  dt;          /* coarse step (s) */
+    double  g;           /* gravity (m s^-2) */
+    double  beta[3];     /* FB weights */
+    double  rho0;        /* reference density for the wind-stress forcing (kg m^-3) */
+    int32_t M;           /* fine subcycles per coarse step (>= 1) */
+    int32_t r;           /* stencil radius for the region widths (2) */
+    int32_t slow;        /* 1: slow terms on (split model); 0: gravity-wave model */
+    int32_t device;      /* CUDA device ordinal */
+    void   *stream;      /* cudaStream_t of the caller (NULL = legacy default stream) */
+    int32_t rank;        /* this process's rank (0 for single GPU) */
+    int32_t nranks;      /* number of ranks (1 for single GPU) */
+    const void *nccl_id; /* 128-byte ncclUniqueId shared by all ranks, NULL if nranks == 1 */
+} fblts_config;
+
+/* Create a context.  *out receives the handle (NULL on failure).
+ * Errors: INVALID_ARG (M < 1, dt <= 0, r < 1, bad rank/nranks), CUDA, NCCL. */
+int fblts_create(fblts_ctx **out, const fblts_config *cfg);
+
+/* Copy and validate the mesh.  Checks index ranges, that every edge appears in
+ * edgesOnCell of exactly its two cellsOnEdge entries, positive lengths/areas,
+ * nEdgesOnCell <= maxEdges; message names field and index.  Errors: MESH, ORDER. */
+int fblts_upload_mesh(fblts_ctx *ctx, const fblts_mesh *m);
+
+/* Label the LTS regions from a fine-cell mask [nCells] (1 = fine), validate the
+ * stencil assumption, build the region-major + SFC permutation and
+ * (nranks > 1) the partition and halo lists.  Errors: LABELS, ORDER. */
+int fblts_set_regions(fblts_ctx *ctx, const uint8_t *fine_mask);
+
+/* Region codes in ORIGINAL order (see FBLTS_REGION_*); either pointer may be NULL. */
+int fblts_get_labels(fblts_ctx *ctx, int8_t *cell_region, int8_t *edge_region);
+
+/* Local entity counts: out[0..7] = nCells, nEdges, nVertices, |int|, |IF-2|, |IF-1|,
+ * |F^1|..  (out must hold 24 int64): cells per code 0..8 at out[3..11], edges per
+ * code 0..8 at out[12..20], out[21] = owned cells, out[22] = owned edges, out[23] = reserved. */
+int fblts_get_counts(fblts_ctx *ctx, int64_t *out);
+
+/* Bytes of device workspace needed after set_regions. */
+int fblts_workspace_size(fblts_ctx *ctx, size_t *bytes);
+
+/* Bind a caller-owned device buffer of >= workspace_size bytes (256-B aligned)
+ * and upload the permuted mesh into it (synchronous on cfg.stream). */
+int fblts_bind_workspace(fblts_ctx *ctx, void *device_ptr, size_t bytes);
+
+/* Per-edge wind-stress projection tau . n_e [nEdges] (N m^-2), original order;
+ * NULL = no forcing.  The slow term adds G_e = tau_n / (rho0 h_e^n) (reading Q19). */
+int fblts_set_forcing(fblts_ctx *ctx, const double *tau_n);
+
+/* Initial state, HOST arrays in original order: h [nCells] (m), u [nEdges] (m/s), t (s).
+ * Errors: STATE (h <= 0 or non-finite at index i), ORDER. */
+int fblts_set_state(fblts_ctx *ctx, const double *h, const double *u, double t);
+
+/* Enqueue n_coarse coarse steps on cfg.stream (asynchronous, CUDA-graph replay). */
+int fblts_step(fblts_ctx *ctx, int32_t n_coarse);
+
+/* Synchronise cfg.stream and report asynchronous device errors (POSITIVITY, CUDA). */
+int fblts_sync(fblts_ctx *ctx);
+
+/* Read back the state into HOST arrays in original order (synchronises). */
+int fblts_get_state(fblts_ctx *ctx, double *h, double *u, double *t);
+
+/* out[4] = { total mass sum A_i h_i, total absolute vorticity sum_v (circulation_v + A_v f_v),
+ *            min h, max Courant number (|u|+sqrt(g h_e)) dt_e / d_e } (Thms 1-2, eq. cfl).
+ * Deterministic double-double reductions (synchronises). */
+int fblts_diagnostics(fblts_ctx *ctx, double out[4]);
+
+/* Instrumented replay for the roofline: runs n_coarse steps WITHOUT the graph, with
+ * CUDA events around every launch on cfg.stream; ms[k] = total device ms of kernel
+ * kind k, launches[k] = launch count, for k < FBLTS_NUM_KERNELS.  Advances the state. */
+#define FBLTS_NUM_KERNELS 11
+int fblts_profile(fblts_ctx *ctx, int32_t n_coarse, double *ms, int64_t *launches);
+const char *fblts_kernel_name(int32_t kind);
+
+const char *fblts_last_error(const fblts_ctx *ctx);
+void fblts_destroy(fblts_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FBLTS_H */

@@ -156,6 +156,11 @@ def config5(seed=5, dt=None, nx=4096, ny=4096) -> Case:
 
 
 def small_shelf(seed=7, nx=48, ny=40, dc=2e3, **kw) -> Case:
-    """Reduced shelf case for parity tests: same recipe as config 2 on a small mesh."""
+    """Reduced shelf case for parity tests: config 2's recipe with every length scale (ramp width,
+    roughness correlation length, bump width) shrunk by L_x / 1024 km so the regions keep their shape."""
+    s = nx * dc / 1024e3
     kw.setdefault("n_steps", 100)
+    kw.setdefault("W", 20e3 * s)
+    kw.setdefault("corr", 20e3 * s)
+    kw.setdefault("sigma", 40e3 * s)
     return shelf_case("small_shelf", nx, ny, dc, seed, **kw)

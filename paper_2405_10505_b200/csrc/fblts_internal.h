@@ -1,0 +1,126 @@
+// fblts_internal.h -- device-side data layout of libfblts (not part of the C ABI).
+//
+// Layout in HBM: every entity family is renumbered
+// region-major then by space-filling curve, so each phase extent of FB-LTS is one
+// contiguous index range:
+//   cells : [ C^int | C^IF-2 | C^IF-1 | F^1 | F^2\F^1 | ... | F^5\F^4 | F\F^5 ]
+//   edges : [ int_E | IF-2_E | IF-1_E | F^1_E | ... | F_E\F^5_E ]
+//   vertices: SFC order.
+// Per-cell slot tables are stored slot-major ([slot][strideC]) so that lane i of
+// a warp reading slot j of cell i touches consecutive words.  edgesOnCell is
+// sign-encoded: e if the cell is cellsOnEdge[e][0] (n_{e,i} = +1), ~e otherwise;
+// edgesOnVertex likewise: e if the vertex is verticesOnEdge[e][1] (t_{e,v} = +1).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fblts {
+
+enum KernelKind {
+    K_SLOW_PRE = 0, K_SLOW_EDGE, K_COARSE_S1, K_COARSE_S2, K_COARSE_S3, K_COARSE_VEL,
+    K_FINE_S1, K_FINE_S2, K_FINE_S3, K_FINE_VEL, K_CORRECT, K_NUM
+};
+
+// Region boundaries of one region-major block: [0,if2) int, [if2,if1) IF-2,
+// [if1,f) IF-1, [f,end) fine; fl[l] = end of F^l (l = 1..5), fl[0] = f.
+struct Bounds {
+    int32_t if2, if1, f, end;
+    int32_t fl[6];
+};
+
+struct DevMesh {
+    int32_t nC, nE, nV;               // local entity counts
+    int32_t strideC, strideE, strideV; // padded slot strides
+    int32_t maxE, maxE2;
+    const int32_t *__restrict__ nEoC;  // [nC]
+    const int32_t *__restrict__ eoc;   // [maxE][strideC]  sign-encoded
+    const int32_t *__restrict__ coc;   // [maxE][strideC]
+    const double *__restrict__ areaCell;  // [nC]
+    const double *__restrict__ zb;        // [nC]  z_b = -bottomDepth
+    const int2 *__restrict__ coe;      // [nE] (c0, c1)
+    const int2 *__restrict__ voe;      // [nE] (v0, v1)
+    const double *__restrict__ dv;     // [nE] l_e
+    const double *__restrict__ dc;     // [nE] d_e
+    const int32_t *__restrict__ nEoE;  // [nE]
+    const int32_t *__restrict__ eoe;   // [maxE2][strideE]
+    const double *__restrict__ W;      // [maxE2][strideE]
+    const double *__restrict__ tau;    // [nE] tau . n_e
+    const int32_t *__restrict__ eov;   // [3][strideV] sign-encoded
+    const int32_t *__restrict__ cov;   // [3][strideV]
+    const double *__restrict__ kite;   // [3][strideV]
+    const double *__restrict__ areaTri; // [nV]
+    const double *__restrict__ fV;     // [nV]
+    Bounds cb, eb;                     // cell / edge region bounds
+};
+
+// Device error record (positivity / NaN), first failure wins.
+struct DevError {
+    int32_t flag;    // 0 = ok, 1 = positivity
+    int32_t kind;    // KernelKind
+    int32_t k;       // fine subcycle (or -1)
+    int32_t index;   // local (permuted) cell index
+    double value;
+};
+
+// Scalars of one coarse step, computed once on the host in double exactly as
+// the oracle does (SURVEY c.1 canonical constants).
+struct StepConst {
+    double g, rho0;
+    double b1, b2, b3, omb1, omb2, om2b3;
+    double c1, c2, c3;        // dt/3, dt/2, dt
+    double c1f, c2f, c3f;     // dt/(3M), dt/(2M), dt/M
+    int32_t M;
+};
+
+// Prediction coefficients for subcycle k (eq. preds): a = k/M, oma = 1 - a,
+// a1 = (k+1)/M, oma1 = 1 - a1, b = 1/M, c = 1 - (k+1)/M.
+struct PredConst {
+    double a, oma, a1, oma1, b, c;
+};
+
+// Device pointers of the state and scratch arrays (all in the caller's workspace).
+struct DevState {
+    double *hN, *hNew, *h1, *h2, *hT;   // cells
+    double *uN, *uNew, *uT, *S, *F;     // edges
+    double *q;                          // vertices
+    double *K;                          // cells
+    double *accH, *accU;                // IF cells [cb.if2, cb.f), IF edges [eb.if2, eb.f)
+    double *stage;                      // staging for set/get_state (max(nC, nE) doubles)
+    int32_t *cellOld, *edgeOld;         // new -> old permutation (device)
+    double *diag;                       // reduction scratch
+    DevError *err;
+};
+
+// Kernel launchers (kernels.cu).  All enqueue on `s`.
+void launch_slow_pre(const DevMesh &m, const DevState &st, const double *h, const double *u, cudaStream_t s);
+void launch_slow_edge(const DevMesh &m, const DevState &st, const double *h, const StepConst &sc, cudaStream_t s);
+void launch_coarse_s1(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
+                      const StepConst &sc, cudaStream_t s);
+void launch_coarse_s2(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
+                      const StepConst &sc, cudaStream_t s);
+void launch_coarse_s3(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
+                      double *hNew, const StepConst &sc, cudaStream_t s);
+void launch_coarse_vel(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
+                       const double *hNew, double *uNew, const StepConst &sc, cudaStream_t s);
+void launch_fine_s1(const DevMesh &m, const DevState &st, const double *hN, const double *hNew,
+                    const double *hk, const double *uk, const StepConst &sc, const PredConst &pc,
+                    int k, cudaStream_t s);
+void launch_fine_s2(const DevMesh &m, const DevState &st, const double *hN, const double *hNew,
+                    const double *hk, const double *uk, const StepConst &sc, const PredConst &pc,
+                    int k, cudaStream_t s);
+void launch_fine_s3(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
+                    const double *hNew, const double *hk, const double *uk, double *hnext,
+                    const StepConst &sc, const PredConst &pc, int k, cudaStream_t s);
+void launch_fine_vel(const DevMesh &m, const DevState &st, const double *hN, const double *hNew,
+                     const double *hk, const double *hnext, const double *uk, double *unext,
+                     const StepConst &sc, const PredConst &pc, int k, cudaStream_t s);
+void launch_correct(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
+                    double *hNew, double *uNew, const StepConst &sc, cudaStream_t s);
+void launch_permute_in(const int32_t *old_of_new, const double *src, double *dst, int n, cudaStream_t s);
+void launch_permute_out(const int32_t *old_of_new, const double *src, double *dst, int n, cudaStream_t s);
+void launch_check_state(const double *h, int n, DevError *err, cudaStream_t s);
+// diagnostics: writes out[4] (device) = mass, Gamma, min h, max nu
+void launch_diagnostics(const DevMesh &m, const DevState &st, const double *h, const double *u,
+                        const StepConst &sc, double *out_dev, cudaStream_t s);
+
+}  // namespace fblts

@@ -1,0 +1,601 @@
+// kernels.cu -- sm_100a fp64 kernels of the FB-LTS hot path (split mode).
+//
+// Every kernel evaluates the paper's formulas in the canonical order listed in
+// DESIGN.md ("Canonical arithmetic"): sums sequential in slot order from +0.0,
+// left-to-right products, IEEE division, no FMA contraction (--fmad=false), so
+// the results agree bit for bit with a literal implementation of the paper.
+//
+// Fusion: in split mode Phi^fast_e depends only on cell
+// data, so the stage-s velocity  u_bar_{s-1,e} = u_base,e + c_{s-1} (Phi^fast_e(h_FB) + S_e)
+// is recomputed inside the stage-s cell kernel from the two cells of e instead
+// of being stored; the FB averages h*, h**, h*** and the IF-1 predictions
+// (eq. preds) are likewise recomputed from the stored stage
+// thicknesses.  Velocity is written once per (sub)step.
+#include "fblts_internal.h"
+
+namespace fblts {
+
+constexpr int TPB = 256;
+
+static inline unsigned nblocks(long n) { return (unsigned)((n + TPB - 1) / TPB); }
+
+// cell class: 2 = F, 1 = IF-1, 0 = other coarse (IF-2 or int)
+__device__ __forceinline__ int ccls(const Bounds &b, int x) { return x >= b.f ? 2 : (x >= b.if1 ? 1 : 0); }
+// edge class: 3 = F_E, 2 = IF-1_E, 1 = IF-2_E, 0 = int_E
+__device__ __forceinline__ int ecls(const Bounds &b, int e) {
+    return e >= b.f ? 3 : (e >= b.if1 ? 2 : (e >= b.if2 ? 1 : 0));
+}
+
+__device__ __forceinline__ void report(DevError *err, int kind, int k, int i, double v) {
+    if (atomicCAS(&err->flag, 0, 1) == 0) {
+        err->kind = kind;
+        err->k = k;
+        err->index = i;
+        err->value = v;
+    }
+}
+
+// Phi^fast_e = -g ((h_c1 + z_b,c1) - (h_c0 + z_b,c0)) / d_e   (eq. fast_terms; Q15)
+__device__ __forceinline__ double phi_fast(double g, double hs0, double zb0, double hs1, double zb1, double dc) {
+    const double t1 = hs1 + zb1;
+    const double t0 = hs0 + zb0;
+    return -g * (t1 - t0) / dc;
+}
+
+__device__ __forceinline__ int decode(int es, bool &pos) {
+    pos = es >= 0;
+    return pos ? es : ~es;
+}
+
+// ---------------------------------------------------------------- slow terms
+// One launch, three index spaces: vertices (q_v), cells (K_i), edges (F_e).
+// q_v = (zeta_v + f_v) / h_v,  zeta_v = (sum t d u)/A_v,  h_v = (sum kite h)/A_v
+// K_i = (sum 0.25 l d u u) / A_i   (Q18);   F_e = (0.5 (h_c0 + h_c1)) u_e   (Q1)
+__global__ void __launch_bounds__(TPB) k_slow_pre(DevMesh m, const double *__restrict__ h,
+                                                  const double *__restrict__ u, double *__restrict__ q,
+                                                  double *__restrict__ K, double *__restrict__ F,
+                                                  unsigned nbV, unsigned nbC) {
+    const unsigned b = blockIdx.x;
+    if (b < nbV) {
+        const int v = b * TPB + threadIdx.x;
+        if (v >= m.nV) return;
+        double circ = 0.0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            bool pos;
+            const int e = decode(m.eov[k * m.strideV + v], pos);
+            const double t = m.dc[e] * u[e];
+            circ = circ + (pos ? t : -t);
+        }
+        const double A = m.areaTri[v];
+        const double zeta = circ / A;
+        double hv = 0.0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) hv = hv + m.kite[k * m.strideV + v] * h[m.cov[k * m.strideV + v]];
+        hv = hv / A;
+        q[v] = (zeta + m.fV[v]) / hv;
+    } else if (b < nbV + nbC) {
+        const int i = (b - nbV) * TPB + threadIdx.x;
+        if (i >= m.nC) return;
+        const int n = m.nEoC[i];
+        double acc = 0.0;
+        for (int j = 0; j < n; ++j) {
+            bool pos;
+            const int e = decode(m.eoc[j * m.strideC + i], pos);
+            const double ue = u[e];
+            acc = acc + 0.25 * m.dv[e] * m.dc[e] * ue * ue;
+        }
+        K[i] = acc / m.areaCell[i];
+    } else {
+        const int e = (b - nbV - nbC) * TPB + threadIdx.x;
+        if (e >= m.nE) return;
+        const int2 c = m.coe[e];
+        F[e] = (0.5 * (h[c.x] + h[c.y])) * u[e];
+    }
+}
+
+// S_e = q_hat_e F_perp_e - (K_c1 - K_c0) / d_e + G_e   (Q2, Q5, Q19)
+__global__ void __launch_bounds__(TPB) k_slow_edge(DevMesh m, const double *__restrict__ h,
+                                                   const double *__restrict__ q, const double *__restrict__ K,
+                                                   const double *__restrict__ F, double *__restrict__ S,
+                                                   double rho0) {
+    const int e = blockIdx.x * TPB + threadIdx.x;
+    if (e >= m.nE) return;
+    const int n = m.nEoE[e];
+    double fp = 0.0;
+    for (int j = 0; j < n; ++j) fp = fp + m.W[j * m.strideE + e] * F[m.eoe[j * m.strideE + e]];
+    const int2 v = m.voe[e];
+    const int2 c = m.coe[e];
+    const double qh = 0.5 * (q[v.x] + q[v.y]);
+    const double he = 0.5 * (h[c.x] + h[c.y]);
+    const double G = m.tau[e] / (rho0 * he);
+    S[e] = qh * fp - (K[c.y] - K[c.x]) / m.dc[e] + G;
+}
+
+// ---------------------------------------------------------------- coarse stages
+// Stage 1 (eq. if_h_s1 / coarse_h_s1): h1 = h^n + dt/3 Psi(u^n, h^n) on C u F^5.
+// Stage 2 (eq. if_h_s2 / coarse_h_s2): h2 = h^n + dt/2 Psi(u1, h1) on C u F^3,
+//   u1_e = u^n_e + dt/3 (Phi^fast_e(h*) + S_e), h* = b1 h1 + (1-b1) h^n.
+// Stage 3 (eq. if_h_s3 / coarse_h_s3): h3 = h^n + dt Psi(u2, h2) on C u F^1,
+//   u2_e = u^n_e + dt/2 (Phi^fast_e(h**) + S_e), h** = b2 h2 + (1-b2) h^n.
+template <int STAGE>
+__global__ void __launch_bounds__(TPB) k_coarse_stage(DevMesh m, const double *__restrict__ hN,
+                                                      const double *__restrict__ hprev,
+                                                      const double *__restrict__ uN,
+                                                      const double *__restrict__ S, double *__restrict__ out,
+                                                      StepConst sc, int end, DevError *err) {
+    const int i = blockIdx.x * TPB + threadIdx.x;
+    if (i >= end) return;
+    const double cu = STAGE == 2 ? sc.c1 : sc.c2;        // c_{s-1} of the velocity
+    const double ch = STAGE == 1 ? sc.c1 : (STAGE == 2 ? sc.c2 : sc.c3);
+    const double bb = STAGE == 2 ? sc.b1 : sc.b2;
+    const double omb = STAGE == 2 ? sc.omb1 : sc.omb2;
+    const double hNi = hN[i];
+    const double Hi = STAGE == 1 ? hNi : hprev[i];
+    const double HSi = STAGE == 1 ? 0.0 : bb * Hi + omb * hNi;
+    const double zbi = STAGE == 1 ? 0.0 : m.zb[i];
+    const int n = m.nEoC[i];
+    double acc = 0.0;
+    for (int j = 0; j < n; ++j) {
+        bool pos;
+        const int e = decode(m.eoc[j * m.strideC + i], pos);
+        const int nb = m.coc[j * m.strideC + i];
+        double ue, Hn;
+        if (STAGE == 1) {
+            Hn = hN[nb];
+            ue = uN[e];
+        } else {
+            Hn = hprev[nb];
+            const double HSn = bb * Hn + omb * hN[nb];
+            const double zbn = m.zb[nb];
+            const double phi = pos ? phi_fast(sc.g, HSi, zbi, HSn, zbn, m.dc[e])
+                                   : phi_fast(sc.g, HSn, zbn, HSi, zbi, m.dc[e]);
+            ue = uN[e] + cu * (phi + S[e]);
+        }
+        const double Fe = (0.5 * (Hi + Hn)) * ue;
+        const double t = m.dv[e] * Fe;
+        acc = acc + (pos ? t : -t);
+    }
+    const double psi = -acc / m.areaCell[i];
+    const double v = hNi + ch * psi;
+    out[i] = v;
+    if (!(v > 0.0)) report(err, STAGE == 1 ? K_COARSE_S1 : (STAGE == 2 ? K_COARSE_S2 : K_COARSE_S3), -1, i, v);
+}
+
+// coarse FB averages (tilde / bar data)
+__device__ __forceinline__ double hs2c(const StepConst &sc, const double *h2, const double *hN, int x) {
+    return sc.b2 * h2[x] + sc.omb2 * hN[x];
+}
+__device__ __forceinline__ double hs3c(const StepConst &sc, const double *h3, const double *h2, const double *hN,
+                                       int x) {
+    return sc.b3 * h3[x] + sc.om2b3 * h2[x] + sc.b3 * hN[x];
+}
+
+// Velocity stage 3 on C^int_E: u^{n+1} = u^n + dt (Phi^fast(h***) + S).
+// IF-1_E tilde u^{n+1} is never stored: the fine phase recomputes it (Q10).
+__global__ void __launch_bounds__(TPB) k_coarse_vel(DevMesh m, const double *__restrict__ hN,
+                                                    const double *__restrict__ h2,
+                                                    const double *__restrict__ h3, const double *__restrict__ uN,
+                                                    const double *__restrict__ S, double *__restrict__ uNew,
+                                                    StepConst sc, int end) {
+    const int e = blockIdx.x * TPB + threadIdx.x;
+    if (e >= end) return;
+    const int2 c = m.coe[e];
+    const double phi = phi_fast(sc.g, hs3c(sc, h3, h2, hN, c.x), m.zb[c.x], hs3c(sc, h3, h2, hN, c.y), m.zb[c.y],
+                                m.dc[e]);
+    uNew[e] = uN[e] + sc.c3 * (phi + S[e]);
+}
+
+// ---------------------------------------------------------------- fine subcycles
+// Views (reading Q11): F -> fine data, IF-1 -> predicted (eq. preds,
+// eq. hstar_preds), IF-2 / int -> coarse tilde / bar data.
+struct FineArrays {
+    const double *hN, *h1, *h2, *h3, *hk;   // h3 = coarse stage-3 output (hNew before the correction)
+};
+
+__device__ __forceinline__ double pred_level(const PredConst &p, const FineArrays &a, int x) {
+    return p.a * a.h3[x] + p.oma * a.hN[x];                     // subeqn pred_old, level k
+}
+__device__ __forceinline__ double pred_level1(const PredConst &p, const FineArrays &a, int x) {
+    return p.a1 * a.h3[x] + p.oma1 * a.hN[x];                   // level k+1 (k = M extra)
+}
+__device__ __forceinline__ double pred_stage(const PredConst &p, const double *h3, const double *hs,
+                                             const double *hN, int x) {
+    return p.a * h3[x] + p.b * hs[x] + p.c * hN[x];              // subeqn pred_s1 / pred_s2
+}
+
+// Fine stage 1 (subeqn fine_s1): h_bar^{n,k+1/3} = h^{n,k} + dt/(3M) Psi(u^{n,k}, h^{n,k}) on F.
+__global__ void __launch_bounds__(TPB) k_fine_s1(DevMesh m, FineArrays a, const double *__restrict__ uk,
+                                                 double *__restrict__ out, StepConst sc, PredConst p, int k,
+                                                 DevError *err) {
+    const int i = m.cb.f + blockIdx.x * TPB + threadIdx.x;
+    if (i >= m.cb.end) return;
+    const double Hi = a.hk[i];
+    const int n = m.nEoC[i];
+    double acc = 0.0;
+    for (int j = 0; j < n; ++j) {
+        bool pos;
+        const int e = decode(m.eoc[j * m.strideC + i], pos);
+        const int nb = m.coc[j * m.strideC + i];
+        const int cl = ccls(m.cb, nb);
+        const double Hn = cl == 2 ? a.hk[nb] : (cl == 1 ? pred_level(p, a, nb) : a.hN[nb]);
+        const double Fe = (0.5 * (Hi + Hn)) * uk[e];
+        const double t = m.dv[e] * Fe;
+        acc = acc + (pos ? t : -t);
+    }
+    const double psi = -acc / m.areaCell[i];
+    const double v = Hi + sc.c1f * psi;
+    out[i] = v;
+    if (!(v > 0.0)) report(err, K_FINE_S1, k, i, v);
+}
+
+// view (H1, HS1) for fine stage 2
+__device__ __forceinline__ void view1(const Bounds &b, const StepConst &sc, const PredConst &p, const FineArrays &a,
+                                      int x, double &H, double &HS) {
+    const int cl = ccls(b, x);
+    if (cl == 2) {
+        H = a.h1[x];
+        HS = sc.b1 * H + sc.omb1 * a.hk[x];
+    } else if (cl == 1) {
+        const double hP0 = pred_level(p, a, x);
+        H = pred_stage(p, a.h3, a.h1, a.hN, x);
+        HS = sc.b1 * H + sc.omb1 * hP0;
+    } else {
+        H = a.h1[x];
+        HS = sc.b1 * H + sc.omb1 * a.hN[x];
+    }
+}
+
+// Fine stage 2 (subeqn fine_s2): h_bar^{n,k+1/2} = h^{n,k} + dt/(2M) Psi(u_bar^{n,k+1/3}, h_bar^{n,k+1/3}),
+// u_bar^{n,k+1/3}_e = u^{n,k}_e + dt/(3M) (Phi^fast_e(h^{*,k}) + S_e) recomputed per edge.
+__global__ void __launch_bounds__(TPB) k_fine_s2(DevMesh m, FineArrays a, const double *__restrict__ uk,
+                                                 const double *__restrict__ S, double *__restrict__ out,
+                                                 StepConst sc, PredConst p, int k, DevError *err) {
+    const int i = m.cb.f + blockIdx.x * TPB + threadIdx.x;
+    if (i >= m.cb.end) return;
+    double Hi, HSi;
+    view1(m.cb, sc, p, a, i, Hi, HSi);
+    const double zbi = m.zb[i];
+    const int n = m.nEoC[i];
+    double acc = 0.0;
+    for (int j = 0; j < n; ++j) {
+        bool pos;
+        const int e = decode(m.eoc[j * m.strideC + i], pos);
+        const int nb = m.coc[j * m.strideC + i];
+        double Hn, HSn;
+        view1(m.cb, sc, p, a, nb, Hn, HSn);
+        const double zbn = m.zb[nb];
+        const double phi = pos ? phi_fast(sc.g, HSi, zbi, HSn, zbn, m.dc[e])
+                               : phi_fast(sc.g, HSn, zbn, HSi, zbi, m.dc[e]);
+        const double ue = uk[e] + sc.c1f * (phi + S[e]);
+        const double Fe = (0.5 * (Hi + Hn)) * ue;
+        const double t = m.dv[e] * Fe;
+        acc = acc + (pos ? t : -t);
+    }
+    const double psi = -acc / m.areaCell[i];
+    const double v = a.hk[i] + sc.c2f * psi;
+    out[i] = v;
+    if (!(v > 0.0)) report(err, K_FINE_S2, k, i, v);
+}
+
+// view (H2, HS2) for fine stage 3 / the correction summand
+__device__ __forceinline__ void view2(const Bounds &b, const StepConst &sc, const PredConst &p, const FineArrays &a,
+                                      int x, double &H, double &HS) {
+    const int cl = ccls(b, x);
+    if (cl == 2) {
+        H = a.h2[x];
+        HS = sc.b2 * H + sc.omb2 * a.hk[x];
+    } else if (cl == 1) {
+        const double hP0 = pred_level(p, a, x);
+        H = pred_stage(p, a.h3, a.h2, a.hN, x);
+        HS = sc.b2 * H + sc.omb2 * hP0;
+    } else {
+        H = a.h2[x];
+        HS = sc.b2 * H + sc.omb2 * a.hN[x];
+    }
+}
+
+// Fine stage 3 on F (subeqn fine_s3) fused with the correction summand on IF-1 u IF-2
+// (eq. if_correction, "accumulated during the fine advancement step"):
+//   F:      h^{n,k+1} = h^{n,k} + dt/M Psi(u_bar^{n,k+1/2}, h_bar^{n,k+1/2})
+//   IF:     accH += Psi(u_bar^{n,k+1/2}, h_bar^{n,k+1/2})          (views, reading Q11/Q14)
+// Edge velocity u_bar^{n,k+1/2} by edge region: F_E -> u^{n,k} + dt/(2M)(Phi^fast(h^{**,k}) + S);
+// IF-1_E -> predicted (k/M) u~^{n+1} + (1/M) u~^{n+1/2} + (1-(k+1)/M) u^n with the tilde data
+// recomputed from the coarse thicknesses; IF-2_E / int_E -> coarse u~^{n+1/2}.
+__global__ void __launch_bounds__(TPB) k_fine_s3(DevMesh m, FineArrays a, const double *__restrict__ uN,
+                                                 const double *__restrict__ uk, const double *__restrict__ S,
+                                                 double *__restrict__ hnext, double *__restrict__ accH,
+                                                 StepConst sc, PredConst p, int k, DevError *err) {
+    const int i = m.cb.if2 + blockIdx.x * TPB + threadIdx.x;
+    if (i >= m.cb.end) return;
+    double Hi, HSi;
+    view2(m.cb, sc, p, a, i, Hi, HSi);
+    const double zbi = m.zb[i];
+    const int n = m.nEoC[i];
+    double acc = 0.0;
+    for (int j = 0; j < n; ++j) {
+        bool pos;
+        const int e = decode(m.eoc[j * m.strideC + i], pos);
+        const int nb = m.coc[j * m.strideC + i];
+        double Hn, HSn;
+        view2(m.cb, sc, p, a, nb, Hn, HSn);
+        const double zbn = m.zb[nb];
+        const int c0 = pos ? i : nb, c1 = pos ? nb : i;
+        const int ec = ecls(m.eb, e);
+        double ue;
+        if (ec == 3) {
+            const double phi = pos ? phi_fast(sc.g, HSi, zbi, HSn, zbn, m.dc[e])
+                                   : phi_fast(sc.g, HSn, zbn, HSi, zbi, m.dc[e]);
+            ue = uk[e] + sc.c2f * (phi + S[e]);
+        } else {
+            const double phi2 = phi_fast(sc.g, hs2c(sc, a.h2, a.hN, c0), m.zb[c0], hs2c(sc, a.h2, a.hN, c1),
+                                         m.zb[c1], m.dc[e]);
+            const double u2 = uN[e] + sc.c2 * (phi2 + S[e]);
+            if (ec == 2) {
+                const double phi3 = phi_fast(sc.g, hs3c(sc, a.h3, a.h2, a.hN, c0), m.zb[c0],
+                                             hs3c(sc, a.h3, a.h2, a.hN, c1), m.zb[c1], m.dc[e]);
+                const double u3 = uN[e] + sc.c3 * (phi3 + S[e]);
+                ue = p.a * u3 + p.b * u2 + p.c * uN[e];
+            } else {
+                ue = u2;
+            }
+        }
+        const double Fe = (0.5 * (Hi + Hn)) * ue;
+        const double t = m.dv[e] * Fe;
+        acc = acc + (pos ? t : -t);
+    }
+    const double psi = -acc / m.areaCell[i];
+    if (i >= m.cb.f) {
+        const double v = a.hk[i] + sc.c3f * psi;
+        hnext[i] = v;
+        if (!(v > 0.0)) report(err, K_FINE_S3, k, i, v);
+    } else {
+        const int ai = i - m.cb.if2;
+        const double prev = k == 0 ? 0.0 : accH[ai];
+        accH[ai] = prev + psi;
+    }
+}
+
+// view HS3 (h^{***,k}) for the fine velocity stage 3
+__device__ __forceinline__ double view3(const Bounds &b, const StepConst &sc, const PredConst &p,
+                                        const FineArrays &a, const double *hnext, int x) {
+    const int cl = ccls(b, x);
+    if (cl == 2) return sc.b3 * hnext[x] + sc.om2b3 * a.h2[x] + sc.b3 * a.hk[x];
+    if (cl == 1) {
+        const double hP0 = pred_level(p, a, x);
+        const double hP0n = pred_level1(p, a, x);
+        const double hP2 = pred_stage(p, a.h3, a.h2, a.hN, x);
+        return sc.b3 * hP0n + sc.om2b3 * hP2 + sc.b3 * hP0;
+    }
+    return hs3c(sc, a.h3, a.h2, a.hN, x);
+}
+
+// Fine velocity stage 3 (subeqn fine_s3) on F_E fused with the momentum correction summand on
+// IF-1_E u IF-2_E (eq. if_correction): F_E: u^{n,k+1} = u^{n,k} + dt/M (Phi^fast(h^{***,k}) + S);
+// IF_E: accU += Phi^fast(h^{***,k}) + S.
+__global__ void __launch_bounds__(TPB) k_fine_vel(DevMesh m, FineArrays a, const double *__restrict__ hnext,
+                                                  const double *__restrict__ uk, const double *__restrict__ S,
+                                                  double *__restrict__ unext, double *__restrict__ accU,
+                                                  StepConst sc, PredConst p, int k) {
+    const int e = m.eb.if2 + blockIdx.x * TPB + threadIdx.x;
+    if (e >= m.eb.end) return;
+    const int2 c = m.coe[e];
+    const double phi = phi_fast(sc.g, view3(m.cb, sc, p, a, hnext, c.x), m.zb[c.x],
+                                view3(m.cb, sc, p, a, hnext, c.y), m.zb[c.y], m.dc[e]);
+    if (e >= m.eb.f) {
+        unext[e] = uk[e] + sc.c3f * (phi + S[e]);
+    } else {
+        const int ai = e - m.eb.if2;
+        const double prev = k == 0 ? 0.0 : accU[ai];
+        accU[ai] = prev + (phi + S[e]);
+    }
+}
+
+// Interface Correction (eq. if_correction; reading Q14):
+// h^{n+1} = h^n + dt/M accH on IF-1 u IF-2, u^{n+1} = u^n + dt/M accU on IF-1_E u IF-2_E.
+__global__ void __launch_bounds__(TPB) k_correct(DevMesh m, const double *__restrict__ hN,
+                                                 const double *__restrict__ uN, const double *__restrict__ accH,
+                                                 const double *__restrict__ accU, double *__restrict__ hNew,
+                                                 double *__restrict__ uNew, StepConst sc, unsigned nbC,
+                                                 DevError *err) {
+    if (blockIdx.x < nbC) {
+        const int i = m.cb.if2 + blockIdx.x * TPB + threadIdx.x;
+        if (i >= m.cb.f) return;
+        const double v = hN[i] + sc.c3f * accH[i - m.cb.if2];
+        hNew[i] = v;
+        if (!(v > 0.0)) report(err, K_CORRECT, -1, i, v);
+    } else {
+        const int e = m.eb.if2 + (blockIdx.x - nbC) * TPB + threadIdx.x;
+        if (e >= m.eb.f) return;
+        uNew[e] = uN[e] + sc.c3f * accU[e - m.eb.if2];
+    }
+}
+
+// ---------------------------------------------------------------- permutation, diagnostics
+__global__ void k_permute_in(const int32_t *__restrict__ old, const double *__restrict__ src,
+                             double *__restrict__ dst, int n) {
+    const int i = blockIdx.x * TPB + threadIdx.x;
+    if (i < n) dst[i] = src[old[i]];
+}
+__global__ void k_permute_out(const int32_t *__restrict__ old, const double *__restrict__ src,
+                              double *__restrict__ dst, int n) {
+    const int i = blockIdx.x * TPB + threadIdx.x;
+    if (i < n) dst[old[i]] = src[i];
+}
+
+// double-double accumulation (Knuth TwoSum), deterministic for a fixed launch shape
+struct DD {
+    double hi, lo;
+};
+__device__ __forceinline__ void dd_add(DD &a, double x) {
+    const double s = a.hi + x;
+    const double bb = s - a.hi;
+    const double err = (a.hi - (s - bb)) + (x - bb);
+    a.hi = s;
+    a.lo = a.lo + err;
+}
+__device__ __forceinline__ DD dd_merge(DD a, DD b) {
+    const double s = a.hi + b.hi;
+    const double bb = s - a.hi;
+    const double err = (a.hi - (s - bb)) + (b.hi - bb) + (a.lo + b.lo);
+    DD r;
+    r.hi = s + err;
+    r.lo = err - (r.hi - s);
+    return r;
+}
+
+constexpr int DIAG_BLOCKS = 296;
+
+__global__ void __launch_bounds__(TPB) k_diag_partial(DevMesh m, const double *__restrict__ h,
+                                                      const double *__restrict__ u, StepConst sc,
+                                                      double *__restrict__ part) {
+    const int tid = blockIdx.x * TPB + threadIdx.x;
+    const int T = gridDim.x * TPB;
+    DD mass{0.0, 0.0}, gam{0.0, 0.0};
+    double hmin = 1.0 / 0.0, numax = 0.0;
+    for (int i = tid; i < m.cb.end; i += T) {
+        dd_add(mass, m.areaCell[i] * h[i]);
+        hmin = fmin(hmin, h[i]);
+    }
+    for (int v = tid; v < m.nV; v += T) {
+        double circ = 0.0;
+        for (int k = 0; k < 3; ++k) {
+            bool pos;
+            const int e = decode(m.eov[k * m.strideV + v], pos);
+            const double t = m.dc[e] * u[e];
+            circ = circ + (pos ? t : -t);
+        }
+        dd_add(gam, circ + m.areaTri[v] * m.fV[v]);
+    }
+    for (int e = tid; e < m.eb.end; e += T) {
+        const int2 c = m.coe[e];
+        const double he = 0.5 * (h[c.x] + h[c.y]);
+        const double dte = e >= m.eb.f ? sc.c3f : sc.c3;
+        const double nu = (fabs(u[e]) + sqrt(sc.g * he)) * dte / m.dc[e];
+        numax = fmax(numax, nu);
+    }
+    __shared__ double sh[6][TPB];
+    sh[0][threadIdx.x] = mass.hi;
+    sh[1][threadIdx.x] = mass.lo;
+    sh[2][threadIdx.x] = gam.hi;
+    sh[3][threadIdx.x] = gam.lo;
+    sh[4][threadIdx.x] = hmin;
+    sh[5][threadIdx.x] = numax;
+    __syncthreads();
+    for (int w = TPB / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            const int o = threadIdx.x + w;
+            DD a{sh[0][threadIdx.x], sh[1][threadIdx.x]}, b{sh[0][o], sh[1][o]};
+            DD r = dd_merge(a, b);
+            sh[0][threadIdx.x] = r.hi;
+            sh[1][threadIdx.x] = r.lo;
+            DD c{sh[2][threadIdx.x], sh[3][threadIdx.x]}, d{sh[2][o], sh[3][o]};
+            DD r2 = dd_merge(c, d);
+            sh[2][threadIdx.x] = r2.hi;
+            sh[3][threadIdx.x] = r2.lo;
+            sh[4][threadIdx.x] = fmin(sh[4][threadIdx.x], sh[4][o]);
+            sh[5][threadIdx.x] = fmax(sh[5][threadIdx.x], sh[5][o]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x < 6) part[blockIdx.x * 6 + threadIdx.x] = sh[threadIdx.x][0];
+}
+
+__global__ void k_diag_final(const double *__restrict__ part, int nb, double *__restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    DD mass{0.0, 0.0}, gam{0.0, 0.0};
+    double hmin = 1.0 / 0.0, numax = 0.0;
+    for (int b = 0; b < nb; ++b) {
+        mass = dd_merge(mass, DD{part[b * 6 + 0], part[b * 6 + 1]});
+        gam = dd_merge(gam, DD{part[b * 6 + 2], part[b * 6 + 3]});
+        hmin = fmin(hmin, part[b * 6 + 4]);
+        numax = fmax(numax, part[b * 6 + 5]);
+    }
+    out[0] = mass.hi + mass.lo;
+    out[1] = gam.hi + gam.lo;
+    out[2] = hmin;
+    out[3] = numax;
+}
+
+// ---------------------------------------------------------------- launchers
+void launch_slow_pre(const DevMesh &m, const DevState &st, const double *h, const double *u, cudaStream_t s) {
+    const unsigned nbV = nblocks(m.nV), nbC = nblocks(m.nC), nbE = nblocks(m.nE);
+    k_slow_pre<<<nbV + nbC + nbE, TPB, 0, s>>>(m, h, u, st.q, st.K, st.F, nbV, nbC);
+}
+void launch_slow_edge(const DevMesh &m, const DevState &st, const double *h, const StepConst &sc, cudaStream_t s) {
+    k_slow_edge<<<nblocks(m.nE), TPB, 0, s>>>(m, h, st.q, st.K, st.F, st.S, sc.rho0);
+}
+void launch_coarse_s1(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
+                      const StepConst &sc, cudaStream_t s) {
+    const int end = m.cb.fl[5];
+    if (end > 0) k_coarse_stage<1><<<nblocks(end), TPB, 0, s>>>(m, hN, hN, uN, st.S, st.h1, sc, end, st.err);
+}
+void launch_coarse_s2(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
+                      const StepConst &sc, cudaStream_t s) {
+    const int end = m.cb.fl[3];
+    if (end > 0) k_coarse_stage<2><<<nblocks(end), TPB, 0, s>>>(m, hN, st.h1, uN, st.S, st.h2, sc, end, st.err);
+}
+void launch_coarse_s3(const DevMesh &m, const DevState &st, const double *hN, const double *uN, double *hNew,
+                      const StepConst &sc, cudaStream_t s) {
+    const int end = m.cb.fl[1];
+    if (end > 0) k_coarse_stage<3><<<nblocks(end), TPB, 0, s>>>(m, hN, st.h2, uN, st.S, hNew, sc, end, st.err);
+}
+void launch_coarse_vel(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
+                       const double *hNew, double *uNew, const StepConst &sc, cudaStream_t s) {
+    const int end = m.eb.if2;
+    if (end > 0) k_coarse_vel<<<nblocks(end), TPB, 0, s>>>(m, hN, st.h2, hNew, uN, st.S, uNew, sc, end);
+}
+static FineArrays fine_arrays(const DevState &st, const double *hN, const double *hNew, const double *hk) {
+    FineArrays a;
+    a.hN = hN;
+    a.h1 = st.h1;
+    a.h2 = st.h2;
+    a.h3 = hNew;
+    a.hk = hk;
+    return a;
+}
+void launch_fine_s1(const DevMesh &m, const DevState &st, const double *hN, const double *hNew, const double *hk,
+                    const double *uk, const StepConst &sc, const PredConst &pc, int k, cudaStream_t s) {
+    const int n = m.cb.end - m.cb.f;
+    if (n > 0) k_fine_s1<<<nblocks(n), TPB, 0, s>>>(m, fine_arrays(st, hN, hNew, hk), uk, st.h1, sc, pc, k, st.err);
+}
+void launch_fine_s2(const DevMesh &m, const DevState &st, const double *hN, const double *hNew, const double *hk,
+                    const double *uk, const StepConst &sc, const PredConst &pc, int k, cudaStream_t s) {
+    const int n = m.cb.end - m.cb.f;
+    if (n > 0)
+        k_fine_s2<<<nblocks(n), TPB, 0, s>>>(m, fine_arrays(st, hN, hNew, hk), uk, st.S, st.h2, sc, pc, k, st.err);
+}
+void launch_fine_s3(const DevMesh &m, const DevState &st, const double *hN, const double *uN, const double *hNew,
+                    const double *hk, const double *uk, double *hnext, const StepConst &sc, const PredConst &pc,
+                    int k, cudaStream_t s) {
+    const int n = m.cb.end - m.cb.if2;
+    if (n > 0)
+        k_fine_s3<<<nblocks(n), TPB, 0, s>>>(m, fine_arrays(st, hN, hNew, hk), uN, uk, st.S, hnext, st.accH, sc,
+                                             pc, k, st.err);
+}
+void launch_fine_vel(const DevMesh &m, const DevState &st, const double *hN, const double *hNew, const double *hk,
+                     const double *hnext, const double *uk, double *unext, const StepConst &sc,
+                     const PredConst &pc, int k, cudaStream_t s) {
+    const int n = m.eb.end - m.eb.if2;
+    if (n > 0)
+        k_fine_vel<<<nblocks(n), TPB, 0, s>>>(m, fine_arrays(st, hN, hNew, hk), hnext, uk, st.S, unext, st.accU,
+                                              sc, pc, k);
+}
+void launch_correct(const DevMesh &m, const DevState &st, const double *hN, const double *uN, double *hNew,
+                    double *uNew, const StepConst &sc, cudaStream_t s) {
+    const unsigned nbC = nblocks(m.cb.f - m.cb.if2), nbE = nblocks(m.eb.f - m.eb.if2);
+    if (nbC + nbE > 0) k_correct<<<nbC + nbE, TPB, 0, s>>>(m, hN, uN, st.accH, st.accU, hNew, uNew, sc, nbC, st.err);
+}
+void launch_permute_in(const int32_t *old, const double *src, double *dst, int n, cudaStream_t s) {
+    if (n > 0) k_permute_in<<<nblocks(n), TPB, 0, s>>>(old, src, dst, n);
+}
+void launch_permute_out(const int32_t *old, const double *src, double *dst, int n, cudaStream_t s) {
+    if (n > 0) k_permute_out<<<nblocks(n), TPB, 0, s>>>(old, src, dst, n);
+}
+void launch_diagnostics(const DevMesh &m, const DevState &st, const double *h, const double *u, const StepConst &sc,
+                        double *out_dev, cudaStream_t s) {
+    k_diag_partial<<<DIAG_BLOCKS, TPB, 0, s>>>(m, h, u, sc, st.diag);
+    k_diag_final<<<1, 32, 0, s>>>(st.diag, DIAG_BLOCKS, out_dev);
+}
+
+}  // namespace fblts

@@ -1,0 +1,88 @@
+"""Solver: a thin object wrapper over the C ABI (marshalling + torch-owned device memory).
+
+    s = Solver(mesh, fine_mask, dt=..., M=4)       # upload, label, reorder, bind workspace
+    s.set_state(h0, u0)                            # host arrays, original order
+    s.step(100)                                    # enqueued on torch's current stream
+    h, u, t = s.state()                            # host arrays, original order
+    mass, gamma, hmin, numax = s.diagnostics()
+
+PyTorch supplies only the device workspace (one uint8 tensor), the stream and,
+for several ranks, the process group; every step of the method runs in
+libfblts.so's CUDA kernels.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _abi as abi
+
+
+class Solver:
+    def __init__(self, mesh, fine_mask, dt, M, *, g=9.81, beta=(0.531, 0.531, 0.313), rho0=1000.0, r=2,
+                 slow=True, tau_n=None, device=None, stream=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2405_10505_b200.Solver needs a CUDA device (no CPU fallback)")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.nCells, self.nEdges = int(mesh.nCells), int(mesh.nEdges)
+        self.ctx = abi.fblts_create(dt, M, g=g, beta=beta, rho0=rho0, r=r, slow=slow, device=self.device.index,
+                                    stream=self.stream.cuda_stream)
+        try:
+            abi.fblts_upload_mesh(self.ctx, mesh)
+            abi.fblts_set_regions(self.ctx, fine_mask)
+            nbytes = abi.fblts_workspace_size(self.ctx)
+            self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            abi.fblts_bind_workspace(self.ctx, self.workspace.data_ptr(), nbytes)
+            abi.fblts_set_forcing(self.ctx, tau_n)
+        except Exception:
+            abi.fblts_destroy(self.ctx)
+            self.ctx = None
+            raise
+        self.dt, self.M = dt, M
+
+    # --- setup queries
+    def labels(self):
+        return abi.fblts_get_labels(self.ctx, self.nCells, self.nEdges)
+
+    def counts(self):
+        c = abi.fblts_get_counts(self.ctx)
+        return {"nCells": int(c[0]), "nEdges": int(c[1]), "nVertices": int(c[2]),
+                "cells_by_region": c[3:12].tolist(), "edges_by_region": c[12:21].tolist()}
+
+    # --- state and stepping
+    def set_state(self, h, u, t=0.0):
+        abi.fblts_set_state(self.ctx, h, u, t)
+
+    def set_forcing(self, tau_n):
+        abi.fblts_set_forcing(self.ctx, tau_n)
+
+    def step(self, n_coarse=1):
+        abi.fblts_step(self.ctx, n_coarse)
+
+    def sync(self):
+        abi.fblts_sync(self.ctx)
+
+    def state(self, h_out=None, u_out=None):
+        h = np.empty(self.nCells) if h_out is None else h_out
+        u = np.empty(self.nEdges) if u_out is None else u_out
+        t = abi.fblts_get_state(self.ctx, h, u)
+        return h, u, t
+
+    def diagnostics(self):
+        return abi.fblts_diagnostics(self.ctx)
+
+    def profile(self, n_coarse):
+        ms, cnt = abi.fblts_profile(self.ctx, n_coarse)
+        return {abi.fblts_kernel_name(k): (float(ms[k]), int(cnt[k])) for k in range(abi.NUM_KERNELS)}
+
+    def close(self):
+        if self.ctx is not None:
+            abi.fblts_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -68,12 +68,14 @@ def main(names):
         elif name == "config5":
             # proxy: one 256-km tile of config 5 (same dc, profile, roughness recipe, M) in x,
             # 128 km in y; the full 4096^2 mesh is too large for 300 oracle steps per trial.
-            case = configs.shelf_case("config5_proxy", 512, 296, 500.0, 5, n_tiles=1, n_steps=50, dt=1.0)
+            # bump density kept: 8 bumps per 256 x 1773 km tile -> 1 bump on the 256 x 128 km proxy
+            case = configs.shelf_case("config5_proxy", 512, 296, 500.0, 5, n_tiles=1, n_steps=50, dt=1.0,
+                                      bumps_per_tile=1)
         else:
             raise SystemExit(f"unknown config {name}")
         res = scan(name, case)
         if name == "config5":
-            res["proxy"] = "512x296 cells (one 256-km x-tile, dc = 500 m, seed 5)"
+            res["proxy"] = "512x296 cells (one 256-km x-tile, 128 km in y, dc = 500 m, 1 bump, seed 5)"
         print(name, res, flush=True)
         table = json.load(open(OUT)) if os.path.exists(OUT) else {}
         table[name] = res

@@ -1,0 +1,213 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element.
+
+Tolerance (BASELINE.json north_star): max relative error <= 1e-11 in h and u after 100 coarse
+steps, normwise (reading Q26: eps_h = max|dh| / max|h|, eps_u = max|du| / max|u|), and mass /
+absolute-vorticity drift <= 1e-13.  Both sides evaluate the paper's formulas in the same
+canonical order without FMA contraction, so the observed difference is expected to be 0; the
+tests assert the contract tolerance and record the bitwise result.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from inputs import configs
+from oracle import diagnostics as dg
+from oracle import fbrk32, lts
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-11
+DRIFT = 1e-13
+
+
+@pytest.fixture(scope="module")
+def Solver():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2405_10505_b200 import Solver
+    return Solver
+
+
+def phys_of(c):
+    return fbrk32.Phys(g=c.g, beta=c.beta, slow=c.slow, tau_n=c.tau_n, rho0=c.rho0)
+
+
+def run_oracle(c, n, M=None, fine=None):
+    M = c.M if M is None else M
+    fine = c.fine_mask if fine is None else fine
+    lab = lts.label_regions(c.mesh, fine)
+    h, u = lts.run(c.mesh, lab, c.h0, c.u0, c.dt, M, phys_of(c), n)
+    return h, u, lab
+
+
+def run_gpu(Solver, c, n, M=None, fine=None):
+    M = c.M if M is None else M
+    fine = c.fine_mask if fine is None else fine
+    s = Solver(c.mesh, fine, c.dt, M, g=c.g, beta=c.beta, rho0=c.rho0, slow=c.slow, tau_n=c.tau_n)
+    s.set_state(c.h0, c.u0, 0.0)
+    s.step(n)
+    h, u, t = s.state()
+    return s, h, u, t
+
+
+def rel_err(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def assert_parity(hg, ug, ho, uo, tol=TOL):
+    assert np.all(np.isfinite(hg)) and np.all(np.isfinite(ug))
+    eh, eu = rel_err(hg, ho), rel_err(ug, uo)
+    assert eh <= tol and eu <= tol, (eh, eu)
+    return eh, eu
+
+
+@pytest.mark.parametrize("which", ["config1", "shelf", "shelf_ragged"])
+def test_parity_100_steps(Solver, which):
+    """FB-LTS (M = 4) after 100 coarse steps: h and u within 1e-11 of the oracle (expected bitwise)."""
+    c = {"config1": lambda: configs.config1(),
+         "shelf": lambda: configs.small_shelf(nx=48, ny=40, dt=25.0),
+         "shelf_ragged": lambda: configs.small_shelf(nx=70, ny=38, seed=11, dt=25.0)}[which]()
+    n = 100
+    ho, uo, lab = run_oracle(c, n)
+    s, hg, ug, t = run_gpu(Solver, c, n)
+    eh, eu = assert_parity(hg, ug, ho, uo)
+    print(f"{which}: eps_h={eh:.3e} eps_u={eu:.3e} bitwise={np.array_equal(hg, ho) and np.array_equal(ug, uo)}")
+    assert t == pytest.approx(n * c.dt)
+    cell, edge = s.labels()
+    assert np.array_equal(cell, lab.cell) and np.array_equal(edge, lab.edge)
+    m0 = dg.total_mass(c.mesh, c.h0)
+    assert abs(dg.total_mass(c.mesh, hg) - m0) <= DRIFT * m0
+
+
+@pytest.mark.parametrize("M", [1, 2, 3, 8])
+def test_parity_other_M(Solver, M):
+    """Any subcycling ratio; M = 1 reduces to FB-RK(3,2)."""
+    c = configs.small_shelf(nx=48, ny=40, dt=min(5.0 * M, 30.0))      # fine nu ~ 0.5 for every M
+    ho, uo, _ = run_oracle(c, 20, M=M)
+    _, hg, ug, _ = run_gpu(Solver, c, 20, M=M)
+    assert_parity(hg, ug, ho, uo)
+    if M == 1:
+        hh, uu = c.h0.copy(), c.u0.copy()
+        for _ in range(20):
+            hh, uu = fbrk32.fbrk32_step(c.mesh, hh, uu, c.dt, phys_of(c))
+        assert_parity(hg, ug, hh, uu)
+
+
+def test_parity_no_fine_cells_is_global(Solver):
+    """No fine cells: the GPU runs global FB-RK(3,2) (P2; config 3's mode)."""
+    c = configs.small_shelf(nx=48, ny=40, dt=4.0)
+    none = np.zeros(c.mesh.nCells, bool)
+    hh, uu = c.h0.copy(), c.u0.copy()
+    for _ in range(30):
+        hh, uu = fbrk32.fbrk32_step(c.mesh, hh, uu, c.dt, phys_of(c))
+    _, hg, ug, _ = run_gpu(Solver, c, 30, fine=none)
+    assert_parity(hg, ug, hh, uu)
+
+
+def test_parity_all_fine(Solver):
+    """Every cell fine (no coarse region): M fine FB-RK(3,2) subcycles everywhere."""
+    c = configs.small_shelf(nx=40, ny=36, dt=20.0)
+    allf = np.ones(c.mesh.nCells, bool)
+    hh, uu = c.h0.copy(), c.u0.copy()
+    for _ in range(10 * c.M):
+        hh, uu = fbrk32.fbrk32_step(c.mesh, hh, uu, c.dt / c.M, phys_of(c))
+    _, hg, ug, _ = run_gpu(Solver, c, 10, fine=allf)
+    assert_parity(hg, ug, hh, uu)
+
+
+def test_parity_gravity_wave_model(Solver):
+    """Slow terms disabled (eq. grav_wave_model)."""
+    c = configs.config1()
+    c.slow = False
+    ho, uo, _ = run_oracle(c, 50)
+    _, hg, ug, _ = run_gpu(Solver, c, 50)
+    assert_parity(hg, ug, ho, uo)
+
+
+def test_parity_config2_full_size(Solver):
+    """BASELINE config 2 at full size (262,144 cells), 3 coarse steps, element by element."""
+    c = configs.config2()
+    ho, uo, _ = run_oracle(c, 3)
+    _, hg, ug, _ = run_gpu(Solver, c, 3)
+    assert_parity(hg, ug, ho, uo)
+
+
+def test_diagnostics_match_oracle(Solver):
+    """fblts_diagnostics = (mass, Gamma, min h, max nu) of the oracle (Thms 1-2, eq. cfl)."""
+    c = configs.small_shelf(nx=48, ny=40, dt=25.0)
+    ho, uo, lab = run_oracle(c, 10)
+    s, hg, ug, _ = run_gpu(Solver, c, 10)
+    d = s.diagnostics()
+    ref = dg.diagnostics(c.mesh, lab, ho, uo, c.dt, c.M, c.g)
+    assert d[0] == pytest.approx(ref[0], rel=1e-15)
+    fscale = float(np.sum(c.mesh.areaTriangle * np.abs(c.mesh.fVertex)))
+    assert abs(d[1] - ref[1]) <= 1e-15 * fscale
+    assert d[2] == ref[2] and d[3] == pytest.approx(ref[3], rel=1e-15)
+
+
+def test_conservation_on_gpu_long_run(Solver):
+    """Theorem 1 on the GPU: mass drift <= 1e-13 over 200 coarse steps (config 1)."""
+    c = configs.config1()
+    s = Solver(c.mesh, c.fine_mask, c.dt, c.M)
+    s.set_state(c.h0, c.u0)
+    d0 = s.diagnostics()
+    s.step(200)
+    d1 = s.diagnostics()
+    assert abs(d1[0] - d0[0]) <= DRIFT * d0[0]
+    fscale = float(np.sum(c.mesh.areaTriangle * np.abs(c.mesh.fVertex)))
+    assert abs(d1[1] - d0[1]) <= DRIFT * fscale
+
+
+def test_comparison_can_fail(Solver):
+    """Injected fault: perturbing one IF-1 value of the GPU result by 1e-9 relative must trip both
+    the parity check and the conservation check (the tests can see an error of that size)."""
+    c = configs.config1()
+    ho, uo, lab = run_oracle(c, 10)
+    _, hg, ug, _ = run_gpu(Solver, c, 10)
+    i = int(np.nonzero(lab.IF1())[0][0])
+    bad = hg.copy()
+    bad[i] *= 1.0 + 1e-9
+    with pytest.raises(AssertionError):
+        assert_parity(bad, ug, ho, uo)
+    m0 = dg.total_mass(c.mesh, c.h0)
+    assert abs(dg.total_mass(c.mesh, bad) - m0) > DRIFT * m0
+
+
+def test_deterministic(Solver):
+    c = configs.small_shelf(nx=48, ny=40, dt=25.0)
+    _, h1, u1, _ = run_gpu(Solver, c, 15)
+    _, h2, u2, _ = run_gpu(Solver, c, 15)
+    assert np.array_equal(h1, h2) and np.array_equal(u1, u2)
+
+
+def test_positivity_error_is_reported(Solver):
+    """A blow-up (dt far beyond the CFL limit) surfaces as FBLTS_ERR_POSITIVITY naming the kernel."""
+    from paper_2405_10505_b200 import abi
+    c = configs.config1(dt=2000.0)
+    s = Solver(c.mesh, c.fine_mask, c.dt, c.M)
+    s.set_state(c.h0, c.u0)
+    s.step(100)
+    with pytest.raises(abi.FbltsError) as ei:
+        s.state()
+    assert ei.value.code == -7 and "positivity" in str(ei.value)
+
+
+def test_set_state_rejects_bad_h(Solver):
+    from paper_2405_10505_b200 import abi
+    c = configs.config1()
+    s = Solver(c.mesh, c.fine_mask, c.dt, c.M)
+    h = c.h0.copy()
+    h[5] = -1.0
+    with pytest.raises(abi.FbltsError) as ei:
+        s.set_state(h, c.u0)
+    assert ei.value.code == -4 and "h[5]" in str(ei.value)
+
+
+def test_profile_counts_launches(Solver):
+    c = configs.config1()
+    s = Solver(c.mesh, c.fine_mask, c.dt, c.M)
+    s.set_state(c.h0, c.u0)
+    prof = s.profile(2)
+    assert prof["fine_s3"][1] == 2 * c.M and prof["slow_edge"][1] == 2 and prof["correct_if"][1] == 2
+    assert all(ms >= 0.0 for ms, _ in prof.values())
