@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the FB-LTS hot path on B200 (BASELINE.json metric:
+"cell-updates/sec (fine-step equiv) and % of HBM roofline at 1/2/4/8 B200").
+
+One step = one FB-LTS coarse step in split mode (all rows of SURVEY 8(a): slow terms, coarse
+advancement, interface prediction, M fine subcycles with the interface accumulation, interface
+correction) on the workload named in config.workload (default BASELINE config 5: 4096 x 4096
+periodic hex, dc = 500 m, shelf bathymetry tiled 8x in x, M = 4).  value = N_cells * M * K / T
+summed over ranks, T the max over ranks of the CUDA-event time of K steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference] [--config config5]
+
+--impl reference times the ORACLE (oracle/, plain numpy fp64) on the host cores, on a bounded
+sample of the same workload (this tier's reference arm).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "cell-updates/sec (fine-step equiv) and % of HBM roofline at 1/2/4/8 B200"
+UNIT = "cell-updates/s"
+
+
+# ------------------------------------------------------------------ workloads
+def make_case(name, rank=0):
+    from inputs import configs
+    if name == "config5":
+        return configs.config5()
+    if name == "config2":
+        return configs.config2()
+    if name == "config1":
+        return configs.config1()
+    if name.startswith("config5_"):                      # config5_<n>: n x n block of the config-5 recipe
+        n = int(name.split("_")[1])
+        return configs.config5(nx=n, ny=n)
+    raise SystemExit(f"unknown workload {name}")
+
+
+def cpu_sample_case():
+    """Bounded CPU sample of config 5: a 512 x 512 block of its recipe (one 256-km tile, dc = 500 m)."""
+    from inputs import configs
+    c = configs.config5(nx=512, ny=512)
+    return c, "512x512 block of the config-5 recipe (one 256-km x-tile, dc = 500 m, M = 4)"
+
+
+# ------------------------------------------------------------------ byte model
+def byte_model(counts, maxE=6, maxE2=10):
+    """Algorithmic bytes per launch of each kernel kind (the method's arrays, each element once per
+    sweep; recomputable intermediates and padding not counted).  On a hex mesh the stage kernels
+    give SURVEY 8(d)'s 188 B/cell (s >= 2)."""
+    C, E, V = counts["nCells"], counts["nEdges"], counts["nVertices"]
+    cc, ec = counts["cells_by_region"], counts["edges_by_region"]
+    cells = lambda lo, hi: sum(cc[lo:hi + 1])
+    edges = lambda lo, hi: sum(ec[lo:hi + 1])
+    slotC = 4 + 4 * maxE + 4 * maxE          # nEdgesOnCell + edgesOnCell + cellsOnCell
+    cell_s1 = slotC + 8 + 8 + 8              # h_prev(=h^n), areaCell, write
+    cell_s = slotC + 8 + 8 + 8 + 8 + 8       # h_prev, h_base, z_b, areaCell, write
+    edge_s1 = 8 + 8                          # u, l_e
+    edge_s = 8 + 8 + 8 + 8                   # u_base, S, l_e, d_e
+    vel_e = 8 + 8 + 8 + 8 + 8                # cellsOnEdge, u_base, S, d_e, write
+    vel_c = 8 * 4                            # h3, h2, h_base, z_b
+    b = {}
+    b["slow_pre"] = V * (12 + 12 + 24 + 8 + 8) + C * (4 + 4 * maxE + 8 + 8) + E * (8 + 8 + 8 + 8)
+    b["slow_edge"] = E * (4 + 4 * maxE2 + 8 * maxE2 + 8 + 8 + 8 + 8 + 8) + V * 8 + C * 8 + C * 8
+    b["coarse_s1"] = cells(0, 7) * cell_s1 + edges(0, 7) * edge_s1
+    b["coarse_s2"] = cells(0, 5) * cell_s + edges(0, 5) * edge_s
+    b["coarse_s3"] = cells(0, 3) * cell_s + edges(0, 3) * edge_s
+    b["coarse_vel"] = edges(0, 0) * vel_e + cells(0, 1) * vel_c
+    b["fine_s1"] = cells(3, 8) * (slotC + 8 + 8 + 8) + edges(3, 8) * edge_s1
+    b["fine_s2"] = cells(3, 8) * (slotC + 8 + 8 + 8 + 8 + 8 - 8) + edges(3, 8) * edge_s
+    b["fine_s3"] = cells(1, 8) * (slotC + 8 + 8 + 8 + 8 + 8 - 8) + edges(1, 8) * edge_s
+    b["fine_vel"] = edges(1, 8) * vel_e + cells(1, 8) * vel_c
+    b["correct_if"] = cells(1, 2) * 24 + edges(1, 2) * 24
+    return b
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic():
+    """Per-launch DRAM bytes from the committed ncu --set full capture (profiles/), or {}."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_dram_bytes.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+# ------------------------------------------------------------------ clocks during the timed region
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                rows.append((float(p[1]), float(p[2]), p[5:9]))
+            except ValueError:
+                continue
+        os.unlink(self.path)
+        if not rows:
+            return None
+        load = [r for r in rows if r[0] > 0.5 * r[1]] or rows
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for n, v in zip(names, r[2]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(r[0] for r in load), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ arms
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def run_cpu_baseline(steps=3, warmup=1):
+    from oracle import fbrk32, lts
+    c, sample = cpu_sample_case()
+    lab = lts.label_regions(c.mesh, c.fine_mask)
+    phys = fbrk32.Phys(g=c.g, beta=c.beta, slow=c.slow, tau_n=c.tau_n, rho0=c.rho0)
+    h, u = c.h0, c.u0
+    for _ in range(warmup):
+        h, u = lts.fblts_step(c.mesh, lab, h, u, c.dt, c.M, phys)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        h, u = lts.fblts_step(c.mesh, lab, h, u, c.dt, c.M, phys)
+    t = time.perf_counter() - t0
+    return {"value": c.mesh.nCells * c.M * steps / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{sample}; {steps} coarse steps after {warmup} warm-up, numpy single-threaded",
+            "seconds": t}
+
+
+def arm_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from inputs import configs  # noqa: F401
+    c, sample = cpu_sample_case()
+    from oracle import fbrk32, lts
+    lab = lts.label_regions(c.mesh, c.fine_mask)
+    phys = fbrk32.Phys(g=c.g, beta=c.beta, slow=c.slow, tau_n=c.tau_n, rho0=c.rho0)
+    h, u = c.h0, c.u0
+    for _ in range(args.warmup):
+        h, u = lts.fblts_step(c.mesh, lab, h, u, c.dt, c.M, phys)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        h, u = lts.fblts_step(c.mesh, lab, h, u, c.dt, c.M, phys)
+    t = time.perf_counter() - t0
+    value = c.mesh.nCells * c.M * args.steps / t
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": args.config, "sample": sample, "M": c.M,
+                                            "cells": c.mesh.nCells, "dt": c.dt},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def arm_native(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_10505_b200 import Solver
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    t_setup = time.perf_counter()
+    c = make_case(args.config, rank)
+    s = Solver(c.mesh, c.fine_mask, c.dt, c.M, g=c.g, beta=c.beta, rho0=c.rho0, slow=c.slow, tau_n=c.tau_n)
+    s.set_state(c.h0, c.u0, 0.0)
+    counts = s.counts()
+    t_setup = time.perf_counter() - t_setup
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        s.step(1)
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (device, CUDA events on the launching stream)
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    s.step(args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    s.sync()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    units = c.mesh.nCells * c.M * args.steps * world
+    value = units / (ms * 1e-3)
+
+    # ---------------- instrumented replay: per-kernel device time (events on the same stream)
+    n_prof = max(1, min(args.steps, 5))
+    prof = s.profile(n_prof)
+    bytes_per_launch = {}
+    bm = byte_model(counts)
+    for k, (tms, n) in prof.items():
+        if n:
+            bytes_per_launch[k] = bm[k]
+    dom = max((k for k in prof if prof[k][1]), key=lambda k: prof[k][0])
+    dom_ms = prof[dom][0] / prof[dom][1]
+    peak, peak_src = load_peaks()
+    achieved = bm[dom] / (dom_ms * 1e-3) / 1e9
+    traffic = load_traffic().get(args.config, {}).get(dom)
+    launches_per_step = sum(n for (_, n) in prof.values()) / n_prof
+    step_bytes = sum(bm[k] * n for k, (_, n) in prof.items()) / n_prof
+    prof_total = sum(t for (t, _) in prof.values())
+
+    # ---------------- end to end through the public API with HOST buffers
+    e2e = None
+    if not args.no_e2e:
+        h_host = torch.from_numpy(np.ascontiguousarray(c.h0)).pin_memory()
+        u_host = torch.from_numpy(np.ascontiguousarray(c.u0)).pin_memory()
+        h_out = torch.empty_like(h_host).pin_memory()
+        u_out = torch.empty_like(u_host).pin_memory()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        s.set_state(h_host, u_host, 0.0)                # H2D of the initial state (+ device permutation)
+        for _ in range(args.steps):
+            s.step(1)
+            s.diagnostics()                              # per-step run record: D2H of 4 doubles
+        s.state(h_out.numpy(), u_out.numpy())            # D2H of the final state
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ems = f0.elapsed_time(f1)
+        if world > 1:
+            t = torch.tensor([ems], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        state_bytes = 8 * (c.mesh.nCells + c.mesh.nEdges)
+        e2e = {"value": units / (ems * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": state_bytes / args.steps,
+               "d2h_bytes_per_step": 32 + state_bytes / args.steps,
+               "how": "set_state(pinned host h,u) + K x (step(1) + diagnostics()) + get_state(pinned host)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = run_cpu_baseline()
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "cells": c.mesh.nCells, "edges": c.mesh.nEdges,
+                   "vertices": c.mesh.nVertices, "M": c.M, "dt": c.dt,
+                   "cells_by_region": counts["cells_by_region"],
+                   "l2": "inputs larger than L2 (no flush needed)" if c.mesh.nCells > 2_000_000 else
+                         "working set may be L2-resident (no flush)",
+                   "parallelism": "1 GPU" if world == 1 else f"{world} independent weak-scaled blocks",
+                   "setup_s": round(t_setup, 1)},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "bytes_per_launch": bm[dom],
+                     "launch_ms": dom_ms, "share_of_step": prof[dom][0] / prof_total, "peak_source": peak_src,
+                     "step_achieved": step_bytes / (ms_step * 1e-3) / 1e9,
+                     "step_frac": step_bytes / (ms_step * 1e-3) / 1e9 / peak},
+        "kernels": {k: {"ms_per_launch": tms / n, "launches_per_step": n / n_prof,
+                        "GBps": bm[k] / (tms / n * 1e-3) / 1e9}
+                    for k, (tms, n) in prof.items() if n},
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(round(launches_per_step * args.steps)),
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--config", default="config5")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        arm_reference(args)
+    else:
+        arm_native(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -9,21 +9,24 @@ import os
 import numpy as np
 import pytest
 
-from inputs.hexmesh import build_periodic_hex_mesh
+from inputs.hexmesh import build_periodic_hex_mesh, build_periodic_hex_mesh_fast
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_worked_examples.json")))
 SQ3 = np.sqrt(3.0)
 
 
-@pytest.fixture(scope="module")
-def m4():
+BUILDERS = {"generic": build_periodic_hex_mesh, "lattice": build_periodic_hex_mesh_fast}
+
+
+@pytest.fixture(scope="module", params=sorted(BUILDERS))
+def m4(request):
     g = GOLD["hex4x4"]
-    return build_periodic_hex_mesh(g["nx"], g["ny"], g["dc"])
+    return BUILDERS[request.param](g["nx"], g["ny"], g["dc"])
 
 
-@pytest.fixture(scope="module")
-def m12():
-    return build_periodic_hex_mesh(12, 10, 3000.0)
+@pytest.fixture(scope="module", params=sorted(BUILDERS))
+def m12(request):
+    return BUILDERS[request.param](12, 10, 3000.0)
 
 
 def test_hex4x4_counts_and_areas(m4):
@@ -130,13 +133,31 @@ def test_weights_pv_consistency(m12):
     np.testing.assert_allclose(lhs, rhs, atol=1e-13 * scale)
 
 
-def test_mesh_deterministic():
+@pytest.mark.parametrize("builder", sorted(BUILDERS))
+def test_mesh_deterministic(builder):
     """same (nx, ny, dc) -> bit-identical mesh."""
-    a = build_periodic_hex_mesh(8, 6, 1234.5)
-    b = build_periodic_hex_mesh(8, 6, 1234.5)
+    a = BUILDERS[builder](8, 6, 1234.5)
+    b = BUILDERS[builder](8, 6, 1234.5)
     for k, v in a.arrays().items():
         if isinstance(v, np.ndarray):
             assert np.array_equal(v, getattr(b, k)), k
+
+
+def test_lattice_builder_matches_generic():
+    """The lattice builder describes the same mesh as the generic one: same cells, positions,
+    cell adjacency, and per-cell/per-edge geometry up to the edge/vertex numbering and rounding."""
+    a = build_periodic_hex_mesh(10, 8, 2000.0)
+    b = build_periodic_hex_mesh_fast(10, 8, 2000.0)
+    assert (a.nCells, a.nEdges, a.nVertices) == (b.nCells, b.nEdges, b.nVertices)
+    assert np.array_equal(a.cellsOnCell, b.cellsOnCell)
+    np.testing.assert_allclose(a.xCell, b.xCell, atol=1e-9)
+    np.testing.assert_allclose(a.areaCell, b.areaCell, rtol=1e-14)
+    pa = {tuple(sorted(p)): i for i, p in enumerate(a.cellsOnEdge.tolist())}
+    for e in range(b.nEdges):
+        ea = pa[tuple(sorted(b.cellsOnEdge[e].tolist()))]
+        assert abs(a.dvEdge[ea] - b.dvEdge[e]) <= 1e-12 * b.dvEdge[e]
+        sgn = 1.0 if a.cellsOnEdge[ea, 0] == b.cellsOnEdge[e, 0] else -1.0
+        np.testing.assert_allclose(sgn * a.edgeNormal[ea], b.edgeNormal[e], atol=1e-14)
 
 
 def test_rejects_small_or_odd():
