@@ -38,7 +38,8 @@ def build(force=False, verbose=False):
     if not force and up_to_date():
         return LIB
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    cmd = [nvcc(), *NVCC_FLAGS, "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(HERE, "csrc"),
+    extra = os.environ.get("FBLTS_NVCC_EXTRA", "").split()      # development knobs, e.g. -DFBLTS_MINB=8
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(HERE, "csrc"),
            "-o", LIB, *SOURCES]
     if verbose:
         print(" ".join(cmd), flush=True)

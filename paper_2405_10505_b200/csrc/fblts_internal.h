@@ -6,10 +6,13 @@
 //   cells : [ C^int | C^IF-2 | C^IF-1 | F^1 | F^2\F^1 | ... | F^5\F^4 | F\F^5 ]
 //   edges : [ int_E | IF-2_E | IF-1_E | F^1_E | ... | F_E\F^5_E ]
 //   vertices: SFC order.
-// Per-cell slot tables are stored slot-major ([slot][strideC]) so that lane i of
-// a warp reading slot j of cell i touches consecutive words.  edgesOnCell is
-// sign-encoded: e if the cell is cellsOnEdge[e][0] (n_{e,i} = +1), ~e otherwise;
-// edgesOnVertex likewise: e if the vertex is verticesOnEdge[e][1] (t_{e,v} = +1).
+// Cell kernels run one thread per cell and fetch the per-cell slot table
+// ec[i*G + j] = (edge, neighbour) (row stride G = 6, 8 or 16 >= maxEdges, 16-byte
+// aligned rows) with vector loads.  Per-edge tables read by one thread per edge
+// over slots (edgesOnEdge, weightsOnEdge) and per-vertex tables are slot-major
+// ([slot][stride]).  Edges are sign-encoded: e if the cell is cellsOnEdge[e][0]
+// (n_{e,i} = +1), ~e otherwise; edgesOnVertex likewise: e if the vertex is
+// verticesOnEdge[e][1] (t_{e,v} = +1).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -32,9 +35,9 @@ struct DevMesh {
     int32_t nC, nE, nV;               // local entity counts
     int32_t strideC, strideE, strideV; // padded slot strides
     int32_t maxE, maxE2;
+    int32_t ecS;                       // row stride of ec (G: 6, 8 or 16 >= maxEdges)
     const int32_t *__restrict__ nEoC;  // [nC]
-    const int32_t *__restrict__ eoc;   // [maxE][strideC]  sign-encoded
-    const int32_t *__restrict__ coc;   // [maxE][strideC]
+    const int2 *__restrict__ ec;       // [nC*maxE] (sign-encoded edge, neighbour cell), cell-major
     const double *__restrict__ areaCell;  // [nC]
     const double *__restrict__ zb;        // [nC]  z_b = -bottomDepth
     const int2 *__restrict__ coe;      // [nE] (c0, c1)
@@ -118,7 +121,6 @@ void launch_correct(const DevMesh &m, const DevState &st, const double *hN, cons
                     double *hNew, double *uNew, const StepConst &sc, cudaStream_t s);
 void launch_permute_in(const int32_t *old_of_new, const double *src, double *dst, int n, cudaStream_t s);
 void launch_permute_out(const int32_t *old_of_new, const double *src, double *dst, int n, cudaStream_t s);
-void launch_check_state(const double *h, int n, DevError *err, cudaStream_t s);
 // diagnostics: writes out[4] (device) = mass, Gamma, min h, max nu
 void launch_diagnostics(const DevMesh &m, const DevState &st, const double *h, const double *u,
                         const StepConst &sc, double *out_dev, cudaStream_t s);

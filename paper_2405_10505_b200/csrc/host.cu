@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <type_traits>
@@ -63,9 +64,9 @@ struct fblts_ctx {
     bool have_fine = false;
     cudaGraphExec_t exec[2]{};
     // host-side staging of the permuted device tables (filled at set_regions)
-    std::vector<int32_t> d_nEoC, d_eoc, d_coc, d_nEoE, d_eoe, d_eov, d_cov, d_coe, d_voe;
+    std::vector<int32_t> d_nEoC, d_ec, d_nEoE, d_eoe, d_eov, d_cov, d_coe, d_voe;
     std::vector<double> d_area, d_zb, d_dv, d_dc, d_W, d_kite, d_areaTri, d_fV, d_tau;
-    int sC = 0, sE = 0, sV = 0;
+    int sC = 0, sE = 0, sV = 0, ecS = 6;
 };
 
 namespace {
@@ -216,7 +217,7 @@ int fblts_upload_mesh(fblts_ctx *c, const fblts_mesh *m) {
     if (!c || !m) return FBLTS_ERR_INVALID_ARG;
     if (c->phase != P_CREATED) return fail(c, FBLTS_ERR_ORDER, "upload_mesh: mesh already uploaded");
     const int nC = m->nCells, nE = m->nEdges, nV = m->nVertices, mE = m->maxEdges, mE2 = m->maxEdges2;
-    if (nC <= 0 || nE <= 0 || nV <= 0 || mE < 3 || mE2 < 1)
+    if (nC <= 0 || nE <= 0 || nV <= 0 || mE < 3 || mE > 16 || mE2 < 1 || mE2 > 30)
         return fail(c, FBLTS_ERR_MESH, "mesh counts: nCells=%d nEdges=%d nVertices=%d maxEdges=%d maxEdges2=%d", nC,
                     nE, nV, mE, mE2);
     if (!m->nEdgesOnCell || !m->edgesOnCell || !m->cellsOnEdge || !m->verticesOnEdge || !m->nEdgesOnEdge ||
@@ -384,10 +385,10 @@ int fblts_set_regions(fblts_ctx *c, const uint8_t *fine_mask) {
     c->sC = pad32(m.nC);
     c->sE = pad32(m.nE);
     c->sV = pad32(m.nV);
-    const int sC = c->sC, sE = c->sE, sV = c->sV;
+    const int sE = c->sE, sV = c->sV;
     c->d_nEoC.assign(m.nC, 0);
-    c->d_eoc.assign((size_t)m.maxE * sC, 0);
-    c->d_coc.assign((size_t)m.maxE * sC, 0);
+    c->ecS = m.maxE <= 6 ? 6 : (m.maxE <= 8 ? 8 : 16);
+    c->d_ec.assign((size_t)m.nC * c->ecS * 2, 0);
     c->d_area.assign(m.nC, 0.0);
     c->d_zb.assign(m.nC, 0.0);
     for (int i = 0; i < m.nC; ++i) {
@@ -398,8 +399,8 @@ int fblts_set_regions(fblts_ctx *c, const uint8_t *fine_mask) {
         for (int j = 0; j < m.nEoC[o]; ++j) {
             const int e = m.eoc[(size_t)o * m.maxE + j];
             const int en = g.edgeNew[e];
-            c->d_eoc[(size_t)j * sC + i] = m.coe[2 * e] == o ? en : ~en;
-            c->d_coc[(size_t)j * sC + i] = g.cellNew[coc[(size_t)o * m.maxE + j]];
+            c->d_ec[((size_t)i * c->ecS + j) * 2] = m.coe[2 * e] == o ? en : ~en;
+            c->d_ec[((size_t)i * c->ecS + j) * 2 + 1] = g.cellNew[coc[(size_t)o * m.maxE + j]];
         }
     }
     c->d_coe.assign((size_t)m.nE * 2, 0);
@@ -493,12 +494,12 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
     };
     DevMesh &d = c->dm;
     DevState &s = c->ds;
-    int32_t *nEoC, *eoc, *coc, *nEoE, *eoe, *eov, *cov;
-    double *area, *zb, *dv, *dc, *W, *tau, *kite, *areaTri, *fV;
-    int2 *coe, *voe;
+    int32_t *nEoC, *nEoE, *eoe, *eov, *cov;
+    double *area, *zb, *W, *tau, *kite, *areaTri, *fV;
+    int2 *coe, *voe, *ec;
+    double *dv, *dc;
     put(nEoC, m.nC);
-    put(eoc, (size_t)m.maxE * c->sC);
-    put(coc, (size_t)m.maxE * c->sC);
+    put(ec, (size_t)m.nC * c->ecS);
     put(area, m.nC);
     put(zb, m.nC);
     put(coe, m.nE);
@@ -537,8 +538,8 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
     if (base) {
         d.nC = m.nC, d.nE = m.nE, d.nV = m.nV;
         d.strideC = c->sC, d.strideE = c->sE, d.strideV = c->sV;
-        d.maxE = m.maxE, d.maxE2 = m.maxE2;
-        d.nEoC = nEoC, d.eoc = eoc, d.coc = coc, d.areaCell = area, d.zb = zb;
+        d.maxE = m.maxE, d.maxE2 = m.maxE2, d.ecS = c->ecS;
+        d.nEoC = nEoC, d.ec = ec, d.areaCell = area, d.zb = zb;
         d.coe = coe, d.voe = voe, d.dv = dv, d.dc = dc, d.nEoE = nEoE, d.eoe = eoe, d.W = W, d.tau = tau;
         d.eov = eov, d.cov = cov, d.kite = kite, d.areaTri = areaTri, d.fV = fV;
         d.cb = g.cb, d.eb = g.eb;
@@ -575,8 +576,7 @@ int fblts_bind_workspace(fblts_ctx *c, void *ptr, size_t bytes) {
     };
     const HostMesh &m = c->hm;
     CUDA_TRY(c, up(d.nEoC, c->d_nEoC.data(), c->d_nEoC.size() * 4));
-    CUDA_TRY(c, up(d.eoc, c->d_eoc.data(), c->d_eoc.size() * 4));
-    CUDA_TRY(c, up(d.coc, c->d_coc.data(), c->d_coc.size() * 4));
+    CUDA_TRY(c, up(d.ec, c->d_ec.data(), c->d_ec.size() * 4));
     CUDA_TRY(c, up(d.areaCell, c->d_area.data(), m.nC * 8));
     CUDA_TRY(c, up(d.zb, c->d_zb.data(), m.nC * 8));
     CUDA_TRY(c, up(d.coe, c->d_coe.data(), (size_t)m.nE * 8));
@@ -598,8 +598,8 @@ int fblts_bind_workspace(fblts_ctx *c, void *ptr, size_t bytes) {
     CUDA_TRY(c, cudaMemsetAsync(c->ds.err, 0, sizeof(DevError), s));
     CUDA_TRY(c, cudaStreamSynchronize(s));
     // host staging of the device tables is no longer needed
-    std::vector<int32_t>().swap(c->d_eoc);
-    std::vector<int32_t>().swap(c->d_coc);
+    std::vector<int32_t>().swap(c->d_ec);
+
     std::vector<int32_t>().swap(c->d_eoe);
     std::vector<double>().swap(c->d_W);
     c->phase = P_BOUND;

@@ -5,17 +5,33 @@
 // left-to-right products, IEEE division, no FMA contraction (--fmad=false), so
 // the results agree bit for bit with a literal implementation of the paper.
 //
-// Fusion: in split mode Phi^fast_e depends only on cell
-// data, so the stage-s velocity  u_bar_{s-1,e} = u_base,e + c_{s-1} (Phi^fast_e(h_FB) + S_e)
-// is recomputed inside the stage-s cell kernel from the two cells of e instead
-// of being stored; the FB averages h*, h**, h*** and the IF-1 predictions
-// (eq. preds) are likewise recomputed from the stored stage
-// thicknesses.  Velocity is written once per (sub)step.
+// Thread mapping: one thread per cell (cell kernels) or per
+// edge (edge kernels), 256-thread blocks over a contiguous index range.  A cell
+// fetches its (edge, neighbour) row with 16-byte vector loads and the slot loop is
+// unrolled to G >= maxEdges with predication, so every gather of the cell can be
+// in flight at once.
+//
+// Band / deep split: cells are ordered [int | IF-2 | IF-1 | F^1 | F^2 .. | F\F^5]
+// and edges likewise.  Only the "band" [IF-2, F^1] can see a neighbour of another
+// region; a cell of F\F^1 has only fine neighbours (its hop distance to C is >= 3)
+// and an edge of F_E\F^1_E has two fine cells.  Every fine kernel is therefore
+// launched twice: a BAND instance with the region views and a DEEP instance with
+// none (no class tests, fewer registers).
+//
+// Fusion: in split mode Phi^fast_e depends only on cell data, so the stage-s
+// velocity  u_bar_{s-1,e} = u_base,e + c_{s-1} (Phi^fast_e(h_FB) + S_e)  is
+// recomputed inside the stage-s cell kernel from the two cells of e instead of
+// being stored; the FB averages h*, h**, h*** and the IF-1 predictions (eq. preds,
+// P:L683-742) are likewise recomputed from the stored stage thicknesses.
 #include "fblts_internal.h"
 
 namespace fblts {
 
 constexpr int TPB = 256;
+// min resident blocks per SM requested for the register-heavy stage kernels (occupancy knob)
+#ifndef FBLTS_MINB
+#define FBLTS_MINB 6
+#endif
 
 static inline unsigned nblocks(long n) { return (unsigned)((n + TPB - 1) / TPB); }
 
@@ -47,10 +63,30 @@ __device__ __forceinline__ int decode(int es, bool &pos) {
     return pos ? es : ~es;
 }
 
+// One slot of Psi_i: the signed term n_{e,i} l_e F_e with F_e = (0.5 (H_c0 + H_c1)) u_e.
+__device__ __forceinline__ double psi_term(bool pos, double Hi, double Hn, double ue, double l) {
+    const double Fe = (0.5 * (Hi + Hn)) * ue;
+    const double t = l * Fe;
+    return pos ? t : -t;
+}
+
+// (edge, neighbour) row of cell i with G/2 16-byte loads (row stride G, 16-B aligned)
+template <int G>
+__device__ __forceinline__ void load_row(const DevMesh &m, int i, int2 (&r)[G]) {
+    const int4 *p = reinterpret_cast<const int4 *>(m.ec + (size_t)i * G);
+#pragma unroll
+    for (int q = 0; q < G / 2; ++q) {
+        const int4 v = p[q];
+        r[2 * q] = make_int2(v.x, v.y);
+        r[2 * q + 1] = make_int2(v.z, v.w);
+    }
+}
+
 // ---------------------------------------------------------------- slow terms
 // One launch, three index spaces: vertices (q_v), cells (K_i), edges (F_e).
 // q_v = (zeta_v + f_v) / h_v,  zeta_v = (sum t d u)/A_v,  h_v = (sum kite h)/A_v
 // K_i = (sum 0.25 l d u u) / A_i   (Q18);   F_e = (0.5 (h_c0 + h_c1)) u_e   (Q1)
+template <int G>
 __global__ void __launch_bounds__(TPB) k_slow_pre(DevMesh m, const double *__restrict__ h,
                                                   const double *__restrict__ u, double *__restrict__ q,
                                                   double *__restrict__ K, double *__restrict__ F,
@@ -77,13 +113,18 @@ __global__ void __launch_bounds__(TPB) k_slow_pre(DevMesh m, const double *__res
     } else if (b < nbV + nbC) {
         const int i = (b - nbV) * TPB + threadIdx.x;
         if (i >= m.nC) return;
+        int2 r[G];
+        load_row<G>(m, i, r);
         const int n = m.nEoC[i];
         double acc = 0.0;
-        for (int j = 0; j < n; ++j) {
-            bool pos;
-            const int e = decode(m.eoc[j * m.strideC + i], pos);
-            const double ue = u[e];
-            acc = acc + 0.25 * m.dv[e] * m.dc[e] * ue * ue;
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+            if (j < n) {
+                bool pos;
+                const int e = decode(r[j].x, pos);
+                const double ue = u[e];
+                acc = acc + 0.25 * m.dv[e] * m.dc[e] * ue * ue;
+            }
         }
         K[i] = acc / m.areaCell[i];
     } else {
@@ -95,6 +136,7 @@ __global__ void __launch_bounds__(TPB) k_slow_pre(DevMesh m, const double *__res
 }
 
 // S_e = q_hat_e F_perp_e - (K_c1 - K_c0) / d_e + G_e   (Q2, Q5, Q19)
+template <int MAXE2>
 __global__ void __launch_bounds__(TPB) k_slow_edge(DevMesh m, const double *__restrict__ h,
                                                    const double *__restrict__ q, const double *__restrict__ K,
                                                    const double *__restrict__ F, double *__restrict__ S,
@@ -102,8 +144,18 @@ __global__ void __launch_bounds__(TPB) k_slow_edge(DevMesh m, const double *__re
     const int e = blockIdx.x * TPB + threadIdx.x;
     if (e >= m.nE) return;
     const int n = m.nEoE[e];
+    double w[MAXE2], f[MAXE2];
+#pragma unroll
+    for (int j = 0; j < MAXE2; ++j) {
+        if (j < n) {
+            w[j] = m.W[j * m.strideE + e];
+            f[j] = F[m.eoe[j * m.strideE + e]];
+        }
+    }
     double fp = 0.0;
-    for (int j = 0; j < n; ++j) fp = fp + m.W[j * m.strideE + e] * F[m.eoe[j * m.strideE + e]];
+#pragma unroll
+    for (int j = 0; j < MAXE2; ++j)
+        if (j < n) fp = fp + w[j] * f[j];
     const int2 v = m.voe[e];
     const int2 c = m.coe[e];
     const double qh = 0.5 * (q[v.x] + q[v.y]);
@@ -118,44 +170,47 @@ __global__ void __launch_bounds__(TPB) k_slow_edge(DevMesh m, const double *__re
 //   u1_e = u^n_e + dt/3 (Phi^fast_e(h*) + S_e), h* = b1 h1 + (1-b1) h^n.
 // Stage 3 (eq. if_h_s3 / coarse_h_s3): h3 = h^n + dt Psi(u2, h2) on C u F^1,
 //   u2_e = u^n_e + dt/2 (Phi^fast_e(h**) + S_e), h** = b2 h2 + (1-b2) h^n.
-template <int STAGE>
-__global__ void __launch_bounds__(TPB) k_coarse_stage(DevMesh m, const double *__restrict__ hN,
+template <int G, int STAGE>
+__global__ void __launch_bounds__(TPB, FBLTS_MINB) k_coarse_stage(DevMesh m, const double *__restrict__ hN,
                                                       const double *__restrict__ hprev,
                                                       const double *__restrict__ uN,
                                                       const double *__restrict__ S, double *__restrict__ out,
                                                       StepConst sc, int end, DevError *err) {
     const int i = blockIdx.x * TPB + threadIdx.x;
     if (i >= end) return;
+    int2 r[G];
+    load_row<G>(m, i, r);
+    const int n = m.nEoC[i];
     const double cu = STAGE == 2 ? sc.c1 : sc.c2;        // c_{s-1} of the velocity
-    const double ch = STAGE == 1 ? sc.c1 : (STAGE == 2 ? sc.c2 : sc.c3);
     const double bb = STAGE == 2 ? sc.b1 : sc.b2;
     const double omb = STAGE == 2 ? sc.omb1 : sc.omb2;
     const double hNi = hN[i];
     const double Hi = STAGE == 1 ? hNi : hprev[i];
     const double HSi = STAGE == 1 ? 0.0 : bb * Hi + omb * hNi;
     const double zbi = STAGE == 1 ? 0.0 : m.zb[i];
-    const int n = m.nEoC[i];
     double acc = 0.0;
-    for (int j = 0; j < n; ++j) {
-        bool pos;
-        const int e = decode(m.eoc[j * m.strideC + i], pos);
-        const int nb = m.coc[j * m.strideC + i];
-        double ue, Hn;
-        if (STAGE == 1) {
-            Hn = hN[nb];
-            ue = uN[e];
-        } else {
-            Hn = hprev[nb];
-            const double HSn = bb * Hn + omb * hN[nb];
-            const double zbn = m.zb[nb];
-            const double phi = pos ? phi_fast(sc.g, HSi, zbi, HSn, zbn, m.dc[e])
-                                   : phi_fast(sc.g, HSn, zbn, HSi, zbi, m.dc[e]);
-            ue = uN[e] + cu * (phi + S[e]);
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+        if (j < n) {
+            bool pos;
+            const int e = decode(r[j].x, pos);
+            const int nb = r[j].y;
+            double ue, Hn;
+            if (STAGE == 1) {
+                Hn = hN[nb];
+                ue = uN[e];
+            } else {
+                Hn = hprev[nb];
+                const double HSn = bb * Hn + omb * hN[nb];
+                const double zbn = m.zb[nb];
+                const double dc = m.dc[e];
+                const double phi = pos ? phi_fast(sc.g, HSi, zbi, HSn, zbn, dc) : phi_fast(sc.g, HSn, zbn, HSi, zbi, dc);
+                ue = uN[e] + cu * (phi + S[e]);
+            }
+            acc = acc + psi_term(pos, Hi, Hn, ue, m.dv[e]);
         }
-        const double Fe = (0.5 * (Hi + Hn)) * ue;
-        const double t = m.dv[e] * Fe;
-        acc = acc + (pos ? t : -t);
     }
+    const double ch = STAGE == 1 ? sc.c1 : (STAGE == 2 ? sc.c2 : sc.c3);
     const double psi = -acc / m.areaCell[i];
     const double v = hNi + ch * psi;
     out[i] = v;
@@ -188,7 +243,8 @@ __global__ void __launch_bounds__(TPB) k_coarse_vel(DevMesh m, const double *__r
 
 // ---------------------------------------------------------------- fine subcycles
 // Views (reading Q11): F -> fine data, IF-1 -> predicted (eq. preds,
-// eq. hstar_preds), IF-2 / int -> coarse tilde / bar data.
+// eq. hstar_preds), IF-2 / int -> coarse tilde / bar data.  In a DEEP instance every
+// cell and edge touched is fine, so the views reduce to the fine arrays.
 struct FineArrays {
     const double *hN, *h1, *h2, *h3, *hk;   // h3 = coarse stage-3 output (hNew before the correction)
 };
@@ -204,35 +260,23 @@ __device__ __forceinline__ double pred_stage(const PredConst &p, const double *h
     return p.a * h3[x] + p.b * hs[x] + p.c * hN[x];              // subeqn pred_s1 / pred_s2
 }
 
-// Fine stage 1 (subeqn fine_s1): h_bar^{n,k+1/3} = h^{n,k} + dt/(3M) Psi(u^{n,k}, h^{n,k}) on F.
-__global__ void __launch_bounds__(TPB) k_fine_s1(DevMesh m, FineArrays a, const double *__restrict__ uk,
-                                                 double *__restrict__ out, StepConst sc, PredConst p, int k,
-                                                 DevError *err) {
-    const int i = m.cb.f + blockIdx.x * TPB + threadIdx.x;
-    if (i >= m.cb.end) return;
-    const double Hi = a.hk[i];
-    const int n = m.nEoC[i];
-    double acc = 0.0;
-    for (int j = 0; j < n; ++j) {
-        bool pos;
-        const int e = decode(m.eoc[j * m.strideC + i], pos);
-        const int nb = m.coc[j * m.strideC + i];
-        const int cl = ccls(m.cb, nb);
-        const double Hn = cl == 2 ? a.hk[nb] : (cl == 1 ? pred_level(p, a, nb) : a.hN[nb]);
-        const double Fe = (0.5 * (Hi + Hn)) * uk[e];
-        const double t = m.dv[e] * Fe;
-        acc = acc + (pos ? t : -t);
-    }
-    const double psi = -acc / m.areaCell[i];
-    const double v = Hi + sc.c1f * psi;
-    out[i] = v;
-    if (!(v > 0.0)) report(err, K_FINE_S1, k, i, v);
+template <bool BAND>
+__device__ __forceinline__ int cclass(const Bounds &b, int x) { return BAND ? ccls(b, x) : 2; }
+template <bool BAND>
+__device__ __forceinline__ int eclass(const Bounds &b, int e) { return BAND ? ecls(b, e) : 3; }
+
+// view H0 (h^{n,k}) for fine stage 1
+template <bool BAND>
+__device__ __forceinline__ double view0(const Bounds &b, const PredConst &p, const FineArrays &a, int x) {
+    const int cl = cclass<BAND>(b, x);
+    return cl == 2 ? a.hk[x] : (cl == 1 ? pred_level(p, a, x) : a.hN[x]);
 }
 
 // view (H1, HS1) for fine stage 2
+template <bool BAND>
 __device__ __forceinline__ void view1(const Bounds &b, const StepConst &sc, const PredConst &p, const FineArrays &a,
                                       int x, double &H, double &HS) {
-    const int cl = ccls(b, x);
+    const int cl = cclass<BAND>(b, x);
     if (cl == 2) {
         H = a.h1[x];
         HS = sc.b1 * H + sc.omb1 * a.hk[x];
@@ -246,42 +290,11 @@ __device__ __forceinline__ void view1(const Bounds &b, const StepConst &sc, cons
     }
 }
 
-// Fine stage 2 (subeqn fine_s2): h_bar^{n,k+1/2} = h^{n,k} + dt/(2M) Psi(u_bar^{n,k+1/3}, h_bar^{n,k+1/3}),
-// u_bar^{n,k+1/3}_e = u^{n,k}_e + dt/(3M) (Phi^fast_e(h^{*,k}) + S_e) recomputed per edge.
-__global__ void __launch_bounds__(TPB) k_fine_s2(DevMesh m, FineArrays a, const double *__restrict__ uk,
-                                                 const double *__restrict__ S, double *__restrict__ out,
-                                                 StepConst sc, PredConst p, int k, DevError *err) {
-    const int i = m.cb.f + blockIdx.x * TPB + threadIdx.x;
-    if (i >= m.cb.end) return;
-    double Hi, HSi;
-    view1(m.cb, sc, p, a, i, Hi, HSi);
-    const double zbi = m.zb[i];
-    const int n = m.nEoC[i];
-    double acc = 0.0;
-    for (int j = 0; j < n; ++j) {
-        bool pos;
-        const int e = decode(m.eoc[j * m.strideC + i], pos);
-        const int nb = m.coc[j * m.strideC + i];
-        double Hn, HSn;
-        view1(m.cb, sc, p, a, nb, Hn, HSn);
-        const double zbn = m.zb[nb];
-        const double phi = pos ? phi_fast(sc.g, HSi, zbi, HSn, zbn, m.dc[e])
-                               : phi_fast(sc.g, HSn, zbn, HSi, zbi, m.dc[e]);
-        const double ue = uk[e] + sc.c1f * (phi + S[e]);
-        const double Fe = (0.5 * (Hi + Hn)) * ue;
-        const double t = m.dv[e] * Fe;
-        acc = acc + (pos ? t : -t);
-    }
-    const double psi = -acc / m.areaCell[i];
-    const double v = a.hk[i] + sc.c2f * psi;
-    out[i] = v;
-    if (!(v > 0.0)) report(err, K_FINE_S2, k, i, v);
-}
-
 // view (H2, HS2) for fine stage 3 / the correction summand
+template <bool BAND>
 __device__ __forceinline__ void view2(const Bounds &b, const StepConst &sc, const PredConst &p, const FineArrays &a,
                                       int x, double &H, double &HS) {
-    const int cl = ccls(b, x);
+    const int cl = cclass<BAND>(b, x);
     if (cl == 2) {
         H = a.h2[x];
         HS = sc.b2 * H + sc.omb2 * a.hk[x];
@@ -295,71 +308,11 @@ __device__ __forceinline__ void view2(const Bounds &b, const StepConst &sc, cons
     }
 }
 
-// Fine stage 3 on F (subeqn fine_s3) fused with the correction summand on IF-1 u IF-2
-// (eq. if_correction, "accumulated during the fine advancement step", P:L787):
-//   F:      h^{n,k+1} = h^{n,k} + dt/M Psi(u_bar^{n,k+1/2}, h_bar^{n,k+1/2})
-//   IF:     accH += Psi(u_bar^{n,k+1/2}, h_bar^{n,k+1/2})          (views, reading Q11/Q14)
-// Edge velocity u_bar^{n,k+1/2} by edge region: F_E -> u^{n,k} + dt/(2M)(Phi^fast(h^{**,k}) + S);
-// IF-1_E -> predicted (k/M) u~^{n+1} + (1/M) u~^{n+1/2} + (1-(k+1)/M) u^n with the tilde data
-// recomputed from the coarse thicknesses; IF-2_E / int_E -> coarse u~^{n+1/2}.
-__global__ void __launch_bounds__(TPB) k_fine_s3(DevMesh m, FineArrays a, const double *__restrict__ uN,
-                                                 const double *__restrict__ uk, const double *__restrict__ S,
-                                                 double *__restrict__ hnext, double *__restrict__ accH,
-                                                 StepConst sc, PredConst p, int k, DevError *err) {
-    const int i = m.cb.if2 + blockIdx.x * TPB + threadIdx.x;
-    if (i >= m.cb.end) return;
-    double Hi, HSi;
-    view2(m.cb, sc, p, a, i, Hi, HSi);
-    const double zbi = m.zb[i];
-    const int n = m.nEoC[i];
-    double acc = 0.0;
-    for (int j = 0; j < n; ++j) {
-        bool pos;
-        const int e = decode(m.eoc[j * m.strideC + i], pos);
-        const int nb = m.coc[j * m.strideC + i];
-        double Hn, HSn;
-        view2(m.cb, sc, p, a, nb, Hn, HSn);
-        const double zbn = m.zb[nb];
-        const int c0 = pos ? i : nb, c1 = pos ? nb : i;
-        const int ec = ecls(m.eb, e);
-        double ue;
-        if (ec == 3) {
-            const double phi = pos ? phi_fast(sc.g, HSi, zbi, HSn, zbn, m.dc[e])
-                                   : phi_fast(sc.g, HSn, zbn, HSi, zbi, m.dc[e]);
-            ue = uk[e] + sc.c2f * (phi + S[e]);
-        } else {
-            const double phi2 = phi_fast(sc.g, hs2c(sc, a.h2, a.hN, c0), m.zb[c0], hs2c(sc, a.h2, a.hN, c1),
-                                         m.zb[c1], m.dc[e]);
-            const double u2 = uN[e] + sc.c2 * (phi2 + S[e]);
-            if (ec == 2) {
-                const double phi3 = phi_fast(sc.g, hs3c(sc, a.h3, a.h2, a.hN, c0), m.zb[c0],
-                                             hs3c(sc, a.h3, a.h2, a.hN, c1), m.zb[c1], m.dc[e]);
-                const double u3 = uN[e] + sc.c3 * (phi3 + S[e]);
-                ue = p.a * u3 + p.b * u2 + p.c * uN[e];
-            } else {
-                ue = u2;
-            }
-        }
-        const double Fe = (0.5 * (Hi + Hn)) * ue;
-        const double t = m.dv[e] * Fe;
-        acc = acc + (pos ? t : -t);
-    }
-    const double psi = -acc / m.areaCell[i];
-    if (i >= m.cb.f) {
-        const double v = a.hk[i] + sc.c3f * psi;
-        hnext[i] = v;
-        if (!(v > 0.0)) report(err, K_FINE_S3, k, i, v);
-    } else {
-        const int ai = i - m.cb.if2;
-        const double prev = k == 0 ? 0.0 : accH[ai];
-        accH[ai] = prev + psi;
-    }
-}
-
 // view HS3 (h^{***,k}) for the fine velocity stage 3
+template <bool BAND>
 __device__ __forceinline__ double view3(const Bounds &b, const StepConst &sc, const PredConst &p,
                                         const FineArrays &a, const double *hnext, int x) {
-    const int cl = ccls(b, x);
+    const int cl = cclass<BAND>(b, x);
     if (cl == 2) return sc.b3 * hnext[x] + sc.om2b3 * a.h2[x] + sc.b3 * a.hk[x];
     if (cl == 1) {
         const double hP0 = pred_level(p, a, x);
@@ -370,19 +323,149 @@ __device__ __forceinline__ double view3(const Bounds &b, const StepConst &sc, co
     return hs3c(sc, a.h3, a.h2, a.hN, x);
 }
 
+// Fine stage 1 (subeqn fine_s1): h_bar^{n,k+1/3} = h^{n,k} + dt/(3M) Psi(u^{n,k}, h^{n,k}) on F.
+template <int G, bool BAND>
+__global__ void __launch_bounds__(TPB) k_fine_s1(DevMesh m, FineArrays a, const double *__restrict__ uk,
+                                                 double *__restrict__ out, StepConst sc, PredConst p, int k,
+                                                 int begin, int end, DevError *err) {
+    const int i = begin + blockIdx.x * TPB + threadIdx.x;
+    if (i >= end) return;
+    int2 r[G];
+    load_row<G>(m, i, r);
+    const int n = m.nEoC[i];
+    const double Hi = a.hk[i];
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+        if (j < n) {
+            bool pos;
+            const int e = decode(r[j].x, pos);
+            acc = acc + psi_term(pos, Hi, view0<BAND>(m.cb, p, a, r[j].y), uk[e], m.dv[e]);
+        }
+    }
+    const double psi = -acc / m.areaCell[i];
+    const double v = Hi + sc.c1f * psi;
+    out[i] = v;
+    if (!(v > 0.0)) report(err, K_FINE_S1, k, i, v);
+}
+
+// Fine stage 2 (subeqn fine_s2): h_bar^{n,k+1/2} = h^{n,k} + dt/(2M) Psi(u_bar^{n,k+1/3}, h_bar^{n,k+1/3}),
+// u_bar^{n,k+1/3}_e = u^{n,k}_e + dt/(3M) (Phi^fast_e(h^{*,k}) + S_e) recomputed per edge.
+template <int G, bool BAND>
+__global__ void __launch_bounds__(TPB, BAND ? 1 : FBLTS_MINB) k_fine_s2(DevMesh m, FineArrays a, const double *__restrict__ uk,
+                                                 const double *__restrict__ S, double *__restrict__ out,
+                                                 StepConst sc, PredConst p, int k, int begin, int end,
+                                                 DevError *err) {
+    const int i = begin + blockIdx.x * TPB + threadIdx.x;
+    if (i >= end) return;
+    int2 r[G];
+    load_row<G>(m, i, r);
+    const int n = m.nEoC[i];
+    double Hi, HSi;
+    view1<BAND>(m.cb, sc, p, a, i, Hi, HSi);
+    const double zbi = m.zb[i];
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+        if (j < n) {
+            bool pos;
+            const int e = decode(r[j].x, pos);
+            const int nb = r[j].y;
+            double Hn, HSn;
+            view1<BAND>(m.cb, sc, p, a, nb, Hn, HSn);
+            const double zbn = m.zb[nb];
+            const double dc = m.dc[e];
+            const double phi = pos ? phi_fast(sc.g, HSi, zbi, HSn, zbn, dc) : phi_fast(sc.g, HSn, zbn, HSi, zbi, dc);
+            const double ue = uk[e] + sc.c1f * (phi + S[e]);
+            acc = acc + psi_term(pos, Hi, Hn, ue, m.dv[e]);
+        }
+    }
+    const double psi = -acc / m.areaCell[i];
+    const double v = a.hk[i] + sc.c2f * psi;
+    out[i] = v;
+    if (!(v > 0.0)) report(err, K_FINE_S2, k, i, v);
+}
+
+// Fine stage 3 on F (subeqn fine_s3) fused with the correction summand on IF-1 u IF-2
+// (eq. if_correction, "accumulated during the fine advancement step", P:L787):
+//   F:      h^{n,k+1} = h^{n,k} + dt/M Psi(u_bar^{n,k+1/2}, h_bar^{n,k+1/2})
+//   IF:     accH += Psi(u_bar^{n,k+1/2}, h_bar^{n,k+1/2})          (views, reading Q11/Q14)
+// Edge velocity u_bar^{n,k+1/2} by edge region: F_E -> u^{n,k} + dt/(2M)(Phi^fast(h^{**,k}) + S);
+// IF-1_E -> predicted (k/M) u~^{n+1} + (1/M) u~^{n+1/2} + (1-(k+1)/M) u^n with the tilde data
+// recomputed from the coarse thicknesses; IF-2_E / int_E -> coarse u~^{n+1/2}.
+template <int G, bool BAND>
+__global__ void __launch_bounds__(TPB, BAND ? 1 : FBLTS_MINB) k_fine_s3(DevMesh m, FineArrays a, const double *__restrict__ uN,
+                                                 const double *__restrict__ uk, const double *__restrict__ S,
+                                                 double *__restrict__ hnext, double *__restrict__ accH,
+                                                 StepConst sc, PredConst p, int k, int begin, int end,
+                                                 DevError *err) {
+    const int i = begin + blockIdx.x * TPB + threadIdx.x;
+    if (i >= end) return;
+    int2 r[G];
+    load_row<G>(m, i, r);
+    const int n = m.nEoC[i];
+    double Hi, HSi;
+    view2<BAND>(m.cb, sc, p, a, i, Hi, HSi);
+    const double zbi = m.zb[i];
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+        if (j < n) {
+            bool pos;
+            const int e = decode(r[j].x, pos);
+            const int nb = r[j].y;
+            double Hn, HSn;
+            view2<BAND>(m.cb, sc, p, a, nb, Hn, HSn);
+            const double dc = m.dc[e];
+            double ue;
+            const int ec = eclass<BAND>(m.eb, e);
+            if (ec == 3) {
+                const double zbn = m.zb[nb];
+                const double phi = pos ? phi_fast(sc.g, HSi, zbi, HSn, zbn, dc) : phi_fast(sc.g, HSn, zbn, HSi, zbi, dc);
+                ue = uk[e] + sc.c2f * (phi + S[e]);
+            } else {
+                const int c0 = pos ? i : nb, c1 = pos ? nb : i;
+                const double zb0 = m.zb[c0], zb1 = m.zb[c1];
+                const double phi2 = phi_fast(sc.g, hs2c(sc, a.h2, a.hN, c0), zb0, hs2c(sc, a.h2, a.hN, c1), zb1, dc);
+                const double u2 = uN[e] + sc.c2 * (phi2 + S[e]);
+                if (ec == 2) {
+                    const double phi3 = phi_fast(sc.g, hs3c(sc, a.h3, a.h2, a.hN, c0), zb0,
+                                                 hs3c(sc, a.h3, a.h2, a.hN, c1), zb1, dc);
+                    const double u3 = uN[e] + sc.c3 * (phi3 + S[e]);
+                    ue = p.a * u3 + p.b * u2 + p.c * uN[e];
+                } else {
+                    ue = u2;
+                }
+            }
+            acc = acc + psi_term(pos, Hi, Hn, ue, m.dv[e]);
+        }
+    }
+    const double psi = -acc / m.areaCell[i];
+    if (!BAND || i >= m.cb.f) {
+        const double v = a.hk[i] + sc.c3f * psi;
+        hnext[i] = v;
+        if (!(v > 0.0)) report(err, K_FINE_S3, k, i, v);
+    } else {
+        const int ai = i - m.cb.if2;
+        const double prev = k == 0 ? 0.0 : accH[ai];
+        accH[ai] = prev + psi;
+    }
+}
+
 // Fine velocity stage 3 (subeqn fine_s3) on F_E fused with the momentum correction summand on
 // IF-1_E u IF-2_E (eq. if_correction): F_E: u^{n,k+1} = u^{n,k} + dt/M (Phi^fast(h^{***,k}) + S);
 // IF_E: accU += Phi^fast(h^{***,k}) + S.
+template <bool BAND>
 __global__ void __launch_bounds__(TPB) k_fine_vel(DevMesh m, FineArrays a, const double *__restrict__ hnext,
                                                   const double *__restrict__ uk, const double *__restrict__ S,
                                                   double *__restrict__ unext, double *__restrict__ accU,
-                                                  StepConst sc, PredConst p, int k) {
-    const int e = m.eb.if2 + blockIdx.x * TPB + threadIdx.x;
-    if (e >= m.eb.end) return;
+                                                  StepConst sc, PredConst p, int k, int begin, int end) {
+    const int e = begin + blockIdx.x * TPB + threadIdx.x;
+    if (e >= end) return;
     const int2 c = m.coe[e];
-    const double phi = phi_fast(sc.g, view3(m.cb, sc, p, a, hnext, c.x), m.zb[c.x],
-                                view3(m.cb, sc, p, a, hnext, c.y), m.zb[c.y], m.dc[e]);
-    if (e >= m.eb.f) {
+    const double phi = phi_fast(sc.g, view3<BAND>(m.cb, sc, p, a, hnext, c.x), m.zb[c.x],
+                                view3<BAND>(m.cb, sc, p, a, hnext, c.y), m.zb[c.y], m.dc[e]);
+    if (!BAND || e >= m.eb.f) {
         unext[e] = uk[e] + sc.c3f * (phi + S[e]);
     } else {
         const int ai = e - m.eb.if2;
@@ -452,7 +535,7 @@ __global__ void __launch_bounds__(TPB) k_diag_partial(DevMesh m, const double *_
     const int tid = blockIdx.x * TPB + threadIdx.x;
     const int T = gridDim.x * TPB;
     DD mass{0.0, 0.0}, gam{0.0, 0.0};
-    double hmin = 1.0 / 0.0, numax = 0.0;
+    double hmin = (double)INFINITY, numax = 0.0;
     for (int i = tid; i < m.cb.end; i += T) {
         dd_add(mass, m.areaCell[i] * h[i]);
         hmin = fmin(hmin, h[i]);
@@ -504,7 +587,7 @@ __global__ void __launch_bounds__(TPB) k_diag_partial(DevMesh m, const double *_
 __global__ void k_diag_final(const double *__restrict__ part, int nb, double *__restrict__ out) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     DD mass{0.0, 0.0}, gam{0.0, 0.0};
-    double hmin = 1.0 / 0.0, numax = 0.0;
+    double hmin = (double)INFINITY, numax = 0.0;
     for (int b = 0; b < nb; ++b) {
         mass = dd_merge(mass, DD{part[b * 6 + 0], part[b * 6 + 1]});
         gam = dd_merge(gam, DD{part[b * 6 + 2], part[b * 6 + 3]});
@@ -518,27 +601,53 @@ __global__ void k_diag_final(const double *__restrict__ part, int nb, double *__
 }
 
 // ---------------------------------------------------------------- launchers
+// G = row stride of ec = unrolled slot bound (6, 8 or 16 >= maxEdges).
+#define FBLTS_DISPATCH_G(ecS, ...) \
+    do {                           \
+        if ((ecS) == 6) {          \
+            constexpr int G = 6;   \
+            __VA_ARGS__;           \
+        } else if ((ecS) == 8) {   \
+            constexpr int G = 8;   \
+            __VA_ARGS__;           \
+        } else {                   \
+            constexpr int G = 16;  \
+            __VA_ARGS__;           \
+        }                          \
+    } while (0)
+
 void launch_slow_pre(const DevMesh &m, const DevState &st, const double *h, const double *u, cudaStream_t s) {
     const unsigned nbV = nblocks(m.nV), nbC = nblocks(m.nC), nbE = nblocks(m.nE);
-    k_slow_pre<<<nbV + nbC + nbE, TPB, 0, s>>>(m, h, u, st.q, st.K, st.F, nbV, nbC);
+    FBLTS_DISPATCH_G(m.ecS, k_slow_pre<G><<<nbV + nbC + nbE, TPB, 0, s>>>(m, h, u, st.q, st.K, st.F, nbV, nbC));
 }
 void launch_slow_edge(const DevMesh &m, const DevState &st, const double *h, const StepConst &sc, cudaStream_t s) {
-    k_slow_edge<<<nblocks(m.nE), TPB, 0, s>>>(m, h, st.q, st.K, st.F, st.S, sc.rho0);
+    if (m.maxE2 <= 10)
+        k_slow_edge<10><<<nblocks(m.nE), TPB, 0, s>>>(m, h, st.q, st.K, st.F, st.S, sc.rho0);
+    else if (m.maxE2 <= 14)
+        k_slow_edge<14><<<nblocks(m.nE), TPB, 0, s>>>(m, h, st.q, st.K, st.F, st.S, sc.rho0);
+    else
+        k_slow_edge<30><<<nblocks(m.nE), TPB, 0, s>>>(m, h, st.q, st.K, st.F, st.S, sc.rho0);
 }
 void launch_coarse_s1(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
                       const StepConst &sc, cudaStream_t s) {
     const int end = m.cb.fl[5];
-    if (end > 0) k_coarse_stage<1><<<nblocks(end), TPB, 0, s>>>(m, hN, hN, uN, st.S, st.h1, sc, end, st.err);
+    if (end > 0)
+        FBLTS_DISPATCH_G(m.ecS, k_coarse_stage<G, 1><<<nblocks(end), TPB, 0, s>>>(m, hN, hN, uN, st.S, st.h1, sc,
+                                                                                   end, st.err));
 }
 void launch_coarse_s2(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
                       const StepConst &sc, cudaStream_t s) {
     const int end = m.cb.fl[3];
-    if (end > 0) k_coarse_stage<2><<<nblocks(end), TPB, 0, s>>>(m, hN, st.h1, uN, st.S, st.h2, sc, end, st.err);
+    if (end > 0)
+        FBLTS_DISPATCH_G(m.ecS, k_coarse_stage<G, 2><<<nblocks(end), TPB, 0, s>>>(m, hN, st.h1, uN, st.S, st.h2, sc,
+                                                                                   end, st.err));
 }
 void launch_coarse_s3(const DevMesh &m, const DevState &st, const double *hN, const double *uN, double *hNew,
                       const StepConst &sc, cudaStream_t s) {
     const int end = m.cb.fl[1];
-    if (end > 0) k_coarse_stage<3><<<nblocks(end), TPB, 0, s>>>(m, hN, st.h2, uN, st.S, hNew, sc, end, st.err);
+    if (end > 0)
+        FBLTS_DISPATCH_G(m.ecS, k_coarse_stage<G, 3><<<nblocks(end), TPB, 0, s>>>(m, hN, st.h2, uN, st.S, hNew, sc,
+                                                                                   end, st.err));
 }
 void launch_coarse_vel(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
                        const double *hNew, double *uNew, const StepConst &sc, cudaStream_t s) {
@@ -554,32 +663,50 @@ static FineArrays fine_arrays(const DevState &st, const double *hN, const double
     a.hk = hk;
     return a;
 }
+// Fine kernels: BAND instance over [b0, b1) (needs the region views), DEEP over [b1, end).
 void launch_fine_s1(const DevMesh &m, const DevState &st, const double *hN, const double *hNew, const double *hk,
                     const double *uk, const StepConst &sc, const PredConst &pc, int k, cudaStream_t s) {
-    const int n = m.cb.end - m.cb.f;
-    if (n > 0) k_fine_s1<<<nblocks(n), TPB, 0, s>>>(m, fine_arrays(st, hN, hNew, hk), uk, st.h1, sc, pc, k, st.err);
+    const FineArrays a = fine_arrays(st, hN, hNew, hk);
+    const int b0 = m.cb.f, b1 = m.cb.fl[1], end = m.cb.end;
+    FBLTS_DISPATCH_G(m.ecS, {
+        if (b1 > b0) k_fine_s1<G, true><<<nblocks(b1 - b0), TPB, 0, s>>>(m, a, uk, st.h1, sc, pc, k, b0, b1, st.err);
+        if (end > b1) k_fine_s1<G, false><<<nblocks(end - b1), TPB, 0, s>>>(m, a, uk, st.h1, sc, pc, k, b1, end, st.err);
+    });
 }
 void launch_fine_s2(const DevMesh &m, const DevState &st, const double *hN, const double *hNew, const double *hk,
                     const double *uk, const StepConst &sc, const PredConst &pc, int k, cudaStream_t s) {
-    const int n = m.cb.end - m.cb.f;
-    if (n > 0)
-        k_fine_s2<<<nblocks(n), TPB, 0, s>>>(m, fine_arrays(st, hN, hNew, hk), uk, st.S, st.h2, sc, pc, k, st.err);
+    const FineArrays a = fine_arrays(st, hN, hNew, hk);
+    const int b0 = m.cb.f, b1 = m.cb.fl[1], end = m.cb.end;
+    FBLTS_DISPATCH_G(m.ecS, {
+        if (b1 > b0)
+            k_fine_s2<G, true><<<nblocks(b1 - b0), TPB, 0, s>>>(m, a, uk, st.S, st.h2, sc, pc, k, b0, b1, st.err);
+        if (end > b1)
+            k_fine_s2<G, false><<<nblocks(end - b1), TPB, 0, s>>>(m, a, uk, st.S, st.h2, sc, pc, k, b1, end, st.err);
+    });
 }
 void launch_fine_s3(const DevMesh &m, const DevState &st, const double *hN, const double *uN, const double *hNew,
                     const double *hk, const double *uk, double *hnext, const StepConst &sc, const PredConst &pc,
                     int k, cudaStream_t s) {
-    const int n = m.cb.end - m.cb.if2;
-    if (n > 0)
-        k_fine_s3<<<nblocks(n), TPB, 0, s>>>(m, fine_arrays(st, hN, hNew, hk), uN, uk, st.S, hnext, st.accH, sc,
-                                             pc, k, st.err);
+    const FineArrays a = fine_arrays(st, hN, hNew, hk);
+    const int b0 = m.cb.if2, b1 = m.cb.fl[1], end = m.cb.end;
+    FBLTS_DISPATCH_G(m.ecS, {
+        if (b1 > b0)
+            k_fine_s3<G, true><<<nblocks(b1 - b0), TPB, 0, s>>>(m, a, uN, uk, st.S, hnext, st.accH, sc, pc, k, b0,
+                                                                 b1, st.err);
+        if (end > b1)
+            k_fine_s3<G, false><<<nblocks(end - b1), TPB, 0, s>>>(m, a, uN, uk, st.S, hnext, st.accH, sc, pc, k, b1,
+                                                                   end, st.err);
+    });
 }
 void launch_fine_vel(const DevMesh &m, const DevState &st, const double *hN, const double *hNew, const double *hk,
                      const double *hnext, const double *uk, double *unext, const StepConst &sc,
                      const PredConst &pc, int k, cudaStream_t s) {
-    const int n = m.eb.end - m.eb.if2;
-    if (n > 0)
-        k_fine_vel<<<nblocks(n), TPB, 0, s>>>(m, fine_arrays(st, hN, hNew, hk), hnext, uk, st.S, unext, st.accU,
-                                              sc, pc, k);
+    const FineArrays a = fine_arrays(st, hN, hNew, hk);
+    const int b0 = m.eb.if2, b1 = m.eb.fl[1], end = m.eb.end;
+    if (b1 > b0)
+        k_fine_vel<true><<<nblocks(b1 - b0), TPB, 0, s>>>(m, a, hnext, uk, st.S, unext, st.accU, sc, pc, k, b0, b1);
+    if (end > b1)
+        k_fine_vel<false><<<nblocks(end - b1), TPB, 0, s>>>(m, a, hnext, uk, st.S, unext, st.accU, sc, pc, k, b1, end);
 }
 void launch_correct(const DevMesh &m, const DevState &st, const double *hN, const double *uN, double *hNew,
                     double *uNew, const StepConst &sc, cudaStream_t s) {
