@@ -265,7 +265,7 @@ def arm_native(args):
     peak, peak_src = load_peaks()
     achieved = bm[dom] / (dom_ms * 1e-3) / 1e9
     traffic = load_traffic().get(args.config, {}).get(dom)
-    launches_per_step = sum(n for (_, n) in prof.values()) / n_prof
+    launches_per_step = s.counts()["kernels_per_step"]         # nodes of the captured step graph
     step_bytes = sum(bm[k] * n for k, (_, n) in prof.items()) / n_prof
     prof_total = sum(t for (t, _) in prof.values())
 

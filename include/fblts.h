@@ -129,9 +129,10 @@ int fblts_set_regions(fblts_ctx *ctx, const uint8_t *fine_mask);
 /* Region codes in ORIGINAL order (see FBLTS_REGION_*); either pointer may be NULL. */
 int fblts_get_labels(fblts_ctx *ctx, int8_t *cell_region, int8_t *edge_region);
 
-/* Local entity counts: out[0..7] = nCells, nEdges, nVertices, |int|, |IF-2|, |IF-1|,
- * |F^1|..  (out must hold 24 int64): cells per code 0..8 at out[3..11], edges per
- * code 0..8 at out[12..20], out[21] = owned cells, out[22] = owned edges, out[23] = reserved. */
+/* Entity counts (out must hold 24 int64): out[0..2] = nCells, nEdges, nVertices; cells per
+ * region code 0..8 at out[3..11], edges per code 0..8 at out[12..20]; out[21] = owned cells,
+ * out[22] = owned edges (equal to nCells, nEdges for one rank); out[23] = kernel launches per
+ * coarse step (nodes of the captured CUDA graph, 0 before the first fblts_step). */
 int fblts_get_counts(fblts_ctx *ctx, int64_t *out);
 
 /* Bytes of device workspace needed after set_regions. */

@@ -63,6 +63,7 @@ struct fblts_ctx {
     double t = 0.0;
     bool have_fine = false;
     cudaGraphExec_t exec[2]{};
+    size_t graph_nodes = 0;   // kernel launches per coarse step (nodes of the captured graph)
     // host-side staging of the permuted device tables (filled at set_regions)
     std::vector<int32_t> d_nEoC, d_ec, d_nEoE, d_eoe, d_eov, d_cov, d_coe, d_voe;
     std::vector<double> d_area, d_zb, d_dv, d_dc, d_W, d_kite, d_areaTri, d_fV, d_tau;
@@ -466,7 +467,7 @@ int fblts_get_counts(fblts_ctx *c, int64_t *out) {
     }
     out[21] = c->hm.nC;
     out[22] = c->hm.nE;
-    out[23] = 0;
+    out[23] = (int64_t)c->graph_nodes;
     return FBLTS_OK;
 }
 
@@ -718,6 +719,9 @@ int capture(fblts_ctx *c, int par) {
     CUDA_TRY(c, cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
     enqueue_step(c, par, c->cap, nullptr);
     CUDA_TRY(c, cudaStreamEndCapture(c->cap, &g));
+    size_t nodes = 0;
+    CUDA_TRY(c, cudaGraphGetNodes(g, nullptr, &nodes));
+    c->graph_nodes = nodes;
     CUDA_TRY(c, cudaGraphInstantiate(&c->exec[par], g, 0));
     CUDA_TRY(c, cudaGraphDestroy(g));
     return FBLTS_OK;

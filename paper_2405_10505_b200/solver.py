@@ -48,7 +48,8 @@ class Solver:
     def counts(self):
         c = abi.fblts_get_counts(self.ctx)
         return {"nCells": int(c[0]), "nEdges": int(c[1]), "nVertices": int(c[2]),
-                "cells_by_region": c[3:12].tolist(), "edges_by_region": c[12:21].tolist()}
+                "cells_by_region": c[3:12].tolist(), "edges_by_region": c[12:21].tolist(),
+                "kernels_per_step": int(c[23])}
 
     # --- state and stepping
     def set_state(self, h, u, t=0.0):
