@@ -109,7 +109,8 @@ typedef struct {
     void   *stream;      /* cudaStream_t of the caller (NULL = legacy default stream) */
     int32_t rank;        /* this process's rank (0 for single GPU) */
     int32_t nranks;      /* number of ranks (1 for single GPU) */
-    const void *nccl_id; /* 128-byte ncclUniqueId shared by all ranks, NULL if nranks == 1 */
+    const void *nccl_id; /* 128-byte ncclUniqueId shared by all ranks; NULL if nranks == 1, or for
+                            the members of a one-process loopback group (fblts_step_group) */
 } fblts_config;
 
 /* Create a context.  *out receives the handle (NULL on failure).
@@ -135,6 +136,16 @@ int fblts_get_labels(fblts_ctx *ctx, int8_t *cell_region, int8_t *edge_region);
  * coarse step (nodes of the captured CUDA graph, 0 before the first fblts_step). */
 int fblts_get_counts(fblts_ctx *ctx, int64_t *out);
 
+/* Halo exchange lists of this rank with `peer` (host logic, no device needed): which = 0 ring-1
+ * cells (after every thickness stage), 1 = rings 1-2 cells (end of step), 2 = remote-owned edges
+ * (end of step).  *n_send / *n_recv receive the counts; send_ids / recv_ids (may be NULL) receive
+ * the GLOBAL ids in exchange order (ascending global id, identical on both sides). */
+int fblts_get_halo(fblts_ctx *ctx, int32_t which, int32_t peer, int64_t *n_send, int64_t *n_recv,
+                   int64_t *send_ids, int64_t *recv_ids);
+
+/* 128-byte ncclUniqueId for a multi-rank context (call on rank 0, broadcast, pass as cfg.nccl_id). */
+int fblts_nccl_unique_id(void *out128);
+
 /* Bytes of device workspace needed after set_regions. */
 int fblts_workspace_size(fblts_ctx *ctx, size_t *bytes);
 
@@ -153,15 +164,23 @@ int fblts_set_state(fblts_ctx *ctx, const double *h, const double *u, double t);
 /* Enqueue n_coarse coarse steps on cfg.stream (asynchronous, CUDA-graph replay). */
 int fblts_step(fblts_ctx *ctx, int32_t n_coarse);
 
+/* Loopback group (testing the partitioned path on ONE device): the `n` contexts ctxs[r] (rank r of
+ * n, same device and stream, all bound and with state set) advance n_coarse steps together; each
+ * halo exchange is a device-to-device copy between their buffers.  No kernel waits on another. */
+int fblts_step_group(fblts_ctx **ctxs, int32_t n, int32_t n_coarse);
+int fblts_diagnostics_group(fblts_ctx **ctxs, int32_t n, double out[4]);
+
 /* Synchronise cfg.stream and report asynchronous device errors (POSITIVITY, CUDA). */
 int fblts_sync(fblts_ctx *ctx);
 
-/* Read back the state into HOST arrays in original order (synchronises). */
+/* Read back the state into HOST arrays in original order (synchronises).  With nranks > 1 only
+ * this rank's owned cells and the edges touching them are written; other entries are unchanged. */
 int fblts_get_state(fblts_ctx *ctx, double *h, double *u, double *t);
 
 /* out[4] = { total mass sum A_i h_i, total absolute vorticity sum_v (circulation_v + A_v f_v),
  *            min h, max Courant number (|u|+sqrt(g h_e)) dt_e / d_e } (Thms 1-2, eq. cfl).
- * Deterministic double-double reductions (synchronises). */
+ * Deterministic double-double reductions; with nranks > 1 the per-rank partials are all-gathered
+ * (NCCL) and combined in rank order, so every rank returns the same bits (synchronises). */
 int fblts_diagnostics(fblts_ctx *ctx, double out[4]);
 
 /* Instrumented replay for the roofline: runs n_coarse steps WITHOUT the graph, with

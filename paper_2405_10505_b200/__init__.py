@@ -2,13 +2,13 @@
 include/fblts.h, with a thin ctypes binding.  ``Solver`` needs a CUDA device; importing
 the binding fails loudly if libfblts.so has not been built (no CPU fallback)."""
 
-__all__ = ["Solver", "abi"]
+__all__ = ["Solver", "SolverGroup", "abi"]
 
 
 def __getattr__(name):
-    if name == "Solver":
-        from .solver import Solver
-        return Solver
+    if name in ("Solver", "SolverGroup"):
+        from . import solver
+        return getattr(solver, name)
     if name == "abi":
         from . import _abi
         return _abi

@@ -77,9 +77,15 @@ _lib_profile = _sig("fblts_profile", C.c_int, _vp, C.c_int32, _f64p, C.POINTER(C
 _lib_kname = _sig("fblts_kernel_name", C.c_char_p, C.c_int32)
 _lib_last_error = _sig("fblts_last_error", C.c_char_p, _vp)
 _lib_destroy = _sig("fblts_destroy", None, _vp)
+_i64p = C.POINTER(C.c_int64)
+_lib_halo = _sig("fblts_get_halo", C.c_int, _vp, C.c_int32, C.c_int32, _i64p, _i64p, _i64p, _i64p)
+_lib_uid = _sig("fblts_nccl_unique_id", C.c_int, C.c_void_p)
+_lib_step_group = _sig("fblts_step_group", C.c_int, C.POINTER(_vp), C.c_int32, C.c_int32)
+_lib_diag_group = _sig("fblts_diagnostics_group", C.c_int, C.POINTER(_vp), C.c_int32, _f64p)
 
 EXPORTED = ["fblts_create", "fblts_upload_mesh", "fblts_set_regions", "fblts_get_labels", "fblts_get_counts",
-            "fblts_workspace_size", "fblts_bind_workspace", "fblts_set_forcing", "fblts_set_state", "fblts_step",
+            "fblts_get_halo", "fblts_nccl_unique_id", "fblts_workspace_size", "fblts_bind_workspace",
+            "fblts_set_forcing", "fblts_set_state", "fblts_step", "fblts_step_group", "fblts_diagnostics_group",
             "fblts_sync", "fblts_get_state", "fblts_diagnostics", "fblts_profile", "fblts_kernel_name",
             "fblts_last_error", "fblts_destroy"]
 
@@ -101,9 +107,11 @@ def _arr(a, dtype):
 # ------------------------------------------------------------------ entry points
 def fblts_create(dt, M, g=9.81, beta=(0.531, 0.531, 0.313), rho0=1000.0, r=2, slow=True, device=0,
                  stream=None, rank=0, nranks=1, nccl_id=None):
+    """nccl_id: 128 bytes from fblts_nccl_unique_id() on rank 0 (None: single rank or loopback group)."""
+    idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id is not None else None
     cfg = fblts_config(dt=float(dt), g=float(g), beta=(C.c_double * 3)(*beta), rho0=float(rho0), M=int(M),
                        r=int(r), slow=1 if slow else 0, device=int(device), stream=stream, rank=int(rank),
-                       nranks=int(nranks), nccl_id=nccl_id)
+                       nranks=int(nranks), nccl_id=C.cast(idbuf, C.c_void_p) if idbuf is not None else None)
     ctx = _vp()
     rc = _lib_create(C.byref(ctx), C.byref(cfg))
     if rc != FBLTS_OK:
@@ -142,6 +150,38 @@ def fblts_get_labels(ctx, nCells, nEdges):
 def fblts_get_counts(ctx):
     out = np.zeros(24, np.int64)
     _check(ctx, _lib_counts(ctx, _ptr(out, C.c_int64)))
+    return out
+
+
+def fblts_get_halo(ctx, which, peer):
+    """(send global ids, recv global ids) of halo exchange `which` (0 ring-1 cells, 1 rings 1-2
+    cells, 2 remote-owned edges) with `peer`."""
+    ns, nr = C.c_int64(), C.c_int64()
+    _check(ctx, _lib_halo(ctx, int(which), int(peer), C.byref(ns), C.byref(nr), None, None))
+    snd = np.zeros(ns.value, np.int64)
+    rcv = np.zeros(nr.value, np.int64)
+    _check(ctx, _lib_halo(ctx, int(which), int(peer), C.byref(ns), C.byref(nr), _ptr(snd, C.c_int64),
+                          _ptr(rcv, C.c_int64)))
+    return snd, rcv
+
+
+def fblts_nccl_unique_id():
+    buf = (C.c_uint8 * 128)()
+    rc = _lib_uid(C.cast(buf, C.c_void_p))
+    if rc != FBLTS_OK:
+        raise FbltsError(rc, "ncclGetUniqueId failed")
+    return bytes(buf)
+
+
+def fblts_step_group(ctxs, n_coarse):
+    arr = (_vp * len(ctxs))(*[c.value if isinstance(c, _vp) else c for c in ctxs])
+    _check(ctxs[0], _lib_step_group(arr, len(ctxs), int(n_coarse)))
+
+
+def fblts_diagnostics_group(ctxs):
+    arr = (_vp * len(ctxs))(*[c.value if isinstance(c, _vp) else c for c in ctxs])
+    out = np.zeros(4)
+    _check(ctxs[0], _lib_diag_group(arr, len(ctxs), _ptr(out, C.c_double)))
     return out
 
 

@@ -12,6 +12,17 @@ LIB = os.path.join(HERE, "lib", "libfblts.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("host.cu", "kernels.cu")]
 HEADERS = [os.path.join(ROOT, "include", "fblts.h"), os.path.join(HERE, "csrc", "fblts_internal.h")]
 
+def nccl_root():
+    """The NCCL torch loads (the nvidia-nccl wheel), so the library shares torch's libnccl.so.2."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations if spec else []):
+        root = os.path.join(base, "nccl")
+        if os.path.exists(os.path.join(root, "include", "nccl.h")):
+            return root
+    raise RuntimeError("nccl.h not found in the nvidia-nccl wheel")
+
+
 NVCC_FLAGS = [
     "-std=c++17", "-O3", "-lineinfo",
     "--fmad=false",                       # canonical arithmetic: no FMA contraction (DESIGN.md)
@@ -39,8 +50,10 @@ def build(force=False, verbose=False):
         return LIB
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     extra = os.environ.get("FBLTS_NVCC_EXTRA", "").split()      # development knobs, e.g. -DFBLTS_MINB=8
+    nccl = nccl_root()
     cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(HERE, "csrc"),
-           "-o", LIB, *SOURCES]
+           "-I" + os.path.join(nccl, "include"), "-o", LIB, *SOURCES,
+           "-L" + os.path.join(nccl, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(nccl, "lib")]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)

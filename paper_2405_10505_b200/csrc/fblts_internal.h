@@ -32,7 +32,8 @@ struct Bounds {
 };
 
 struct DevMesh {
-    int32_t nC, nE, nV;               // local entity counts
+    int32_t nC, nE, nV;               // local entity counts (owned + halo)
+    int32_t nOwnC, nOwnE;              // owned cells [0, nOwnC); edges touching owned cells [0, nOwnE)
     int32_t strideC, strideE, strideV; // padded slot strides
     int32_t maxE, maxE2;
     int32_t ecS;                       // row stride of ec (G: 6, 8 or 16 >= maxEdges)
@@ -53,7 +54,10 @@ struct DevMesh {
     const double *__restrict__ kite;   // [3][strideV]
     const double *__restrict__ areaTri; // [nV]
     const double *__restrict__ fV;     // [nV]
-    Bounds cb, eb;                     // cell / edge region bounds
+    const uint8_t *__restrict__ vOwn;  // [nV] 1 if this rank reports the vertex in the diagnostics
+    const uint8_t *__restrict__ eOwn;  // [nE] 1 if this rank reports the edge in the diagnostics
+    Bounds cb, eb;                     // owned cell / edge region bounds (cb.end = nOwnC, eb.end = nOwnE)
+    Bounds cbh;                        // halo cell block [nOwnC, nC), region-major, absolute indices
 };
 
 // Device error record (positivity / NaN), first failure wins.
@@ -91,6 +95,8 @@ struct DevState {
     double *stage;                      // staging for set/get_state (max(nC, nE) doubles)
     int32_t *cellOld, *edgeOld;         // new -> old permutation (device)
     double *diag;                       // reduction scratch
+    double *sendbuf, *recvbuf;          // halo exchange buffers
+    int32_t *xidx;                      // halo exchange index lists (all exchanges, send then recv)
     DevError *err;
 };
 
@@ -122,6 +128,9 @@ void launch_correct(const DevMesh &m, const DevState &st, const double *hN, cons
 void launch_permute_in(const int32_t *old_of_new, const double *src, double *dst, int n, cudaStream_t s);
 void launch_permute_out(const int32_t *old_of_new, const double *src, double *dst, int n, cudaStream_t s);
 // diagnostics: writes out[4] (device) = mass, Gamma, min h, max nu
+// halo exchange: buf[k] = a[idx[k]] (pack), a[idx[k]] = buf[k] (unpack)
+void launch_pack(const int32_t *idx, const double *a, double *buf, int n, cudaStream_t s);
+void launch_unpack(const int32_t *idx, const double *buf, double *a, int n, cudaStream_t s);
 void launch_diagnostics(const DevMesh &m, const DevState &st, const double *h, const double *u,
                         const StepConst &sc, double *out_dev, cudaStream_t s);
 

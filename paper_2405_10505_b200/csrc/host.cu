@@ -1,6 +1,7 @@
 // host.cu -- C ABI of libfblts.so (include/fblts.h): context, mesh validation, LTS
 // region labelling, region-major + space-filling-curve renumbering,
-// workspace carving, CUDA-graph step replay, state I/O and diagnostics.
+// partition into per-rank subdomains with halo lists, workspace carving, CUDA-graph step
+// replay with NCCL halo exchanges, state I/O and diagnostics.
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
@@ -11,6 +12,8 @@
 #include <type_traits>
 #include <string>
 #include <vector>
+
+#include <nccl.h>
 
 #include "fblts.h"
 #include "fblts_internal.h"
@@ -30,15 +33,28 @@ struct HostMesh {
     std::vector<double> W, kite, areaCell, areaTri, dv, dc, fV, H, x, y, z;
 };
 
-struct Region {
+struct Region {                 // global LTS labels (identical on every rank)
     std::vector<int8_t> cell, edge;
-    std::vector<int32_t> cellOld, cellNew, edgeOld, edgeNew, vertOld, vertNew;
-    Bounds cb{}, eb{};
     int64_t ccount[9]{}, ecount[9]{};
 };
 
-struct Buf {
-    size_t off, bytes;
+// One halo exchange pattern: for each peer, the local indices this rank sends (its owned
+// entries that the peer holds as halo) and receives (its halo entries owned by the peer),
+// both in ascending global-id order so the two sides agree element by element.
+struct Xchg {
+    std::vector<int32_t> sendIdx, recvIdx;
+    std::vector<int64_t> sendOff, recvOff;   // [nranks + 1]
+    size_t sendAt = 0, recvAt = 0;           // offsets of the lists inside the device xidx table
+};
+enum { X_C1 = 0, X_C2 = 1, X_E = 2, X_NUM = 3 };
+
+struct Local {                  // this rank's subdomain in local (device) numbering
+    int nOwnC = 0, nC = 0, nOwnE = 0, nE = 0, nV = 0;
+    std::vector<int32_t> cellGlob, edgeGlob, vertGlob;   // local -> global
+    Bounds cb{}, cbh{}, eb{};
+    int64_t ocount[9]{}, oecount[9]{};                   // owned cells / edges touching owned, per code
+    std::vector<uint8_t> vOwn, eOwn;
+    Xchg x[X_NUM];
 };
 
 }  // namespace
@@ -51,6 +67,7 @@ struct fblts_ctx {
     int phase = P_CREATED;
     HostMesh hm;
     Region rg;
+    Local lo;
     StepConst sc{};
     // device
     char *ws = nullptr;
@@ -64,12 +81,14 @@ struct fblts_ctx {
     bool have_fine = false;
     cudaGraphExec_t exec[2]{};
     size_t graph_nodes = 0;   // kernel launches per coarse step (nodes of the captured graph)
+    void *nccl = nullptr;     // ncclComm_t (nranks > 1)
+    unsigned char nccl_id[128]{};
     // host-side staging of the permuted device tables (filled at set_regions)
-    std::vector<int32_t> d_nEoC, d_ec, d_nEoE, d_eoe, d_eov, d_cov, d_coe, d_voe;
-    std::vector<double> d_area, d_zb, d_dv, d_dc, d_W, d_kite, d_areaTri, d_fV, d_tau;
-    int sC = 0, sE = 0, sV = 0, ecS = 6;
+    std::vector<int32_t> d_nEoC, d_ec, d_nEoE, d_eoe, d_eov, d_cov, d_coe, d_voe, d_xidx;
+    std::vector<double> d_area, d_zb, d_dv, d_dc, d_W, d_kite, d_areaTri, d_fV;
+    int sE = 0, sV = 0, ecS = 6;
+    size_t xmax = 1;           // largest send/recv buffer (doubles)
 };
-
 namespace {
 
 int fail(fblts_ctx *c, int code, const char *fmt, ...) {
@@ -171,6 +190,29 @@ std::vector<int32_t> hops(const HostMesh &m, const std::vector<int32_t> &coc, co
 
 int region_class(int code) { return code < 3 ? code : 3; }
 
+
+// ---------------------------------------------------------------- NCCL transport (nranks > 1)
+int nccl_init(fblts_ctx *c) {
+    ncclUniqueId id;
+    std::memcpy(&id, c->cfg.nccl_id, sizeof id);
+    ncclComm_t comm;
+    const ncclResult_t r = ncclCommInitRank(&comm, c->cfg.nranks, id, c->cfg.rank);
+    if (r != ncclSuccess) return fail(c, FBLTS_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    c->nccl = comm;
+    return FBLTS_OK;
+}
+
+void nccl_destroy(fblts_ctx *c) {
+    if (c->nccl) ncclCommDestroy((ncclComm_t)c->nccl);
+    c->nccl = nullptr;
+}
+
+#define NCCL_TRY(ctx, call)                                                                            \
+    do {                                                                                               \
+        ncclResult_t r_ = (call);                                                                      \
+        if (r_ != ncclSuccess) return fail(ctx, FBLTS_ERR_NCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
+    } while (0)
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -180,16 +222,28 @@ const char *fblts_kernel_name(int32_t kind) { return (kind >= 0 && kind < K_NUM)
 
 const char *fblts_last_error(const fblts_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
+int fblts_nccl_unique_id(void *out128) {
+    if (!out128) return FBLTS_ERR_INVALID_ARG;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return FBLTS_ERR_NCCL;
+    std::memcpy(out128, &id, sizeof id);
+    return FBLTS_OK;
+}
+
 int fblts_create(fblts_ctx **out, const fblts_config *cfg) {
     if (!out || !cfg) return FBLTS_ERR_INVALID_ARG;
     *out = nullptr;
     if (!(cfg->dt > 0.0) || cfg->M < 1 || cfg->r < 1 || !(cfg->g > 0.0) || !(cfg->rho0 > 0.0))
         return FBLTS_ERR_INVALID_ARG;
-    if (cfg->nranks != 1 || cfg->rank != 0) return FBLTS_ERR_INVALID_ARG;  // multi-rank: see DESIGN.md
+    if (cfg->nranks < 1 || cfg->nranks > 64 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return FBLTS_ERR_INVALID_ARG;
     // No CUDA call here: mesh upload, labelling and renumbering are host work, so a context
     // can be created (and its labels inspected) on a machine without a GPU.
     fblts_ctx *c = new fblts_ctx();
     c->cfg = *cfg;
+    if (cfg->nccl_id) {                          // the caller's buffer is only borrowed
+        std::memcpy(c->nccl_id, cfg->nccl_id, sizeof c->nccl_id);
+        c->cfg.nccl_id = c->nccl_id;
+    }
     c->stream = (cudaStream_t)cfg->stream;
     // canonical constants (computed once in double, SURVEY c.1)
     StepConst &s = c->sc;
@@ -299,6 +353,279 @@ int fblts_upload_mesh(fblts_ctx *c, const fblts_mesh *m) {
     return FBLTS_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// ---------------------------------------------------------------- partition + local subdomain
+// Dual-set partition: the fine set and the coarse set (int + IF) are each sorted
+// by space-filling-curve key and cut into nranks equal contiguous chunks; rank r owns chunk r of
+// both, so the coarse phase and the fine phase are each balanced.
+std::vector<int32_t> partition(const HostMesh &m, const Region &g, const std::vector<uint64_t> &key, int nranks) {
+    std::vector<int32_t> part(m.nC, 0);
+    if (nranks == 1) return part;
+    for (int fineSet = 0; fineSet < 2; ++fineSet) {
+        std::vector<int32_t> ids;
+        for (int i = 0; i < m.nC; ++i)
+            if ((g.cell[i] >= FBLTS_REGION_F1) == (fineSet == 1)) ids.push_back(i);
+        std::stable_sort(ids.begin(), ids.end(), [&](int a, int b) { return key[a] < key[b]; });
+        const size_t n = ids.size();
+        for (int r = 0; r < nranks; ++r)
+            for (size_t k = n * r / nranks; k < n * (r + 1) / nranks; ++k) part[ids[k]] = r;
+    }
+    return part;
+}
+
+// hop distance (0, 1, 2, 3 = farther) from the cells owned by rank p
+std::vector<int8_t> dist_from(const HostMesh &m, const std::vector<int32_t> &coc, const std::vector<int32_t> &part,
+                              int p) {
+    std::vector<int8_t> d(m.nC, 3);
+    for (int i = 0; i < m.nC; ++i)
+        if (part[i] == p) d[i] = 0;
+    for (int ring = 1; ring <= 2; ++ring)
+        for (int i = 0; i < m.nC; ++i)
+            if (d[i] == ring - 1)
+                for (int j = 0; j < m.nEoC[i]; ++j) {
+                    const int nb = coc[(size_t)i * m.maxE + j];
+                    if (d[nb] == 3) d[nb] = (int8_t)ring;
+                }
+    return d;
+}
+
+Bounds bounds_from(const int64_t *cnt, int begin, int end) {
+    Bounds b{};
+    b.if2 = begin + (int)cnt[0];
+    b.if1 = b.if2 + (int)cnt[1];
+    b.f = b.if1 + (int)cnt[2];
+    b.fl[0] = b.f;
+    for (int l = 1; l <= 5; ++l) b.fl[l] = b.fl[l - 1] + (int)cnt[2 + l];
+    b.end = end;
+    return b;
+}
+
+int build_local(fblts_ctx *c, const std::vector<int32_t> &coc) {
+    const HostMesh &m = c->hm;
+    const Region &g = c->rg;
+    Local &L = c->lo;
+    const int R = c->cfg.nranks, me = c->cfg.rank;
+    const std::vector<uint64_t> key = sfc_keys(m);
+    const std::vector<int32_t> part = partition(m, g, key, R);
+    const std::vector<int8_t> dme = dist_from(m, coc, part, me);
+    // ---- cells: owned (region-major, SFC) then halo rings 1-2 (region-major, ring, SFC)
+    std::vector<int32_t> own, halo;
+    for (int i = 0; i < m.nC; ++i) {
+        if (dme[i] == 0) own.push_back(i);
+        else if (dme[i] <= 2) halo.push_back(i);
+    }
+    std::stable_sort(own.begin(), own.end(), [&](int a, int b) {
+        if (g.cell[a] != g.cell[b]) return g.cell[a] < g.cell[b];
+        return key[a] < key[b];
+    });
+    std::stable_sort(halo.begin(), halo.end(), [&](int a, int b) {
+        if (g.cell[a] != g.cell[b]) return g.cell[a] < g.cell[b];
+        if (dme[a] != dme[b]) return dme[a] < dme[b];
+        return key[a] < key[b];
+    });
+    L.nOwnC = (int)own.size();
+    L.cellGlob = own;
+    L.cellGlob.insert(L.cellGlob.end(), halo.begin(), halo.end());
+    L.nC = (int)L.cellGlob.size();
+    std::vector<int32_t> cellLoc(m.nC, -1);
+    for (int i = 0; i < L.nC; ++i) cellLoc[L.cellGlob[i]] = i;
+    // ---- edges: touching owned cells (region-major, by owner), then the other edges of ring-1 cells
+    std::vector<int32_t> eOwnL, eRest;
+    std::vector<int8_t> emark(m.nE, 0);
+    for (int k = 0; k < L.nC; ++k) {
+        const int i = L.cellGlob[k];
+        if (dme[i] > 1) continue;
+        for (int j = 0; j < m.nEoC[i]; ++j) {
+            const int e = m.eoc[(size_t)i * m.maxE + j];
+            if (emark[e]) continue;
+            emark[e] = 1;
+            const bool touches = dme[m.coe[2 * e]] == 0 || dme[m.coe[2 * e + 1]] == 0;
+            (touches ? eOwnL : eRest).push_back(e);
+        }
+    }
+    auto eowner = [&](int e) { return std::min(cellLoc[m.coe[2 * e]], cellLoc[m.coe[2 * e + 1]]); };
+    std::stable_sort(eOwnL.begin(), eOwnL.end(), [&](int a, int b) {
+        if (g.edge[a] != g.edge[b]) return g.edge[a] < g.edge[b];
+        return eowner(a) < eowner(b);
+    });
+    std::stable_sort(eRest.begin(), eRest.end(), [&](int a, int b) { return eowner(a) < eowner(b); });
+    L.nOwnE = (int)eOwnL.size();
+    L.edgeGlob = eOwnL;
+    L.edgeGlob.insert(L.edgeGlob.end(), eRest.begin(), eRest.end());
+    L.nE = (int)L.edgeGlob.size();
+    std::vector<int32_t> edgeLoc(m.nE, -1);
+    for (int e = 0; e < L.nE; ++e) edgeLoc[L.edgeGlob[e]] = e;
+    // ---- vertices: those of the edges touching owned cells, by owner cell
+    std::vector<int32_t> verts;
+    std::vector<int8_t> vmark(m.nV, 0);
+    for (int k = 0; k < L.nOwnE; ++k) {
+        const int e = L.edgeGlob[k];
+        for (int s = 0; s < 2; ++s) {
+            const int v = m.voe[2 * e + s];
+            if (!vmark[v]) {
+                vmark[v] = 1;
+                verts.push_back(v);
+            }
+        }
+    }
+    auto vowner = [&](int v) {
+        int o = INT32_MAX;
+        for (int k = 0; k < 3; ++k) {
+            const int l = cellLoc[m.cov[3 * v + k]];
+            if (l >= 0) o = std::min(o, l);
+        }
+        return o;
+    };
+    std::stable_sort(verts.begin(), verts.end(), [&](int a, int b) { return vowner(a) < vowner(b); });
+    L.vertGlob = verts;
+    L.nV = (int)verts.size();
+    std::vector<int32_t> vertLoc(m.nV, -1);
+    for (int v = 0; v < L.nV; ++v) vertLoc[L.vertGlob[v]] = v;
+    // ---- bounds (owned cells, halo cells, edges touching owned)
+    std::fill(L.ocount, L.ocount + 9, 0);
+    std::fill(L.oecount, L.oecount + 9, 0);
+    int64_t hcount[9] = {0};
+    for (int k = 0; k < L.nOwnC; ++k) L.ocount[g.cell[L.cellGlob[k]]]++;
+    for (int k = L.nOwnC; k < L.nC; ++k) hcount[g.cell[L.cellGlob[k]]]++;
+    for (int k = 0; k < L.nOwnE; ++k) L.oecount[g.edge[L.edgeGlob[k]]]++;
+    L.cb = bounds_from(L.ocount, 0, L.nOwnC);
+    L.cbh = bounds_from(hcount, L.nOwnC, L.nC);
+    L.eb = bounds_from(L.oecount, 0, L.nOwnE);
+    // diagnostics ownership: the rank owning cellsOnVertex[v][0] / cellsOnEdge[e][0]
+    L.vOwn.assign(L.nV, 0);
+    for (int v = 0; v < L.nV; ++v) L.vOwn[v] = part[m.cov[3 * L.vertGlob[v]]] == me;
+    L.eOwn.assign(L.nE, 0);
+    for (int e = 0; e < L.nOwnE; ++e) L.eOwn[e] = part[m.coe[2 * L.edgeGlob[e]]] == me;
+    c->have_fine = L.cb.f < L.nOwnC;
+    // ---- device tables in local numbering (dummy edge index nE for ring-2 slots outside the subdomain)
+    c->sE = pad32(L.nE);
+    c->sV = pad32(L.nV);
+    const int sE = c->sE, sV = c->sV, G = c->ecS = m.maxE <= 6 ? 6 : (m.maxE <= 8 ? 8 : 16);
+    c->d_nEoC.assign(L.nC, 0);
+    c->d_ec.assign((size_t)L.nC * G * 2, 0);
+    c->d_area.assign(L.nC, 0.0);
+    c->d_zb.assign(L.nC, 0.0);
+    for (int i = 0; i < L.nC; ++i) {
+        const int o = L.cellGlob[i];
+        c->d_nEoC[i] = m.nEoC[o];
+        c->d_area[i] = m.areaCell[o];
+        c->d_zb[i] = -m.H[o];
+        for (int j = 0; j < m.nEoC[o]; ++j) {
+            const int e = m.eoc[(size_t)o * m.maxE + j];
+            const int el = edgeLoc[e] >= 0 ? edgeLoc[e] : L.nE;
+            const int nb = cellLoc[coc[(size_t)o * m.maxE + j]];
+            c->d_ec[((size_t)i * G + j) * 2] = m.coe[2 * e] == o ? el : ~el;
+            c->d_ec[((size_t)i * G + j) * 2 + 1] = nb >= 0 ? nb : 0;
+        }
+    }
+    c->d_coe.assign((size_t)L.nE * 2, 0);
+    c->d_voe.assign((size_t)L.nE * 2, 0);
+    c->d_dv.assign(L.nE + 1, 0.0);
+    c->d_dc.assign(L.nE + 1, 0.0);
+    c->d_nEoE.assign(L.nE, 0);
+    c->d_eoe.assign((size_t)m.maxE2 * sE, 0);
+    c->d_W.assign((size_t)m.maxE2 * sE, 0.0);
+    for (int e = 0; e < L.nE; ++e) {
+        const int o = L.edgeGlob[e];
+        c->d_coe[2 * e] = cellLoc[m.coe[2 * o]];
+        c->d_coe[2 * e + 1] = cellLoc[m.coe[2 * o + 1]];
+        c->d_dv[e] = m.dv[o];
+        c->d_dc[e] = m.dc[o];
+        if (e >= L.nOwnE) continue;           // slow_edge only runs on edges touching owned cells
+        c->d_voe[2 * e] = vertLoc[m.voe[2 * o]];
+        c->d_voe[2 * e + 1] = vertLoc[m.voe[2 * o + 1]];
+        c->d_nEoE[e] = m.nEoE[o];
+        for (int j = 0; j < m.nEoE[o]; ++j) {
+            c->d_eoe[(size_t)j * sE + e] = edgeLoc[m.eoe[(size_t)o * m.maxE2 + j]];
+            c->d_W[(size_t)j * sE + e] = m.W[(size_t)o * m.maxE2 + j];
+        }
+    }
+    c->d_eov.assign((size_t)3 * sV, 0);
+    c->d_cov.assign((size_t)3 * sV, 0);
+    c->d_kite.assign((size_t)3 * sV, 0.0);
+    c->d_areaTri.assign(L.nV, 0.0);
+    c->d_fV.assign(L.nV, 0.0);
+    for (int v = 0; v < L.nV; ++v) {
+        const int o = L.vertGlob[v];
+        c->d_areaTri[v] = m.areaTri[o];
+        c->d_fV[v] = m.fV[o];
+        for (int k = 0; k < 3; ++k) {
+            const int e = m.eov[3 * o + k];
+            const int en = edgeLoc[e];
+            c->d_eov[(size_t)k * sV + v] = m.voe[2 * e + 1] == o ? en : ~en;
+            c->d_cov[(size_t)k * sV + v] = cellLoc[m.cov[3 * o + k]];
+            c->d_kite[(size_t)k * sV + v] = m.kite[3 * o + k];
+        }
+    }
+    // ---- halo exchanges (nranks > 1)
+    for (int x = 0; x < X_NUM; ++x) {
+        L.x[x] = Xchg();
+        L.x[x].sendOff.assign(R + 1, 0);
+        L.x[x].recvOff.assign(R + 1, 0);
+    }
+    c->xmax = 1;
+    if (R > 1) {
+        std::vector<std::vector<int32_t>> sendG[X_NUM], recvG[X_NUM];   // global ids per peer
+        for (int x = 0; x < X_NUM; ++x) {
+            sendG[x].assign(R, {});
+            recvG[x].assign(R, {});
+        }
+        for (int k = L.nOwnC; k < L.nC; ++k) {
+            const int i = L.cellGlob[k];
+            if (dme[i] == 1) recvG[X_C1][part[i]].push_back(i);
+            recvG[X_C2][part[i]].push_back(i);
+        }
+        for (int e = L.nOwnE; e < L.nE; ++e) {
+            const int o = L.edgeGlob[e];
+            recvG[X_E][part[m.coe[2 * o]]].push_back(o);
+        }
+        for (int p = 0; p < R; ++p) {
+            if (p == me) continue;
+            const std::vector<int8_t> dp = dist_from(m, coc, part, p);
+            for (int k = 0; k < L.nOwnC; ++k) {
+                const int i = L.cellGlob[k];
+                if (dp[i] == 1) sendG[X_C1][p].push_back(i);
+                if (dp[i] == 1 || dp[i] == 2) sendG[X_C2][p].push_back(i);
+            }
+            for (int k = 0; k < L.nOwnE; ++k) {
+                const int o = L.edgeGlob[k];
+                const int a = m.coe[2 * o], b = m.coe[2 * o + 1];
+                if (part[a] != me) continue;                       // canonical sender: owner of c0
+                if (dp[a] >= 1 && dp[b] >= 1 && std::min(dp[a], dp[b]) == 1) sendG[X_E][p].push_back(o);
+            }
+        }
+        for (int x = 0; x < X_NUM; ++x) {
+            const std::vector<int32_t> &loc = x == X_E ? edgeLoc : cellLoc;
+            Xchg &X = L.x[x];
+            for (int p = 0; p < R; ++p) {
+                std::sort(sendG[x][p].begin(), sendG[x][p].end());
+                std::sort(recvG[x][p].begin(), recvG[x][p].end());
+                for (int gid : sendG[x][p]) X.sendIdx.push_back(loc[gid]);
+                for (int gid : recvG[x][p]) X.recvIdx.push_back(loc[gid]);
+                X.sendOff[p + 1] = (int64_t)X.sendIdx.size();
+                X.recvOff[p + 1] = (int64_t)X.recvIdx.size();
+            }
+            c->xmax = std::max(c->xmax, std::max(X.sendIdx.size(), X.recvIdx.size()));
+        }
+    }
+    c->d_xidx.clear();
+    for (int x = 0; x < X_NUM; ++x) {
+        L.x[x].sendAt = c->d_xidx.size();
+        c->d_xidx.insert(c->d_xidx.end(), L.x[x].sendIdx.begin(), L.x[x].sendIdx.end());
+        L.x[x].recvAt = c->d_xidx.size();
+        c->d_xidx.insert(c->d_xidx.end(), L.x[x].recvIdx.begin(), L.x[x].recvIdx.end());
+    }
+    if (c->d_xidx.empty()) c->d_xidx.push_back(0);
+    return FBLTS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int fblts_set_regions(fblts_ctx *c, const uint8_t *fine_mask) {
     if (!c || !fine_mask) return FBLTS_ERR_INVALID_ARG;
     if (c->phase != P_MESH) return fail(c, FBLTS_ERR_ORDER, "set_regions: needs exactly one prior upload_mesh");
@@ -336,113 +663,12 @@ int fblts_set_regions(fblts_ctx *c, const uint8_t *fine_mask) {
         const bool fa = a >= 3, fb = b >= 3;
         g.edge[e] = (int8_t)(fa && fb ? std::min(a, b) : (fa ? a : (fb ? b : std::max(a, b))));
     }
-    // ---- renumbering: region-major, SFC within a region (cells), owner order (edges, vertices)
-    const std::vector<uint64_t> key = sfc_keys(m);
-    g.cellOld.resize(m.nC);
-    std::iota(g.cellOld.begin(), g.cellOld.end(), 0);
-    std::stable_sort(g.cellOld.begin(), g.cellOld.end(), [&](int a, int b) {
-        if (g.cell[a] != g.cell[b]) return g.cell[a] < g.cell[b];
-        return key[a] < key[b];
-    });
-    g.cellNew.resize(m.nC);
-    for (int i = 0; i < m.nC; ++i) g.cellNew[g.cellOld[i]] = i;
-    std::vector<int32_t> eown(m.nE);
-    for (int e = 0; e < m.nE; ++e) eown[e] = std::min(g.cellNew[m.coe[2 * e]], g.cellNew[m.coe[2 * e + 1]]);
-    g.edgeOld.resize(m.nE);
-    std::iota(g.edgeOld.begin(), g.edgeOld.end(), 0);
-    std::stable_sort(g.edgeOld.begin(), g.edgeOld.end(), [&](int a, int b) {
-        if (g.edge[a] != g.edge[b]) return g.edge[a] < g.edge[b];
-        return eown[a] < eown[b];
-    });
-    g.edgeNew.resize(m.nE);
-    for (int e = 0; e < m.nE; ++e) g.edgeNew[g.edgeOld[e]] = e;
-    std::vector<int32_t> vown(m.nV);
-    for (int v = 0; v < m.nV; ++v)
-        vown[v] = std::min(g.cellNew[m.cov[3 * v]], std::min(g.cellNew[m.cov[3 * v + 1]], g.cellNew[m.cov[3 * v + 2]]));
-    g.vertOld.resize(m.nV);
-    std::iota(g.vertOld.begin(), g.vertOld.end(), 0);
-    std::stable_sort(g.vertOld.begin(), g.vertOld.end(), [&](int a, int b) { return vown[a] < vown[b]; });
-    g.vertNew.resize(m.nV);
-    for (int v = 0; v < m.nV; ++v) g.vertNew[g.vertOld[v]] = v;
-    // ---- region bounds
     std::fill(g.ccount, g.ccount + 9, 0);
     std::fill(g.ecount, g.ecount + 9, 0);
     for (int i = 0; i < m.nC; ++i) g.ccount[g.cell[i]]++;
     for (int e = 0; e < m.nE; ++e) g.ecount[g.edge[e]]++;
-    auto bounds = [](const int64_t *cnt, int n) {
-        Bounds b{};
-        b.if2 = (int)cnt[0];
-        b.if1 = b.if2 + (int)cnt[1];
-        b.f = b.if1 + (int)cnt[2];
-        b.fl[0] = b.f;
-        for (int l = 1; l <= 5; ++l) b.fl[l] = b.fl[l - 1] + (int)cnt[2 + l];
-        b.end = n;
-        return b;
-    };
-    g.cb = bounds(g.ccount, m.nC);
-    g.eb = bounds(g.ecount, m.nE);
-    c->have_fine = g.cb.f < m.nC;
-    // ---- permuted device tables (host staging; uploaded at bind_workspace)
-    c->sC = pad32(m.nC);
-    c->sE = pad32(m.nE);
-    c->sV = pad32(m.nV);
-    const int sE = c->sE, sV = c->sV;
-    c->d_nEoC.assign(m.nC, 0);
-    c->ecS = m.maxE <= 6 ? 6 : (m.maxE <= 8 ? 8 : 16);
-    c->d_ec.assign((size_t)m.nC * c->ecS * 2, 0);
-    c->d_area.assign(m.nC, 0.0);
-    c->d_zb.assign(m.nC, 0.0);
-    for (int i = 0; i < m.nC; ++i) {
-        const int o = g.cellOld[i];
-        c->d_nEoC[i] = m.nEoC[o];
-        c->d_area[i] = m.areaCell[o];
-        c->d_zb[i] = -m.H[o];
-        for (int j = 0; j < m.nEoC[o]; ++j) {
-            const int e = m.eoc[(size_t)o * m.maxE + j];
-            const int en = g.edgeNew[e];
-            c->d_ec[((size_t)i * c->ecS + j) * 2] = m.coe[2 * e] == o ? en : ~en;
-            c->d_ec[((size_t)i * c->ecS + j) * 2 + 1] = g.cellNew[coc[(size_t)o * m.maxE + j]];
-        }
-    }
-    c->d_coe.assign((size_t)m.nE * 2, 0);
-    c->d_voe.assign((size_t)m.nE * 2, 0);
-    c->d_dv.assign(m.nE, 0.0);
-    c->d_dc.assign(m.nE, 0.0);
-    c->d_tau.assign(m.nE, 0.0);
-    c->d_nEoE.assign(m.nE, 0);
-    c->d_eoe.assign((size_t)m.maxE2 * sE, 0);
-    c->d_W.assign((size_t)m.maxE2 * sE, 0.0);
-    for (int e = 0; e < m.nE; ++e) {
-        const int o = g.edgeOld[e];
-        c->d_coe[2 * e] = g.cellNew[m.coe[2 * o]];
-        c->d_coe[2 * e + 1] = g.cellNew[m.coe[2 * o + 1]];
-        c->d_voe[2 * e] = g.vertNew[m.voe[2 * o]];
-        c->d_voe[2 * e + 1] = g.vertNew[m.voe[2 * o + 1]];
-        c->d_dv[e] = m.dv[o];
-        c->d_dc[e] = m.dc[o];
-        c->d_nEoE[e] = m.nEoE[o];
-        for (int j = 0; j < m.nEoE[o]; ++j) {
-            c->d_eoe[(size_t)j * sE + e] = g.edgeNew[m.eoe[(size_t)o * m.maxE2 + j]];
-            c->d_W[(size_t)j * sE + e] = m.W[(size_t)o * m.maxE2 + j];
-        }
-    }
-    c->d_eov.assign((size_t)3 * sV, 0);
-    c->d_cov.assign((size_t)3 * sV, 0);
-    c->d_kite.assign((size_t)3 * sV, 0.0);
-    c->d_areaTri.assign(m.nV, 0.0);
-    c->d_fV.assign(m.nV, 0.0);
-    for (int v = 0; v < m.nV; ++v) {
-        const int o = g.vertOld[v];
-        c->d_areaTri[v] = m.areaTri[o];
-        c->d_fV[v] = m.fV[o];
-        for (int k = 0; k < 3; ++k) {
-            const int e = m.eov[3 * o + k];
-            const int en = g.edgeNew[e];
-            c->d_eov[(size_t)k * sV + v] = m.voe[2 * e + 1] == o ? en : ~en;
-            c->d_cov[(size_t)k * sV + v] = g.cellNew[m.cov[3 * o + k]];
-            c->d_kite[(size_t)k * sV + v] = m.kite[3 * o + k];
-        }
-    }
+    const int rc = build_local(c, coc);
+    if (rc) return rc;
     c->phase = P_REGIONS;
     return FBLTS_OK;
 }
@@ -462,31 +688,47 @@ int fblts_get_counts(fblts_ctx *c, int64_t *out) {
     out[1] = c->hm.nE;
     out[2] = c->hm.nV;
     for (int k = 0; k < 9; ++k) {
-        out[3 + k] = c->rg.ccount[k];
-        out[12 + k] = c->rg.ecount[k];
+        out[3 + k] = c->lo.ocount[k];
+        out[12 + k] = c->lo.oecount[k];
     }
-    out[21] = c->hm.nC;
-    out[22] = c->hm.nE;
+    out[21] = c->lo.nOwnC;
+    out[22] = c->lo.nOwnE;
     out[23] = (int64_t)c->graph_nodes;
     return FBLTS_OK;
 }
 
+int fblts_get_halo(fblts_ctx *c, int32_t which, int32_t peer, int64_t *n_send, int64_t *n_recv, int64_t *send_ids,
+                   int64_t *recv_ids) {
+    if (!c || which < 0 || which >= X_NUM || peer < 0 || peer >= c->cfg.nranks) return FBLTS_ERR_INVALID_ARG;
+    if (c->phase < P_REGIONS) return fail(c, FBLTS_ERR_ORDER, "get_halo: call set_regions first");
+    const Xchg &X = c->lo.x[which];
+    const std::vector<int32_t> &glob = which == X_E ? c->lo.edgeGlob : c->lo.cellGlob;
+    const int64_t s0 = X.sendOff[peer], s1 = X.sendOff[peer + 1], r0 = X.recvOff[peer], r1 = X.recvOff[peer + 1];
+    if (n_send) *n_send = s1 - s0;
+    if (n_recv) *n_recv = r1 - r0;
+    if (send_ids)
+        for (int64_t k = s0; k < s1; ++k) send_ids[k - s0] = glob[X.sendIdx[k]];
+    if (recv_ids)
+        for (int64_t k = r0; k < r1; ++k) recv_ids[k - r0] = glob[X.recvIdx[k]];
+    return FBLTS_OK;
+}
+
+}  // extern "C"
+
 namespace {
 // workspace plan: the same sequence is used for sizing and for carving
 struct Plan {
-    std::vector<size_t> sizes;
     size_t total = 0;
     size_t add(size_t bytes) {
         const size_t off = total;
         total += (bytes + 255) / 256 * 256;
-        sizes.push_back(bytes);
         return off;
     }
 };
 
 size_t plan_workspace(fblts_ctx *c, char *base) {
     const HostMesh &m = c->hm;
-    const Region &g = c->rg;
+    const Local &L = c->lo;
     Plan p;
     auto put = [&](auto *&ptr, size_t count) {
         using T = std::remove_pointer_t<std::remove_reference_t<decltype(ptr)>>;
@@ -496,54 +738,61 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
     DevMesh &d = c->dm;
     DevState &s = c->ds;
     int32_t *nEoC, *nEoE, *eoe, *eov, *cov;
-    double *area, *zb, *W, *tau, *kite, *areaTri, *fV;
+    double *area, *zb, *W, *tau, *kite, *areaTri, *fV, *dv, *dc;
     int2 *coe, *voe, *ec;
-    double *dv, *dc;
-    put(nEoC, m.nC);
-    put(ec, (size_t)m.nC * c->ecS);
-    put(area, m.nC);
-    put(zb, m.nC);
-    put(coe, m.nE);
-    put(voe, m.nE);
-    put(dv, m.nE);
-    put(dc, m.nE);
-    put(tau, m.nE);
-    put(nEoE, m.nE);
+    uint8_t *vOwn, *eOwn;
+    const size_t nE1 = (size_t)L.nE + 1;               // + dummy edge
+    put(nEoC, L.nC);
+    put(ec, (size_t)L.nC * c->ecS);
+    put(area, L.nC);
+    put(zb, L.nC);
+    put(coe, L.nE);
+    put(voe, L.nE);
+    put(dv, nE1);
+    put(dc, nE1);
+    put(tau, L.nE);
+    put(nEoE, L.nE);
     put(eoe, (size_t)m.maxE2 * c->sE);
     put(W, (size_t)m.maxE2 * c->sE);
     put(eov, (size_t)3 * c->sV);
     put(cov, (size_t)3 * c->sV);
     put(kite, (size_t)3 * c->sV);
-    put(areaTri, m.nV);
-    put(fV, m.nV);
+    put(areaTri, L.nV);
+    put(fV, L.nV);
+    put(vOwn, L.nV);
+    put(eOwn, L.nE);
     double *hA, *hB, *uA, *uB;
-    put(hA, m.nC);
-    put(hB, m.nC);
-    put(s.h1, m.nC);
-    put(s.h2, m.nC);
-    put(s.hT, m.nC);
-    put(s.K, m.nC);
-    put(uA, m.nE);
-    put(uB, m.nE);
-    put(s.uT, m.nE);
-    put(s.S, m.nE);
-    put(s.F, m.nE);
-    put(s.q, m.nV);
-    put(s.accH, std::max(1, g.cb.f - g.cb.if2));
-    put(s.accU, std::max(1, g.eb.f - g.eb.if2));
+    put(hA, L.nC);
+    put(hB, L.nC);
+    put(s.h1, L.nC);
+    put(s.h2, L.nC);
+    put(s.hT, L.nC);
+    put(s.K, L.nC);
+    put(uA, nE1);
+    put(uB, nE1);
+    put(s.uT, nE1);
+    put(s.S, L.nE);
+    put(s.F, nE1);
+    put(s.q, L.nV);
+    put(s.accH, std::max(1, L.cb.f - L.cb.if2));
+    put(s.accU, std::max(1, L.eb.f - L.eb.if2));
     put(s.stage, std::max(m.nC, m.nE));
-    put(s.cellOld, m.nC);
-    put(s.edgeOld, m.nE);
-    put(s.diag, 296 * 6 + 8);
+    put(s.cellOld, L.nC);
+    put(s.edgeOld, L.nE);
+    put(s.diag, 296 * 6 + 8 + 6 * 64);
     put(s.err, 1);
+    put(s.sendbuf, c->xmax);
+    put(s.recvbuf, c->xmax);
+    put(s.xidx, c->d_xidx.size());
     if (base) {
-        d.nC = m.nC, d.nE = m.nE, d.nV = m.nV;
-        d.strideC = c->sC, d.strideE = c->sE, d.strideV = c->sV;
+        d.nC = L.nC, d.nE = L.nE, d.nV = L.nV, d.nOwnC = L.nOwnC, d.nOwnE = L.nOwnE;
+        d.strideC = L.nC, d.strideE = c->sE, d.strideV = c->sV;
         d.maxE = m.maxE, d.maxE2 = m.maxE2, d.ecS = c->ecS;
         d.nEoC = nEoC, d.ec = ec, d.areaCell = area, d.zb = zb;
         d.coe = coe, d.voe = voe, d.dv = dv, d.dc = dc, d.nEoE = nEoE, d.eoe = eoe, d.W = W, d.tau = tau;
         d.eov = eov, d.cov = cov, d.kite = kite, d.areaTri = areaTri, d.fV = fV;
-        d.cb = g.cb, d.eb = g.eb;
+        d.vOwn = vOwn, d.eOwn = eOwn;
+        d.cb = L.cb, d.eb = L.eb, d.cbh = L.cbh;
         c->hbuf[0] = hA, c->hbuf[1] = hB, c->ubuf[0] = uA, c->ubuf[1] = uB;
         s.hN = hA, s.hNew = hB, s.uN = uA, s.uNew = uB;
         c->diag_out = s.diag + 296 * 6;
@@ -551,6 +800,8 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
     return p.total;
 }
 }  // namespace
+
+extern "C" {
 
 int fblts_workspace_size(fblts_ctx *c, size_t *bytes) {
     if (!c || !bytes) return FBLTS_ERR_INVALID_ARG;
@@ -567,40 +818,44 @@ int fblts_bind_workspace(fblts_ctx *c, void *ptr, size_t bytes) {
     if ((uintptr_t)ptr % 256) return fail(c, FBLTS_ERR_INVALID_ARG, "bind_workspace: pointer not 256-B aligned");
     CUDA_TRY(c, cudaSetDevice(c->cfg.device));
     if (!c->cap) CUDA_TRY(c, cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
+    if (c->cfg.nranks > 1 && !c->nccl && c->cfg.nccl_id) {   // no id: loopback group member
+        const int rc = nccl_init(c);
+        if (rc) return rc;
+    }
     c->ws = (char *)ptr;
     c->ws_bytes = bytes;
+    CUDA_TRY(c, cudaMemsetAsync(ptr, 0, need, c->stream));
     plan_workspace(c, c->ws);
     cudaStream_t s = c->stream;
     DevMesh &d = c->dm;
     auto up = [&](const void *dst, const void *src, size_t n) {
         return cudaMemcpyAsync(const_cast<void *>(dst), src, n, cudaMemcpyHostToDevice, s);
     };
-    const HostMesh &m = c->hm;
+    const Local &L = c->lo;
     CUDA_TRY(c, up(d.nEoC, c->d_nEoC.data(), c->d_nEoC.size() * 4));
     CUDA_TRY(c, up(d.ec, c->d_ec.data(), c->d_ec.size() * 4));
-    CUDA_TRY(c, up(d.areaCell, c->d_area.data(), m.nC * 8));
-    CUDA_TRY(c, up(d.zb, c->d_zb.data(), m.nC * 8));
-    CUDA_TRY(c, up(d.coe, c->d_coe.data(), (size_t)m.nE * 8));
-    CUDA_TRY(c, up(d.voe, c->d_voe.data(), (size_t)m.nE * 8));
-    CUDA_TRY(c, up(d.dv, c->d_dv.data(), (size_t)m.nE * 8));
-    CUDA_TRY(c, up(d.dc, c->d_dc.data(), (size_t)m.nE * 8));
-    CUDA_TRY(c, up(d.tau, c->d_tau.data(), (size_t)m.nE * 8));
-    CUDA_TRY(c, up(d.nEoE, c->d_nEoE.data(), (size_t)m.nE * 4));
+    CUDA_TRY(c, up(d.areaCell, c->d_area.data(), (size_t)L.nC * 8));
+    CUDA_TRY(c, up(d.zb, c->d_zb.data(), (size_t)L.nC * 8));
+    CUDA_TRY(c, up(d.coe, c->d_coe.data(), (size_t)L.nE * 8));
+    CUDA_TRY(c, up(d.voe, c->d_voe.data(), (size_t)L.nE * 8));
+    CUDA_TRY(c, up(d.dv, c->d_dv.data(), c->d_dv.size() * 8));
+    CUDA_TRY(c, up(d.dc, c->d_dc.data(), c->d_dc.size() * 8));
+    CUDA_TRY(c, up(d.nEoE, c->d_nEoE.data(), (size_t)L.nE * 4));
     CUDA_TRY(c, up(d.eoe, c->d_eoe.data(), c->d_eoe.size() * 4));
     CUDA_TRY(c, up(d.W, c->d_W.data(), c->d_W.size() * 8));
     CUDA_TRY(c, up(d.eov, c->d_eov.data(), c->d_eov.size() * 4));
     CUDA_TRY(c, up(d.cov, c->d_cov.data(), c->d_cov.size() * 4));
     CUDA_TRY(c, up(d.kite, c->d_kite.data(), c->d_kite.size() * 8));
-    CUDA_TRY(c, up(d.areaTri, c->d_areaTri.data(), (size_t)m.nV * 8));
-    CUDA_TRY(c, up(d.fV, c->d_fV.data(), (size_t)m.nV * 8));
-    CUDA_TRY(c, up(c->ds.cellOld, c->rg.cellOld.data(), (size_t)m.nC * 4));
-    CUDA_TRY(c, up(c->ds.edgeOld, c->rg.edgeOld.data(), (size_t)m.nE * 4));
-    CUDA_TRY(c, cudaMemsetAsync(c->ds.S, 0, (size_t)m.nE * 8, s));
-    CUDA_TRY(c, cudaMemsetAsync(c->ds.err, 0, sizeof(DevError), s));
+    CUDA_TRY(c, up(d.areaTri, c->d_areaTri.data(), (size_t)L.nV * 8));
+    CUDA_TRY(c, up(d.fV, c->d_fV.data(), (size_t)L.nV * 8));
+    CUDA_TRY(c, up(d.vOwn, L.vOwn.data(), (size_t)L.nV));
+    CUDA_TRY(c, up(d.eOwn, L.eOwn.data(), (size_t)L.nE));
+    CUDA_TRY(c, up(c->ds.cellOld, L.cellGlob.data(), (size_t)L.nC * 4));
+    CUDA_TRY(c, up(c->ds.edgeOld, L.edgeGlob.data(), (size_t)L.nE * 4));
+    CUDA_TRY(c, up(c->ds.xidx, c->d_xidx.data(), c->d_xidx.size() * 4));
     CUDA_TRY(c, cudaStreamSynchronize(s));
-    // host staging of the device tables is no longer needed
+    // host staging of the big device tables is no longer needed
     std::vector<int32_t>().swap(c->d_ec);
-
     std::vector<int32_t>().swap(c->d_eoe);
     std::vector<double>().swap(c->d_W);
     c->phase = P_BOUND;
@@ -610,14 +865,15 @@ int fblts_bind_workspace(fblts_ctx *c, void *ptr, size_t bytes) {
 int fblts_set_forcing(fblts_ctx *c, const double *tau_n) {
     if (!c) return FBLTS_ERR_INVALID_ARG;
     if (c->phase < P_BOUND) return fail(c, FBLTS_ERR_ORDER, "set_forcing: bind the workspace first");
-    const int nE = c->hm.nE;
-    std::vector<double> t(nE, 0.0);
+    const Local &L = c->lo;
+    std::vector<double> t(L.nE, 0.0);
     if (tau_n)
-        for (int e = 0; e < nE; ++e) {
-            if (!std::isfinite(tau_n[e])) return fail(c, FBLTS_ERR_INVALID_ARG, "forcing[%d] not finite", e);
-            t[e] = tau_n[c->rg.edgeOld[e]];
+        for (int e = 0; e < L.nE; ++e) {
+            const double v = tau_n[L.edgeGlob[e]];
+            if (!std::isfinite(v)) return fail(c, FBLTS_ERR_INVALID_ARG, "forcing[%d] not finite", L.edgeGlob[e]);
+            t[e] = v;
         }
-    CUDA_TRY(c, cudaMemcpyAsync((void *)c->dm.tau, t.data(), (size_t)nE * 8, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync((void *)c->dm.tau, t.data(), (size_t)L.nE * 8, cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     return FBLTS_OK;
 }
@@ -630,12 +886,12 @@ int fblts_set_state(fblts_ctx *c, const double *h, const double *u, double t) {
     for (int e = 0; e < c->hm.nE; ++e)
         if (!std::isfinite(u[e])) return fail(c, FBLTS_ERR_STATE, "set_state: u[%d] not finite", e);
     cudaStream_t s = c->stream;
-    const int nC = c->hm.nC, nE = c->hm.nE;
+    const Local &L = c->lo;
     c->parity = 0;
-    CUDA_TRY(c, cudaMemcpyAsync(c->ds.stage, h, (size_t)nC * 8, cudaMemcpyHostToDevice, s));
-    launch_permute_in(c->ds.cellOld, c->ds.stage, c->hbuf[0], nC, s);
-    CUDA_TRY(c, cudaMemcpyAsync(c->ds.stage, u, (size_t)nE * 8, cudaMemcpyHostToDevice, s));
-    launch_permute_in(c->ds.edgeOld, c->ds.stage, c->ubuf[0], nE, s);
+    CUDA_TRY(c, cudaMemcpyAsync(c->ds.stage, h, (size_t)c->hm.nC * 8, cudaMemcpyHostToDevice, s));
+    launch_permute_in(c->ds.cellOld, c->ds.stage, c->hbuf[0], L.nC, s);
+    CUDA_TRY(c, cudaMemcpyAsync(c->ds.stage, u, (size_t)c->hm.nE * 8, cudaMemcpyHostToDevice, s));
+    launch_permute_in(c->ds.edgeOld, c->ds.stage, c->ubuf[0], L.nE, s);
     CUDA_TRY(c, cudaGetLastError());
     CUDA_TRY(c, cudaMemsetAsync(c->ds.err, 0, sizeof(DevError), s));
     CUDA_TRY(c, cudaStreamSynchronize(s));
@@ -660,8 +916,18 @@ struct Recorder {
     }
 };
 
-// Enqueue one coarse step reading hbuf[par], ubuf[par] and writing hbuf[1-par], ubuf[1-par].
-void enqueue_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
+// A phase is a run of kernels followed (except for a single rank) by one halo exchange of the
+// array it produced: ring 1 after every thickness stage, rings 1-2 of h and the remote-owned
+// edges of u at the end of the step.
+struct PhaseX {
+    int x;            // X_C1, X_C2 or -1
+    double *a;        // array exchanged
+    int x2;           // second exchange (X_E at the end of the step) or -1
+    double *a2;
+};
+
+// Enqueue phase `ph` of the step reading hbuf[par], ubuf[par]; returns false when past the end.
+bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec, PhaseX *px) {
     const DevMesh &m = c->dm;
     DevState st = c->ds;
     const StepConst &sc = c->sc;
@@ -670,55 +936,141 @@ void enqueue_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
     auto mark = [&](int k) {
         if (rec) rec->mark(k, s);
     };
-    if (c->cfg.slow) {
-        mark(K_SLOW_PRE);
-        launch_slow_pre(m, st, hN, uN, s);
-        mark(K_SLOW_EDGE);
-        launch_slow_edge(m, st, hN, sc, s);
-    }
-    mark(K_COARSE_S1);
-    launch_coarse_s1(m, st, hN, uN, sc, s);
-    mark(K_COARSE_S2);
-    launch_coarse_s2(m, st, hN, uN, sc, s);
-    mark(K_COARSE_S3);
-    launch_coarse_s3(m, st, hN, uN, hNew, sc, s);
-    mark(K_COARSE_VEL);
-    launch_coarse_vel(m, st, hN, uN, hNew, uNew, sc, s);
-    if (c->have_fine) {
-        const int M = sc.M;
-        auto hb = [&](int k) { return ((M - 1 - k) % 2 == 0) ? hNew : st.hT; };
-        auto ub = [&](int k) { return ((M - 1 - k) % 2 == 0) ? uNew : st.uT; };
-        for (int k = 0; k < M; ++k) {
-            PredConst pc;
-            pc.a = (double)k / (double)M;
-            pc.oma = 1.0 - pc.a;
-            pc.a1 = (double)(k + 1) / (double)M;
-            pc.oma1 = 1.0 - pc.a1;
-            pc.b = 1.0 / (double)M;
-            pc.c = 1.0 - (double)(k + 1) / (double)M;
-            const double *hk = k == 0 ? hN : hb(k - 1);
-            const double *uk = k == 0 ? uN : ub(k - 1);
-            double *hnext = hb(k), *unext = ub(k);
-            mark(K_FINE_S1);
-            launch_fine_s1(m, st, hN, hNew, hk, uk, sc, pc, k, s);
-            mark(K_FINE_S2);
-            launch_fine_s2(m, st, hN, hNew, hk, uk, sc, pc, k, s);
-            mark(K_FINE_S3);
-            launch_fine_s3(m, st, hN, uN, hNew, hk, uk, hnext, sc, pc, k, s);
-            mark(K_FINE_VEL);
-            launch_fine_vel(m, st, hN, hNew, hk, hnext, uk, unext, sc, pc, k, s);
+    const int M = sc.M;
+    auto hb = [&](int k) { return ((M - 1 - k) % 2 == 0) ? hNew : st.hT; };
+    auto ub = [&](int k) { return ((M - 1 - k) % 2 == 0) ? uNew : st.uT; };
+    auto pred = [&](int k) {
+        PredConst pc;
+        pc.a = (double)k / (double)M;
+        pc.oma = 1.0 - pc.a;
+        pc.a1 = (double)(k + 1) / (double)M;
+        pc.oma1 = 1.0 - pc.a1;
+        pc.b = 1.0 / (double)M;
+        pc.c = 1.0 - (double)(k + 1) / (double)M;
+        return pc;
+    };
+    auto fine_s1 = [&](int k) {
+        mark(K_FINE_S1);
+        launch_fine_s1(m, st, hN, hNew, k == 0 ? hN : hb(k - 1), k == 0 ? uN : ub(k - 1), sc, pred(k), k, s);
+    };
+    *px = PhaseX{-1, nullptr, -1, nullptr};
+    const int nfine = c->have_fine ? 3 * M : 0;
+    if (ph == 0) {
+        if (c->cfg.slow) {
+            mark(K_SLOW_PRE);
+            launch_slow_pre(m, st, hN, uN, s);
+            mark(K_SLOW_EDGE);
+            launch_slow_edge(m, st, hN, sc, s);
         }
-        mark(K_CORRECT);
-        launch_correct(m, st, hN, uN, hNew, uNew, sc, s);
+        mark(K_COARSE_S1);
+        launch_coarse_s1(m, st, hN, uN, sc, s);
+        *px = PhaseX{X_C1, st.h1, -1, nullptr};
+    } else if (ph == 1) {
+        mark(K_COARSE_S2);
+        launch_coarse_s2(m, st, hN, uN, sc, s);
+        *px = PhaseX{X_C1, st.h2, -1, nullptr};
+    } else if (ph == 2) {
+        mark(K_COARSE_S3);
+        launch_coarse_s3(m, st, hN, uN, hNew, sc, s);
+        *px = PhaseX{X_C1, hNew, -1, nullptr};
+    } else if (ph - 3 < nfine) {
+        const int q = ph - 3, k = q / 3, stg = q % 3;
+        if (stg == 0) {
+            if (k == 0) {
+                mark(K_COARSE_VEL);
+                launch_coarse_vel(m, st, hN, uN, hNew, uNew, sc, s);
+            } else {
+                mark(K_FINE_VEL);
+                launch_fine_vel(m, st, hN, hNew, k - 1 == 0 ? hN : hb(k - 2), hb(k - 1), k - 1 == 0 ? uN : ub(k - 2),
+                                ub(k - 1), sc, pred(k - 1), k - 1, s);
+            }
+            fine_s1(k);
+            *px = PhaseX{X_C1, st.h1, -1, nullptr};
+        } else if (stg == 1) {
+            mark(K_FINE_S2);
+            launch_fine_s2(m, st, hN, hNew, k == 0 ? hN : hb(k - 1), k == 0 ? uN : ub(k - 1), sc, pred(k), k, s);
+            *px = PhaseX{X_C1, st.h2, -1, nullptr};
+        } else {
+            mark(K_FINE_S3);
+            launch_fine_s3(m, st, hN, uN, hNew, k == 0 ? hN : hb(k - 1), k == 0 ? uN : ub(k - 1), hb(k), sc, pred(k),
+                           k, s);
+            *px = PhaseX{X_C1, hb(k), -1, nullptr};
+        }
+    } else if (ph == 3 + nfine) {
+        if (c->have_fine) {
+            mark(K_FINE_VEL);
+            launch_fine_vel(m, st, hN, hNew, M - 1 == 0 ? hN : hb(M - 2), hb(M - 1), M - 1 == 0 ? uN : ub(M - 2),
+                            ub(M - 1), sc, pred(M - 1), M - 1, s);
+            mark(K_CORRECT);
+            launch_correct(m, st, hN, uN, hNew, uNew, sc, s);
+        } else {
+            mark(K_COARSE_VEL);
+            launch_coarse_vel(m, st, hN, uN, hNew, uNew, sc, s);
+        }
+        *px = PhaseX{X_C2, hNew, X_E, uNew};
+    } else {
+        return false;
     }
     mark(-1);
+    return true;
+}
+
+void pack(fblts_ctx *c, int x, const double *a, cudaStream_t s) {
+    const Xchg &X = c->lo.x[x];
+    launch_pack(c->ds.xidx + X.sendAt, a, c->ds.sendbuf, (int)X.sendIdx.size(), s);
+}
+void unpack(fblts_ctx *c, int x, double *a, cudaStream_t s) {
+    const Xchg &X = c->lo.x[x];
+    launch_unpack(c->ds.xidx + X.recvAt, c->ds.recvbuf, a, (int)X.recvIdx.size(), s);
+}
+
+
+// pack -> grouped ncclSend/ncclRecv with every peer sharing a halo -> unpack, all on stream s
+int exchange_nccl(fblts_ctx *c, int x, double *a, cudaStream_t s) {
+    if (x < 0) return FBLTS_OK;
+    const Xchg &X = c->lo.x[x];
+    pack(c, x, a, s);
+    ncclComm_t comm = (ncclComm_t)c->nccl;
+    NCCL_TRY(c, ncclGroupStart());
+    for (int p = 0; p < c->cfg.nranks; ++p) {
+        if (p == c->cfg.rank) continue;
+        const size_t ns = X.sendOff[p + 1] - X.sendOff[p], nr = X.recvOff[p + 1] - X.recvOff[p];
+        if (ns) NCCL_TRY(c, ncclSend(c->ds.sendbuf + X.sendOff[p], ns, ncclDouble, p, comm, s));
+        if (nr) NCCL_TRY(c, ncclRecv(c->ds.recvbuf + X.recvOff[p], nr, ncclDouble, p, comm, s));
+    }
+    NCCL_TRY(c, ncclGroupEnd());
+    unpack(c, x, a, s);
+    return FBLTS_OK;
+}
+
+int allgather_nccl(fblts_ctx *c, const double *send6, double *recv) {
+    (void)send6;   // the partial sums are already on the device at diag_out
+    NCCL_TRY(c, ncclAllGather(c->diag_out, c->diag_out + 8, 6, ncclDouble, (ncclComm_t)c->nccl, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(recv, c->diag_out + 8, 6 * sizeof(double) * c->cfg.nranks, cudaMemcpyDeviceToHost,
+                                c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return FBLTS_OK;
+}
+
+// One coarse step on one rank: every phase, with NCCL exchanges when nranks > 1.
+int enqueue_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
+    PhaseX px;
+    for (int ph = 0; enqueue_phase(c, par, ph, s, rec, &px); ++ph) {
+        if (c->cfg.nranks == 1) continue;
+        int rc = exchange_nccl(c, px.x, px.a, s);
+        if (!rc && px.x2 >= 0) rc = exchange_nccl(c, px.x2, px.a2, s);
+        if (rc) return rc;
+    }
+    return FBLTS_OK;
 }
 
 int capture(fblts_ctx *c, int par) {
     cudaGraph_t g;
     CUDA_TRY(c, cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
-    enqueue_step(c, par, c->cap, nullptr);
-    CUDA_TRY(c, cudaStreamEndCapture(c->cap, &g));
+    const int rc = enqueue_step(c, par, c->cap, nullptr);
+    cudaError_t e = cudaStreamEndCapture(c->cap, &g);
+    if (rc) return rc;
+    CUDA_TRY(c, e);
     size_t nodes = 0;
     CUDA_TRY(c, cudaGraphGetNodes(g, nullptr, &nodes));
     c->graph_nodes = nodes;
@@ -731,12 +1083,45 @@ int check_device_error(fblts_ctx *c) {
     DevError e{};
     CUDA_TRY(c, cudaMemcpy(&e, c->ds.err, sizeof e, cudaMemcpyDeviceToHost));
     if (e.flag) {
-        const int idx = e.index >= 0 && e.index < c->hm.nC ? c->rg.cellOld[e.index] : -1;
+        const int idx = e.index >= 0 && e.index < c->lo.nC ? c->lo.cellGlob[e.index] : -1;
         return fail(c, FBLTS_ERR_POSITIVITY, "positivity: h=%g in %s (subcycle k=%d) at cell %d (region %d)", e.value,
                     fblts_kernel_name(e.kind), e.k, idx, idx >= 0 ? (int)c->rg.cell[idx] : -1);
     }
     return FBLTS_OK;
 }
+
+// host double-double merge, identical to the device one
+void dd_merge_host(double &ah, double &al, double bh, double bl) {
+    const double s = ah + bh;
+    const double bb = s - ah;
+    const double err = (ah - (s - bb)) + (bh - bb) + (al + bl);
+    const double hi = s + err;
+    al = err - (hi - s);
+    ah = hi;
+}
+
+int diag_partial(fblts_ctx *c, double out6[6]) {
+    launch_diagnostics(c->dm, c->ds, c->hbuf[c->parity], c->ubuf[c->parity], c->sc, c->diag_out, c->stream);
+    CUDA_TRY(c, cudaGetLastError());
+    CUDA_TRY(c, cudaMemcpyAsync(out6, c->diag_out, 6 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return FBLTS_OK;
+}
+
+void diag_combine(const double *parts, int n, double out[4]) {
+    double mh = 0.0, ml = 0.0, gh = 0.0, gl = 0.0, hmin = INFINITY, numax = 0.0;
+    for (int r = 0; r < n; ++r) {
+        dd_merge_host(mh, ml, parts[6 * r + 0], parts[6 * r + 1]);
+        dd_merge_host(gh, gl, parts[6 * r + 2], parts[6 * r + 3]);
+        hmin = std::min(hmin, parts[6 * r + 4]);
+        numax = std::max(numax, parts[6 * r + 5]);
+    }
+    out[0] = mh + ml;
+    out[1] = gh + gl;
+    out[2] = hmin;
+    out[3] = numax;
+}
+
 
 }  // namespace
 
@@ -745,6 +1130,7 @@ extern "C" {
 int fblts_step(fblts_ctx *c, int32_t n) {
     if (!c || n < 0) return FBLTS_ERR_INVALID_ARG;
     if (c->phase != P_STATE) return fail(c, FBLTS_ERR_ORDER, "step: call set_state first");
+    if (c->cfg.nranks > 1 && !c->nccl) return fail(c, FBLTS_ERR_ORDER, "step: loopback contexts use fblts_step_group");
     CUDA_TRY(c, cudaSetDevice(c->cfg.device));
     for (int p = 0; p < 2; ++p)
         if (!c->exec[p]) {
@@ -759,6 +1145,57 @@ int fblts_step(fblts_ctx *c, int32_t n) {
     return FBLTS_OK;
 }
 
+// Loopback group step: the nranks contexts of ONE process (all on one device and one stream)
+// advance together phase by phase; a halo exchange is a device-to-device copy from the peer's
+// send buffer.  No kernel waits on another; used to test the partitioned path on one GPU.
+int fblts_step_group(fblts_ctx **cs, int32_t n, int32_t n_coarse) {
+    if (!cs || n < 1 || n_coarse < 0) return FBLTS_ERR_INVALID_ARG;
+    for (int r = 0; r < n; ++r) {
+        if (!cs[r] || cs[r]->cfg.rank != r || cs[r]->cfg.nranks != n) return FBLTS_ERR_INVALID_ARG;
+        if (cs[r]->phase != P_STATE) return fail(cs[r], FBLTS_ERR_ORDER, "step_group: call set_state first");
+        if (cs[r]->stream != cs[0]->stream) return fail(cs[r], FBLTS_ERR_INVALID_ARG, "step_group: one stream");
+    }
+    cudaStream_t s = cs[0]->stream;
+    for (int it = 0; it < n_coarse; ++it) {
+        std::vector<PhaseX> px(n);
+        for (int ph = 0;; ++ph) {
+            bool any = false;
+            for (int r = 0; r < n; ++r) any = enqueue_phase(cs[r], cs[r]->parity, ph, s, nullptr, &px[r]) || any;
+            if (!any) break;
+            for (int pass = 0; pass < 2; ++pass) {
+                for (int r = 0; r < n; ++r) {
+                    const int x = pass == 0 ? px[r].x : px[r].x2;
+                    if (x >= 0) pack(cs[r], x, pass == 0 ? px[r].a : px[r].a2, s);
+                }
+                for (int r = 0; r < n; ++r) {
+                    const int x = pass == 0 ? px[r].x : px[r].x2;
+                    if (x < 0) continue;
+                    const Xchg &X = cs[r]->lo.x[x];
+                    for (int p = 0; p < n; ++p) {
+                        const int64_t cnt = X.recvOff[p + 1] - X.recvOff[p];
+                        if (!cnt) continue;
+                        const Xchg &Y = cs[p]->lo.x[x];
+                        if (Y.sendOff[r + 1] - Y.sendOff[r] != cnt)
+                            return fail(cs[r], FBLTS_ERR_INVALID_ARG, "step_group: halo size mismatch with rank %d", p);
+                        CUDA_TRY(cs[r], cudaMemcpyAsync(cs[r]->ds.recvbuf + X.recvOff[p], cs[p]->ds.sendbuf + Y.sendOff[r],
+                                                        cnt * 8, cudaMemcpyDeviceToDevice, s));
+                    }
+                }
+                for (int r = 0; r < n; ++r) {
+                    const int x = pass == 0 ? px[r].x : px[r].x2;
+                    if (x >= 0) unpack(cs[r], x, pass == 0 ? px[r].a : px[r].a2, s);
+                }
+            }
+        }
+        for (int r = 0; r < n; ++r) {
+            cs[r]->parity ^= 1;
+            cs[r]->t += cs[r]->cfg.dt;
+        }
+    }
+    CUDA_TRY(cs[0], cudaGetLastError());
+    return FBLTS_OK;
+}
+
 int fblts_sync(fblts_ctx *c) {
     if (!c) return FBLTS_ERR_INVALID_ARG;
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -770,14 +1207,18 @@ int fblts_get_state(fblts_ctx *c, double *h, double *u, double *t) {
     if (!c) return FBLTS_ERR_INVALID_ARG;
     if (c->phase != P_STATE) return fail(c, FBLTS_ERR_ORDER, "get_state: no state set");
     cudaStream_t s = c->stream;
-    const int nC = c->hm.nC, nE = c->hm.nE;
+    const Local &L = c->lo;
+    // owned entries only (all entries for one rank); other entries of h, u are left untouched
     if (h) {
-        launch_permute_out(c->ds.cellOld, c->hbuf[c->parity], c->ds.stage, nC, s);
-        CUDA_TRY(c, cudaMemcpyAsync(h, c->ds.stage, (size_t)nC * 8, cudaMemcpyDeviceToHost, s));
+        if (c->cfg.nranks > 1) CUDA_TRY(c, cudaMemcpyAsync(c->ds.stage, h, (size_t)c->hm.nC * 8, cudaMemcpyHostToDevice, s));
+        launch_permute_out(c->ds.cellOld, c->hbuf[c->parity], c->ds.stage, L.nOwnC, s);
+        CUDA_TRY(c, cudaMemcpyAsync(h, c->ds.stage, (size_t)c->hm.nC * 8, cudaMemcpyDeviceToHost, s));
     }
     if (u) {
-        launch_permute_out(c->ds.edgeOld, c->ubuf[c->parity], c->ds.stage, nE, s);
-        CUDA_TRY(c, cudaMemcpyAsync(u, c->ds.stage, (size_t)nE * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(c, cudaStreamSynchronize(s));
+        if (c->cfg.nranks > 1) CUDA_TRY(c, cudaMemcpyAsync(c->ds.stage, u, (size_t)c->hm.nE * 8, cudaMemcpyHostToDevice, s));
+        launch_permute_out(c->ds.edgeOld, c->ubuf[c->parity], c->ds.stage, L.nOwnE, s);
+        CUDA_TRY(c, cudaMemcpyAsync(u, c->ds.stage, (size_t)c->hm.nE * 8, cudaMemcpyDeviceToHost, s));
     }
     CUDA_TRY(c, cudaStreamSynchronize(s));
     CUDA_TRY(c, cudaGetLastError());
@@ -788,23 +1229,51 @@ int fblts_get_state(fblts_ctx *c, double *h, double *u, double *t) {
 int fblts_diagnostics(fblts_ctx *c, double out[4]) {
     if (!c || !out) return FBLTS_ERR_INVALID_ARG;
     if (c->phase != P_STATE) return fail(c, FBLTS_ERR_ORDER, "diagnostics: no state set");
-    launch_diagnostics(c->dm, c->ds, c->hbuf[c->parity], c->ubuf[c->parity], c->sc, c->diag_out, c->stream);
-    CUDA_TRY(c, cudaGetLastError());
-    CUDA_TRY(c, cudaMemcpyAsync(out, c->diag_out, 4 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (c->cfg.nranks > 1 && !c->nccl)
+        return fail(c, FBLTS_ERR_ORDER, "diagnostics: loopback contexts use fblts_diagnostics_group");
+    double part[6];
+    int rc = diag_partial(c, part);
+    if (rc) return rc;
+    if (c->cfg.nranks == 1) {
+        diag_combine(part, 1, out);
+    } else {
+        std::vector<double> all(6 * (size_t)c->cfg.nranks);
+        rc = allgather_nccl(c, part, all.data());
+        if (rc) return rc;
+        diag_combine(all.data(), c->cfg.nranks, out);
+    }
     return check_device_error(c);
+}
+
+// Diagnostics of a loopback group (partial sums combined in rank order, as over NCCL).
+int fblts_diagnostics_group(fblts_ctx **cs, int32_t n, double out[4]) {
+    if (!cs || n < 1 || !out) return FBLTS_ERR_INVALID_ARG;
+    std::vector<double> all(6 * (size_t)n);
+    for (int r = 0; r < n; ++r) {
+        if (cs[r]->phase != P_STATE) return fail(cs[r], FBLTS_ERR_ORDER, "diagnostics_group: no state set");
+        const int rc = diag_partial(cs[r], &all[6 * (size_t)r]);
+        if (rc) return rc;
+    }
+    diag_combine(all.data(), n, out);
+    for (int r = 0; r < n; ++r) {
+        const int rc = check_device_error(cs[r]);
+        if (rc) return rc;
+    }
+    return FBLTS_OK;
 }
 
 int fblts_profile(fblts_ctx *c, int32_t n, double *ms, int64_t *launches) {
     if (!c || !ms || !launches || n < 0) return FBLTS_ERR_INVALID_ARG;
     if (c->phase != P_STATE) return fail(c, FBLTS_ERR_ORDER, "profile: call set_state first");
+    if (c->cfg.nranks > 1 && !c->nccl) return fail(c, FBLTS_ERR_ORDER, "profile: not for loopback contexts");
     for (int k = 0; k < K_NUM; ++k) {
         ms[k] = 0.0;
         launches[k] = 0;
     }
     for (int i = 0; i < n; ++i) {
         Recorder rec;
-        enqueue_step(c, c->parity, c->stream, &rec);
+        const int rc = enqueue_step(c, c->parity, c->stream, &rec);
+        if (rc) return rc;
         CUDA_TRY(c, cudaGetLastError());
         CUDA_TRY(c, cudaStreamSynchronize(c->stream));
         for (size_t j = 0; j + 1 < rec.ev.size(); ++j) {
@@ -827,6 +1296,7 @@ void fblts_destroy(fblts_ctx *c) {
     for (auto &e : c->exec)
         if (e) cudaGraphExecDestroy(e);
     if (c->cap) cudaStreamDestroy(c->cap);
+    nccl_destroy(c);
     delete c;
 }
 

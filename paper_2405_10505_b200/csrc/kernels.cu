@@ -35,8 +35,12 @@ constexpr int TPB = 256;
 
 static inline unsigned nblocks(long n) { return (unsigned)((n + TPB - 1) / TPB); }
 
-// cell class: 2 = F, 1 = IF-1, 0 = other coarse (IF-2 or int)
-__device__ __forceinline__ int ccls(const Bounds &b, int x) { return x >= b.f ? 2 : (x >= b.if1 ? 1 : 0); }
+// cell class: 2 = F, 1 = IF-1, 0 = other coarse (IF-2 or int); owned block [0, nOwnC) and halo
+// block [nOwnC, nC) are each region-major
+__device__ __forceinline__ int ccls(const DevMesh &m, int x) {
+    const Bounds &b = x < m.nOwnC ? m.cb : m.cbh;
+    return x >= b.f ? 2 : (x >= b.if1 ? 1 : 0);
+}
 // edge class: 3 = F_E, 2 = IF-1_E, 1 = IF-2_E, 0 = int_E
 __device__ __forceinline__ int ecls(const Bounds &b, int e) {
     return e >= b.f ? 3 : (e >= b.if1 ? 2 : (e >= b.if2 ? 1 : 0));
@@ -142,7 +146,7 @@ __global__ void __launch_bounds__(TPB) k_slow_edge(DevMesh m, const double *__re
                                                    const double *__restrict__ F, double *__restrict__ S,
                                                    double rho0) {
     const int e = blockIdx.x * TPB + threadIdx.x;
-    if (e >= m.nE) return;
+    if (e >= m.nOwnE) return;
     const int n = m.nEoE[e];
     double w[MAXE2], f[MAXE2];
 #pragma unroll
@@ -261,20 +265,20 @@ __device__ __forceinline__ double pred_stage(const PredConst &p, const double *h
 }
 
 template <bool BAND>
-__device__ __forceinline__ int cclass(const Bounds &b, int x) { return BAND ? ccls(b, x) : 2; }
+__device__ __forceinline__ int cclass(const DevMesh &m, int x) { return BAND ? ccls(m, x) : 2; }
 template <bool BAND>
 __device__ __forceinline__ int eclass(const Bounds &b, int e) { return BAND ? ecls(b, e) : 3; }
 
 // view H0 (h^{n,k}) for fine stage 1
 template <bool BAND>
-__device__ __forceinline__ double view0(const Bounds &b, const PredConst &p, const FineArrays &a, int x) {
+__device__ __forceinline__ double view0(const DevMesh &b, const PredConst &p, const FineArrays &a, int x) {
     const int cl = cclass<BAND>(b, x);
     return cl == 2 ? a.hk[x] : (cl == 1 ? pred_level(p, a, x) : a.hN[x]);
 }
 
 // view (H1, HS1) for fine stage 2
 template <bool BAND>
-__device__ __forceinline__ void view1(const Bounds &b, const StepConst &sc, const PredConst &p, const FineArrays &a,
+__device__ __forceinline__ void view1(const DevMesh &b, const StepConst &sc, const PredConst &p, const FineArrays &a,
                                       int x, double &H, double &HS) {
     const int cl = cclass<BAND>(b, x);
     if (cl == 2) {
@@ -292,7 +296,7 @@ __device__ __forceinline__ void view1(const Bounds &b, const StepConst &sc, cons
 
 // view (H2, HS2) for fine stage 3 / the correction summand
 template <bool BAND>
-__device__ __forceinline__ void view2(const Bounds &b, const StepConst &sc, const PredConst &p, const FineArrays &a,
+__device__ __forceinline__ void view2(const DevMesh &b, const StepConst &sc, const PredConst &p, const FineArrays &a,
                                       int x, double &H, double &HS) {
     const int cl = cclass<BAND>(b, x);
     if (cl == 2) {
@@ -310,7 +314,7 @@ __device__ __forceinline__ void view2(const Bounds &b, const StepConst &sc, cons
 
 // view HS3 (h^{***,k}) for the fine velocity stage 3
 template <bool BAND>
-__device__ __forceinline__ double view3(const Bounds &b, const StepConst &sc, const PredConst &p,
+__device__ __forceinline__ double view3(const DevMesh &b, const StepConst &sc, const PredConst &p,
                                         const FineArrays &a, const double *hnext, int x) {
     const int cl = cclass<BAND>(b, x);
     if (cl == 2) return sc.b3 * hnext[x] + sc.om2b3 * a.h2[x] + sc.b3 * a.hk[x];
@@ -340,7 +344,7 @@ __global__ void __launch_bounds__(TPB) k_fine_s1(DevMesh m, FineArrays a, const 
         if (j < n) {
             bool pos;
             const int e = decode(r[j].x, pos);
-            acc = acc + psi_term(pos, Hi, view0<BAND>(m.cb, p, a, r[j].y), uk[e], m.dv[e]);
+            acc = acc + psi_term(pos, Hi, view0<BAND>(m, p, a, r[j].y), uk[e], m.dv[e]);
         }
     }
     const double psi = -acc / m.areaCell[i];
@@ -362,7 +366,7 @@ __global__ void __launch_bounds__(TPB, BAND ? 1 : FBLTS_MINB) k_fine_s2(DevMesh 
     load_row<G>(m, i, r);
     const int n = m.nEoC[i];
     double Hi, HSi;
-    view1<BAND>(m.cb, sc, p, a, i, Hi, HSi);
+    view1<BAND>(m, sc, p, a, i, Hi, HSi);
     const double zbi = m.zb[i];
     double acc = 0.0;
 #pragma unroll
@@ -372,7 +376,7 @@ __global__ void __launch_bounds__(TPB, BAND ? 1 : FBLTS_MINB) k_fine_s2(DevMesh 
             const int e = decode(r[j].x, pos);
             const int nb = r[j].y;
             double Hn, HSn;
-            view1<BAND>(m.cb, sc, p, a, nb, Hn, HSn);
+            view1<BAND>(m, sc, p, a, nb, Hn, HSn);
             const double zbn = m.zb[nb];
             const double dc = m.dc[e];
             const double phi = pos ? phi_fast(sc.g, HSi, zbi, HSn, zbn, dc) : phi_fast(sc.g, HSn, zbn, HSi, zbi, dc);
@@ -405,7 +409,7 @@ __global__ void __launch_bounds__(TPB, BAND ? 1 : FBLTS_MINB) k_fine_s3(DevMesh 
     load_row<G>(m, i, r);
     const int n = m.nEoC[i];
     double Hi, HSi;
-    view2<BAND>(m.cb, sc, p, a, i, Hi, HSi);
+    view2<BAND>(m, sc, p, a, i, Hi, HSi);
     const double zbi = m.zb[i];
     double acc = 0.0;
 #pragma unroll
@@ -415,7 +419,7 @@ __global__ void __launch_bounds__(TPB, BAND ? 1 : FBLTS_MINB) k_fine_s3(DevMesh 
             const int e = decode(r[j].x, pos);
             const int nb = r[j].y;
             double Hn, HSn;
-            view2<BAND>(m.cb, sc, p, a, nb, Hn, HSn);
+            view2<BAND>(m, sc, p, a, nb, Hn, HSn);
             const double dc = m.dc[e];
             double ue;
             const int ec = eclass<BAND>(m.eb, e);
@@ -463,8 +467,8 @@ __global__ void __launch_bounds__(TPB) k_fine_vel(DevMesh m, FineArrays a, const
     const int e = begin + blockIdx.x * TPB + threadIdx.x;
     if (e >= end) return;
     const int2 c = m.coe[e];
-    const double phi = phi_fast(sc.g, view3<BAND>(m.cb, sc, p, a, hnext, c.x), m.zb[c.x],
-                                view3<BAND>(m.cb, sc, p, a, hnext, c.y), m.zb[c.y], m.dc[e]);
+    const double phi = phi_fast(sc.g, view3<BAND>(m, sc, p, a, hnext, c.x), m.zb[c.x],
+                                view3<BAND>(m, sc, p, a, hnext, c.y), m.zb[c.y], m.dc[e]);
     if (!BAND || e >= m.eb.f) {
         unext[e] = uk[e] + sc.c3f * (phi + S[e]);
     } else {
@@ -506,6 +510,17 @@ __global__ void k_permute_out(const int32_t *__restrict__ old, const double *__r
     if (i < n) dst[old[i]] = src[i];
 }
 
+__global__ void k_pack(const int32_t *__restrict__ idx, const double *__restrict__ a, double *__restrict__ buf,
+                       int n) {
+    const int k = blockIdx.x * TPB + threadIdx.x;
+    if (k < n) buf[k] = a[idx[k]];
+}
+__global__ void k_unpack(const int32_t *__restrict__ idx, const double *__restrict__ buf, double *__restrict__ a,
+                         int n) {
+    const int k = blockIdx.x * TPB + threadIdx.x;
+    if (k < n) a[idx[k]] = buf[k];
+}
+
 // double-double accumulation (Knuth TwoSum), deterministic for a fixed launch shape
 struct DD {
     double hi, lo;
@@ -541,6 +556,7 @@ __global__ void __launch_bounds__(TPB) k_diag_partial(DevMesh m, const double *_
         hmin = fmin(hmin, h[i]);
     }
     for (int v = tid; v < m.nV; v += T) {
+        if (!m.vOwn[v]) continue;
         double circ = 0.0;
         for (int k = 0; k < 3; ++k) {
             bool pos;
@@ -551,6 +567,7 @@ __global__ void __launch_bounds__(TPB) k_diag_partial(DevMesh m, const double *_
         dd_add(gam, circ + m.areaTri[v] * m.fV[v]);
     }
     for (int e = tid; e < m.eb.end; e += T) {
+        if (!m.eOwn[e]) continue;
         const int2 c = m.coe[e];
         const double he = 0.5 * (h[c.x] + h[c.y]);
         const double dte = e >= m.eb.f ? sc.c3f : sc.c3;
@@ -594,10 +611,12 @@ __global__ void k_diag_final(const double *__restrict__ part, int nb, double *__
         hmin = fmin(hmin, part[b * 6 + 4]);
         numax = fmax(numax, part[b * 6 + 5]);
     }
-    out[0] = mass.hi + mass.lo;
-    out[1] = gam.hi + gam.lo;
-    out[2] = hmin;
-    out[3] = numax;
+    out[0] = mass.hi;          // raw double-double parts: ranks are combined on the host in rank order
+    out[1] = mass.lo;
+    out[2] = gam.hi;
+    out[3] = gam.lo;
+    out[4] = hmin;
+    out[5] = numax;
 }
 
 // ---------------------------------------------------------------- launchers
@@ -621,12 +640,13 @@ void launch_slow_pre(const DevMesh &m, const DevState &st, const double *h, cons
     FBLTS_DISPATCH_G(m.ecS, k_slow_pre<G><<<nbV + nbC + nbE, TPB, 0, s>>>(m, h, u, st.q, st.K, st.F, nbV, nbC));
 }
 void launch_slow_edge(const DevMesh &m, const DevState &st, const double *h, const StepConst &sc, cudaStream_t s) {
+    if (m.nOwnE <= 0) return;
     if (m.maxE2 <= 10)
-        k_slow_edge<10><<<nblocks(m.nE), TPB, 0, s>>>(m, h, st.q, st.K, st.F, st.S, sc.rho0);
+        k_slow_edge<10><<<nblocks(m.nOwnE), TPB, 0, s>>>(m, h, st.q, st.K, st.F, st.S, sc.rho0);
     else if (m.maxE2 <= 14)
-        k_slow_edge<14><<<nblocks(m.nE), TPB, 0, s>>>(m, h, st.q, st.K, st.F, st.S, sc.rho0);
+        k_slow_edge<14><<<nblocks(m.nOwnE), TPB, 0, s>>>(m, h, st.q, st.K, st.F, st.S, sc.rho0);
     else
-        k_slow_edge<30><<<nblocks(m.nE), TPB, 0, s>>>(m, h, st.q, st.K, st.F, st.S, sc.rho0);
+        k_slow_edge<30><<<nblocks(m.nOwnE), TPB, 0, s>>>(m, h, st.q, st.K, st.F, st.S, sc.rho0);
 }
 void launch_coarse_s1(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
                       const StepConst &sc, cudaStream_t s) {
@@ -718,6 +738,12 @@ void launch_permute_in(const int32_t *old, const double *src, double *dst, int n
 }
 void launch_permute_out(const int32_t *old, const double *src, double *dst, int n, cudaStream_t s) {
     if (n > 0) k_permute_out<<<nblocks(n), TPB, 0, s>>>(old, src, dst, n);
+}
+void launch_pack(const int32_t *idx, const double *a, double *buf, int n, cudaStream_t s) {
+    if (n > 0) k_pack<<<nblocks(n), TPB, 0, s>>>(idx, a, buf, n);
+}
+void launch_unpack(const int32_t *idx, const double *buf, double *a, int n, cudaStream_t s) {
+    if (n > 0) k_unpack<<<nblocks(n), TPB, 0, s>>>(idx, buf, a, n);
 }
 void launch_diagnostics(const DevMesh &m, const DevState &st, const double *h, const double *u, const StepConst &sc,
                         double *out_dev, cudaStream_t s) {

@@ -20,14 +20,15 @@ from . import _abi as abi
 
 class Solver:
     def __init__(self, mesh, fine_mask, dt, M, *, g=9.81, beta=(0.531, 0.531, 0.313), rho0=1000.0, r=2,
-                 slow=True, tau_n=None, device=None, stream=None):
+                 slow=True, tau_n=None, device=None, stream=None, rank=0, nranks=1, nccl_id=None):
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2405_10505_b200.Solver needs a CUDA device (no CPU fallback)")
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.nCells, self.nEdges = int(mesh.nCells), int(mesh.nEdges)
         self.ctx = abi.fblts_create(dt, M, g=g, beta=beta, rho0=rho0, r=r, slow=slow, device=self.device.index,
-                                    stream=self.stream.cuda_stream)
+                                    stream=self.stream.cuda_stream, rank=rank, nranks=nranks, nccl_id=nccl_id)
+        self.rank, self.nranks = rank, nranks
         try:
             abi.fblts_upload_mesh(self.ctx, mesh)
             abi.fblts_set_regions(self.ctx, fine_mask)
@@ -49,7 +50,7 @@ class Solver:
         c = abi.fblts_get_counts(self.ctx)
         return {"nCells": int(c[0]), "nEdges": int(c[1]), "nVertices": int(c[2]),
                 "cells_by_region": c[3:12].tolist(), "edges_by_region": c[12:21].tolist(),
-                "kernels_per_step": int(c[23])}
+                "owned_cells": int(c[21]), "owned_edges": int(c[22]), "kernels_per_step": int(c[23])}
 
     # --- state and stepping
     def set_state(self, h, u, t=0.0):
@@ -87,3 +88,37 @@ class Solver:
             self.close()
         except Exception:
             pass
+
+
+class SolverGroup:
+    """n partitions of one mesh driven together on ONE device (loopback halo exchange through
+    device copies, fblts_step_group).  Exercises the partitioned multi-rank path -- dual-set
+    partition, local numbering, halo lists, pack/unpack, per-rank diagnostics -- without NCCL."""
+
+    def __init__(self, mesh, fine_mask, dt, M, nranks, **kw):
+        self.solvers = [Solver(mesh, fine_mask, dt, M, rank=r, nranks=nranks, **kw) for r in range(nranks)]
+        self.nCells, self.nEdges = int(mesh.nCells), int(mesh.nEdges)
+
+    def set_state(self, h, u, t=0.0):
+        for s in self.solvers:
+            s.set_state(h, u, t)
+
+    def step(self, n_coarse=1):
+        abi.fblts_step_group([s.ctx for s in self.solvers], n_coarse)
+
+    def state(self):
+        h, u = np.full(self.nCells, np.nan), np.full(self.nEdges, np.nan)
+        t = None
+        for s in self.solvers:
+            t = abi.fblts_get_state(s.ctx, h, u)      # each rank fills its owned entries
+        return h, u, t
+
+    def diagnostics(self):
+        return abi.fblts_diagnostics_group([s.ctx for s in self.solvers])
+
+    def counts(self):
+        return [s.counts() for s in self.solvers]
+
+    def close(self):
+        for s in self.solvers:
+            s.close()

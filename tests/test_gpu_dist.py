@@ -1,0 +1,65 @@
+"""Partitioned (multi-rank) path on ONE GPU through the loopback group (fblts_step_group): the
+dual-set partition, local numbering, halo lists, pack/unpack and per-rank diagnostics.  Results
+must be bit-identical to the single-rank run (and hence to the oracle) for any rank count
+("results bitwise identical for 1/2/4/8 GPUs")."""
+import numpy as np
+import pytest
+
+from inputs import configs
+from oracle import fbrk32, lts
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mods():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2405_10505_b200 import Solver, SolverGroup
+    return Solver, SolverGroup
+
+
+def single(Solver, c, n):
+    s = Solver(c.mesh, c.fine_mask, c.dt, c.M, g=c.g, beta=c.beta, rho0=c.rho0, slow=c.slow, tau_n=c.tau_n)
+    s.set_state(c.h0, c.u0)
+    s.step(n)
+    h, u, _ = s.state()
+    d = s.diagnostics()
+    s.close()
+    return h, u, d
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 4, 8])
+@pytest.mark.parametrize("which", ["config1", "shelf"])
+def test_group_bitwise_equals_single_rank(mods, which, nranks):
+    Solver, SolverGroup = mods
+    c = configs.config1() if which == "config1" else configs.small_shelf(nx=64, ny=48, seed=5, dt=25.0)
+    n = 20
+    h1, u1, d1 = single(Solver, c, n)
+    g = SolverGroup(c.mesh, c.fine_mask, c.dt, c.M, nranks, g=c.g, beta=c.beta, rho0=c.rho0, slow=c.slow,
+                    tau_n=c.tau_n)
+    g.set_state(c.h0, c.u0)
+    g.step(n)
+    h, u, t = g.state()
+    assert np.array_equal(h, h1), np.nanmax(np.abs(h - h1))
+    assert np.array_equal(u, u1), np.nanmax(np.abs(u - u1))
+    d = g.diagnostics()
+    assert d[0] == pytest.approx(d1[0], rel=1e-15) and d[2] == d1[2] and d[3] == d1[3]
+    owned = sum(x["owned_cells"] for x in g.counts())
+    assert owned == c.mesh.nCells
+    g.close()
+
+
+def test_group_matches_oracle(mods):
+    _, SolverGroup = mods
+    c = configs.small_shelf(nx=64, ny=48, seed=5, dt=25.0)
+    lab = lts.label_regions(c.mesh, c.fine_mask)
+    phys = fbrk32.Phys(g=c.g, beta=c.beta, slow=c.slow, tau_n=c.tau_n, rho0=c.rho0)
+    ho, uo = lts.run(c.mesh, lab, c.h0, c.u0, c.dt, c.M, phys, 30)
+    g = SolverGroup(c.mesh, c.fine_mask, c.dt, c.M, 4, tau_n=c.tau_n)
+    g.set_state(c.h0, c.u0)
+    g.step(30)
+    h, u, _ = g.state()
+    assert np.array_equal(h, ho) and np.array_equal(u, uo)
+    g.close()
