@@ -16,12 +16,14 @@ import os
 import numpy as np
 
 from .hexmesh import build_periodic_hex_mesh, build_periodic_hex_mesh_fast
+from .icosmesh import EARTH_R, build_icosahedral_mesh
 from .trisk_mesh import Mesh
 
 G = 9.81              # reading Q28
 F_PLANE = 1.0e-4      # f-plane configs 1, 2, 5
 RHO0 = 1000.0         # reading Q19
 TAU_X = 0.1           # N m^-2, reading Q19
+OMEGA = 7.292115e-5   # s^-1, reading Q28 (f = 2 Omega sin(latitude) on the sphere)
 BETA = (0.531, 0.531, 0.313)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -176,3 +178,37 @@ def small_shelf(seed=7, nx=48, ny=40, dc=2e3, **kw) -> Case:
     kw.setdefault("corr", 20e3 * s)
     kw.setdefault("sigma", 40e3 * s)
     return shelf_case("small_shelf", nx, ny, dc, seed, **kw)
+
+
+def config3(seed=3, dt=None, level=8, n_steps=500) -> Case:
+    """BASELINE config 3: icosahedral level-8 dual on R = 6371 km, H = 4000 m, f = 2 Omega sin(phi),
+    global FB-RK(3,2) (no fine cells), u = 0, 16 Gaussian bumps U[10, 100] m with a 300-km
+    great-circle sigma (reading Q23), 500 steps.  dt: 0.9 x the oracle-bisected Courant limit
+    nu_loc (configs/dt.json "config3", measured on a lower level of the same recipe) applied to
+    this mesh's max sqrt(g H)/d_e."""
+    rng = np.random.default_rng(seed)
+    mesh = build_icosahedral_mesh(level)
+    H = np.full(mesh.nCells, 4000.0)
+    mesh.bottomDepth = H
+    lat_v = np.arcsin(np.clip(mesh.zVertex / mesh.radius, -1.0, 1.0))
+    mesh.fVertex = 2.0 * OMEGA * np.sin(lat_v)
+    c = rng.standard_normal((16, 3))
+    c /= np.linalg.norm(c, axis=1, keepdims=True)
+    amps = rng.uniform(10.0, 100.0, 16)
+    x = np.stack([mesh.xCell, mesh.yCell, mesh.zCell], axis=1) / mesh.radius
+    eta = np.zeros(mesh.nCells)
+    sigma = 300e3
+    for k in range(16):
+        d = mesh.radius * np.arccos(np.clip(x @ c[k], -1.0, 1.0))
+        eta += amps[k] * np.exp(-(d * d) / (2.0 * sigma * sigma))
+    if dt is None:
+        try:
+            with open(DT_TABLE) as f:
+                nu = float(json.load(f)["config3"]["nu_loc_limit"])
+        except (OSError, KeyError, ValueError):
+            nu = 1.5767175 * 0.8
+        cmax = np.max(np.sqrt(G * np.maximum(H[mesh.cellsOnEdge[:, 0]], H[mesh.cellsOnEdge[:, 1]])) / mesh.dcEdge)
+        dt = 0.9 * nu / cmax
+    return Case(name="config3", mesh=mesh, h0=H + eta, u0=np.zeros(mesh.nEdges),
+                fine_mask=np.zeros(mesh.nCells, dtype=bool), tau_n=np.zeros(mesh.nEdges), M=1, dt=dt,
+                n_steps=n_steps, seed=seed)

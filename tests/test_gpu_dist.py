@@ -63,3 +63,18 @@ def test_group_matches_oracle(mods):
     h, u, _ = g.state()
     assert np.array_equal(h, ho) and np.array_equal(u, uo)
     g.close()
+
+
+def test_group_on_sphere(mods):
+    """Partitioned run on the sphere (3-D Morton SFC), with a fine polar cap: bitwise = single rank."""
+    Solver, SolverGroup = mods
+    c = configs.config3(level=5, n_steps=20)
+    c.fine_mask = c.mesh.zCell > 0.6 * c.mesh.radius
+    c.M = 3
+    h1, u1, _ = single(Solver, c, 20)
+    g = SolverGroup(c.mesh, c.fine_mask, c.dt, c.M, 4)
+    g.set_state(c.h0, c.u0)
+    g.step(20)
+    h, u, _ = g.state()
+    assert np.array_equal(h, h1) and np.array_equal(u, u1)
+    g.close()

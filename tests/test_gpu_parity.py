@@ -217,3 +217,30 @@ def test_profile_counts_launches(Solver):
     prof = s.profile(2)
     assert prof["fine_s3"][1] == 2 * c.M and prof["slow_edge"][1] == 2 and prof["correct_if"][1] == 2
     assert all(ms >= 0.0 for ms, _ in prof.values())
+
+
+def test_parity_sphere_100_steps(Solver):
+    """Config-3 recipe (icosahedral dual, full Coriolis, global FB-RK(3,2)) at level 5, 100 steps."""
+    c = configs.config3(level=5, n_steps=100)
+    ho, uo, _ = run_oracle(c, 100)
+    _, hg, ug, _ = run_gpu(Solver, c, 100)
+    eh, eu = assert_parity(hg, ug, ho, uo)
+    print(f"sphere L5: eps_h={eh:.3e} eps_u={eu:.3e}")
+
+
+def test_parity_config3_full_size(Solver):
+    """BASELINE config 3 at full size (655,362 cells), 3 steps, element by element."""
+    c = configs.config3()
+    ho, uo, _ = run_oracle(c, 3)
+    _, hg, ug, _ = run_gpu(Solver, c, 3)
+    assert_parity(hg, ug, ho, uo)
+
+
+def test_sphere_with_fine_region(Solver):
+    """FB-LTS on the sphere: a fine polar cap (M = 3) on the level-5 icosahedral dual."""
+    c = configs.config3(level=5, n_steps=50)
+    c.fine_mask = c.mesh.zCell > 0.6 * c.mesh.radius
+    c.M = 3
+    ho, uo, _ = run_oracle(c, 50)
+    _, hg, ug, _ = run_gpu(Solver, c, 50)
+    assert_parity(hg, ug, ho, uo)
