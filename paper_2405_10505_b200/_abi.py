@@ -148,7 +148,7 @@ def fblts_get_labels(ctx, nCells, nEdges):
 
 
 def fblts_get_counts(ctx):
-    out = np.zeros(24, np.int64)
+    out = np.zeros(28, np.int64)
     _check(ctx, _lib_counts(ctx, _ptr(out, C.c_int64)))
     return out
 

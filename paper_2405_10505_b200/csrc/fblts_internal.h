@@ -31,6 +31,39 @@ struct Bounds {
     int32_t fl[6];
 };
 
+// Cell tiles for the staged stage kernels.  The owned cells are cut into
+// tiles of at most TILE consecutive cells; tile boundaries include every region block boundary,
+// so each stage extent is a whole number of tiles.  A tile's local cells are its own cells
+// (local index i - c0) followed by its halo cells (neighbours outside the tile; local index
+// HALO0 + position in its sorted halo list).  Its local edges (every edge of its cells) are the
+// contiguous run [eo0, eo1) of edges it owns (local index e - eo0) followed by its "foreign"
+// edges (sorted list; local index (eo1 - eo0) + FGAP + position).  The gaps keep the slack
+// elements of the 16-byte aligned bulk copies of the contiguous ranges clear of the
+// individually copied halo / foreign entries.  Per local edge (in list order, no gap),
+//   ecl = (local cell of c1) << 16 | (local cell of c0),
+// and per cell a slot-major 16-bit slot table  row[j * strideRow + i] = neg << 15 | local edge
+// (TILE_SENT for j >= nEdgesOnCell).  info[t * TINFO + k], k = c0, h0, eo0, eo1, f0, l0 (offsets
+// into the cell range, halo list, edge range, foreign list and ecl); record t + 1 gives the ends.
+#ifndef FBLTS_TILE
+#define FBLTS_TILE 256
+#endif
+constexpr int TILE = FBLTS_TILE;
+constexpr int TINFO = 8;
+constexpr int HALO0 = TILE + 2;
+constexpr int FGAP = 2;
+constexpr uint16_t TILE_SENT = 0xFFFFu;
+constexpr int TILE_SMEM_MAX = 227 * 1024;     // opt-in dynamic shared memory per CTA (sm_100a)
+struct TileMesh {
+    int32_t nTiles;
+    int32_t strideRow;                      // >= nOwnC
+    int32_t hmax, emax;                     // largest halo / local-edge count of any tile
+    const int32_t *__restrict__ info;       // [(nTiles + 1) * TINFO]
+    const int32_t *__restrict__ halo;       // halo cells of all tiles
+    const int32_t *__restrict__ fedge;      // foreign edges of all tiles
+    const uint32_t *__restrict__ ecl;       // local-edge cell pairs of all tiles
+    const uint16_t *__restrict__ row;       // [maxE][strideRow]
+};
+
 struct DevMesh {
     int32_t nC, nE, nV;               // local entity counts (owned + halo)
     int32_t nOwnC, nOwnE;              // owned cells [0, nOwnC); edges touching owned cells [0, nOwnE)
@@ -58,6 +91,7 @@ struct DevMesh {
     const uint8_t *__restrict__ eOwn;  // [nE] 1 if this rank reports the edge in the diagnostics
     Bounds cb, eb;                     // owned cell / edge region bounds (cb.end = nOwnC, eb.end = nOwnE)
     Bounds cbh;                        // halo cell block [nOwnC, nC), region-major, absolute indices
+    TileMesh tm;                       // tiles of the owned cells
 };
 
 // Device error record (positivity / NaN), first failure wins.
@@ -100,6 +134,22 @@ struct DevState {
     DevError *err;
 };
 
+// Staged stage sweep over the whole tiles [tile0, tile1) (kernels.cu): one thread per cell,
+//   out_i = hbase_i + ch * Psi_i(u_bar, hprev),
+//   u_bar_e = ubase_e                                   (STAGE 1)
+//   u_bar_e = ubase_e + cu (Phi^fast_e(bb hprev + omb hbase) + S_e)   (STAGE 2, 3)
+// which is the coarse stage s (hbase = h^n) and the fine stage s inside F (hbase = h^{n,k}).
+struct StageArgs {
+    const double *hbase, *hprev, *ubase, *S;
+    double *out;
+    double cu, bb, omb, ch, g;
+    int32_t kind, k;
+};
+void launch_stage_tiled(const DevMesh &m, int stage, int tile0, int tile1, int hmax, int emax, int nsm,
+                        const StageArgs &a, DevError *err, cudaStream_t s);
+int stage_tiled_smem_bytes_host(int stage, int hmax, int emax);   // bytes for tiles with <= hmax / emax
+int stage_tiled_configure(const DevMesh &m);      // sets the dynamic shared-memory limits (cudaError_t)
+
 // Kernel launchers (kernels.cu).  All enqueue on `s`.
 void launch_slow_pre(const DevMesh &m, const DevState &st, const double *h, const double *u, cudaStream_t s);
 void launch_slow_edge(const DevMesh &m, const DevState &st, const double *h, const StepConst &sc, cudaStream_t s);
@@ -113,13 +163,13 @@ void launch_coarse_vel(const DevMesh &m, const DevState &st, const double *hN, c
                        const double *hNew, double *uNew, const StepConst &sc, cudaStream_t s);
 void launch_fine_s1(const DevMesh &m, const DevState &st, const double *hN, const double *hNew,
                     const double *hk, const double *uk, const StepConst &sc, const PredConst &pc,
-                    int k, cudaStream_t s);
+                    int k, cudaStream_t s, bool deep = true);
 void launch_fine_s2(const DevMesh &m, const DevState &st, const double *hN, const double *hNew,
                     const double *hk, const double *uk, const StepConst &sc, const PredConst &pc,
-                    int k, cudaStream_t s);
+                    int k, cudaStream_t s, bool deep = true);
 void launch_fine_s3(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
                     const double *hNew, const double *hk, const double *uk, double *hnext,
-                    const StepConst &sc, const PredConst &pc, int k, cudaStream_t s);
+                    const StepConst &sc, const PredConst &pc, int k, cudaStream_t s, bool deep = true);
 void launch_fine_vel(const DevMesh &m, const DevState &st, const double *hN, const double *hNew,
                      const double *hk, const double *hnext, const double *uk, double *unext,
                      const StepConst &sc, const PredConst &pc, int k, cudaStream_t s);

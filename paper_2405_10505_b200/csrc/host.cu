@@ -88,6 +88,14 @@ struct fblts_ctx {
     std::vector<double> d_area, d_zb, d_dv, d_dc, d_W, d_kite, d_areaTri, d_fV;
     int sE = 0, sV = 0, ecS = 6;
     size_t xmax = 1;           // largest send/recv buffer (doubles)
+    // tiles of the owned cells (staged stage kernels)
+    std::vector<int32_t> t_start, t_info, t_halo, t_fedge;
+    std::vector<uint32_t> t_ecl;
+    std::vector<uint16_t> t_row;
+    int t_sRow = 32, t_hmax = 0, t_emax = 0;
+    size_t t_nHalo = 0, t_nFedge = 0, t_nEcl = 0;
+    bool tiled = true;
+    int nsm = 148;         // FBLTS_TILED=0 selects the unstaged kernels (development comparisons)
 };
 namespace {
 
@@ -245,6 +253,7 @@ int fblts_create(fblts_ctx **out, const fblts_config *cfg) {
         c->cfg.nccl_id = c->nccl_id;
     }
     c->stream = (cudaStream_t)cfg->stream;
+    if (const char *ev = std::getenv("FBLTS_TILED")) c->tiled = std::atoi(ev) != 0;
     // canonical constants (computed once in double, SURVEY c.1)
     StepConst &s = c->sc;
     const double dt = cfg->dt;
@@ -403,6 +412,103 @@ Bounds bounds_from(const int64_t *cnt, int begin, int end) {
     return b;
 }
 
+// Tiles of the owned cells for the staged stage kernels (fblts_internal.h TileMesh): tile starts
+// every TILE cells inside each region block, so every stage extent is a whole number of tiles.
+int build_tiles(fblts_ctx *c) {
+    const Local &L = c->lo;
+    const int G = c->ecS, maxE = c->hm.maxE;
+    std::vector<int32_t> bnd = {0, L.cb.if2, L.cb.if1, L.cb.f};
+    for (int l = 1; l <= 5; ++l) bnd.push_back(L.cb.fl[l]);
+    bnd.push_back(L.nOwnC);
+    std::sort(bnd.begin(), bnd.end());
+    bnd.erase(std::unique(bnd.begin(), bnd.end()), bnd.end());
+    std::vector<int32_t> &ts = c->t_start;
+    ts.clear();
+    for (size_t k = 0; k + 1 < bnd.size(); ++k)
+        for (int s = bnd[k]; s < bnd[k + 1]; s += TILE) ts.push_back(s);
+    ts.push_back(L.nOwnC);
+    const int nT = (int)ts.size() - 1;
+    c->t_sRow = pad32(std::max(1, L.nOwnC));
+    c->t_info.assign((size_t)(nT + 1) * TINFO, 0);
+    c->t_halo.clear();
+    c->t_fedge.clear();
+    c->t_ecl.clear();
+    c->t_row.assign((size_t)maxE * c->t_sRow, TILE_SENT);
+    c->t_hmax = 0;
+    c->t_emax = 0;
+    std::vector<int32_t> hl, el, fl;
+    for (int t = 0; t < nT; ++t) {
+        const int c0 = ts[t], c1 = ts[t + 1];
+        hl.clear();
+        el.clear();
+        fl.clear();
+        for (int i = c0; i < c1; ++i)
+            for (int j = 0; j < c->d_nEoC[i]; ++j) {
+                const int es = c->d_ec[((size_t)i * G + j) * 2], nb = c->d_ec[((size_t)i * G + j) * 2 + 1];
+                el.push_back(es >= 0 ? es : ~es);
+                if (nb < c0 || nb >= c1) hl.push_back(nb);
+            }
+        std::sort(hl.begin(), hl.end());
+        hl.erase(std::unique(hl.begin(), hl.end()), hl.end());
+        std::sort(el.begin(), el.end());
+        el.erase(std::unique(el.begin(), el.end()), el.end());
+        // longest run of consecutive edge indices = the owned range, the rest are foreign
+        size_t best = 0, bestLen = 0;
+        for (size_t k = 0; k < el.size();) {
+            size_t k2 = k + 1;
+            while (k2 < el.size() && el[k2] == el[k2 - 1] + 1) ++k2;
+            if (k2 - k > bestLen) best = k, bestLen = k2 - k;
+            k = k2;
+        }
+        const int eo0 = el.empty() ? 0 : el[best], eo1 = eo0 + (int)bestLen;
+        for (int e : el)
+            if (e < eo0 || e >= eo1) fl.push_back(e);
+        const int nLE = (int)el.size();
+        if (nLE + FGAP >= 0x7FFF || HALO0 + (int)hl.size() > 0xFFFF)
+            return fail(c, FBLTS_ERR_MESH, "tiles: tile %d has %d edges / %zu halo cells (too many)", t, nLE, hl.size());
+        int32_t *rec = &c->t_info[(size_t)t * TINFO];
+        rec[0] = c0, rec[1] = (int32_t)c->t_halo.size(), rec[2] = eo0, rec[3] = eo1;
+        rec[4] = (int32_t)c->t_fedge.size(), rec[5] = (int32_t)c->t_ecl.size();
+        auto lcell = [&](int x) {
+            return (uint32_t)((x >= c0 && x < c1) ? x - c0
+                                                  : HALO0 + (std::lower_bound(hl.begin(), hl.end(), x) - hl.begin()));
+        };
+        auto ledge = [&](int e) {
+            return (uint32_t)((e >= eo0 && e < eo1) ? e - eo0
+                                                    : (eo1 - eo0) + FGAP + (std::lower_bound(fl.begin(), fl.end(), e) - fl.begin()));
+        };
+        for (int i = c0; i < c1; ++i)
+            for (int j = 0; j < c->d_nEoC[i]; ++j) {
+                const int es = c->d_ec[((size_t)i * G + j) * 2];
+                c->t_row[(size_t)j * c->t_sRow + i] = (uint16_t)((es < 0 ? 0x8000u : 0u) | ledge(es >= 0 ? es : ~es));
+            }
+        auto push_pair = [&](int e) {
+            c->t_ecl.push_back(lcell(c->d_coe[2 * e + 1]) << 16 | lcell(c->d_coe[2 * e]));
+        };
+        for (int e = eo0; e < eo1; ++e) push_pair(e);
+        for (int e : fl) push_pair(e);
+        c->t_halo.insert(c->t_halo.end(), hl.begin(), hl.end());
+        c->t_fedge.insert(c->t_fedge.end(), fl.begin(), fl.end());
+        c->t_hmax = std::max(c->t_hmax, (int)hl.size());
+        c->t_emax = std::max(c->t_emax, nLE);
+    }
+    int32_t *rec = &c->t_info[(size_t)nT * TINFO];
+    rec[0] = L.nOwnC, rec[1] = (int32_t)c->t_halo.size(), rec[4] = (int32_t)c->t_fedge.size();
+    rec[5] = (int32_t)c->t_ecl.size();
+    c->t_nHalo = c->t_halo.size();
+    c->t_nFedge = c->t_fedge.size();
+    c->t_nEcl = c->t_ecl.size();
+    if (c->t_halo.empty()) c->t_halo.push_back(0);
+    if (c->t_fedge.empty()) c->t_fedge.push_back(0);
+    if (c->t_ecl.empty()) c->t_ecl.push_back(0);
+    return FBLTS_OK;
+}
+
+// first tile of the tile run starting at owned cell `cell` (a region block boundary)
+int tile_at(const fblts_ctx *c, int cell) {
+    return (int)(std::lower_bound(c->t_start.begin(), c->t_start.end(), cell) - c->t_start.begin());
+}
+
 int build_local(fblts_ctx *c, const std::vector<int32_t> &coc) {
     const HostMesh &m = c->hm;
     const Region &g = c->rg;
@@ -446,7 +552,20 @@ int build_local(fblts_ctx *c, const std::vector<int32_t> &coc) {
             (touches ? eOwnL : eRest).push_back(e);
         }
     }
-    auto eowner = [&](int e) { return std::min(cellLoc[m.coe[2 * e]], cellLoc[m.coe[2 * e + 1]]); };
+    // edge owner: the cell whose region code is the edge's (the smaller local index on a tie),
+    // falling back to an owned cell; then edges sorted by (code, owner) are also contiguous per
+    // owner-cell range, which gives every cell tile a contiguous range of its edges
+    auto eowner = [&](int e) {
+        const int a = m.coe[2 * e], b = m.coe[2 * e + 1];
+        const int la = cellLoc[a], lb = cellLoc[b];
+        const bool ma = g.cell[a] == g.edge[e] && la >= 0 && la < (int)own.size();
+        const bool mb = g.cell[b] == g.edge[e] && lb >= 0 && lb < (int)own.size();
+        if (ma && mb) return std::min(la, lb);
+        if (ma) return la;
+        if (mb) return lb;
+        if (la >= 0 && lb >= 0) return std::min(la, lb);
+        return la >= 0 ? la : lb;
+    };
     std::stable_sort(eOwnL.begin(), eOwnL.end(), [&](int a, int b) {
         if (g.edge[a] != g.edge[b]) return g.edge[a] < g.edge[b];
         return eowner(a) < eowner(b);
@@ -619,7 +738,7 @@ int build_local(fblts_ctx *c, const std::vector<int32_t> &coc) {
         c->d_xidx.insert(c->d_xidx.end(), L.x[x].recvIdx.begin(), L.x[x].recvIdx.end());
     }
     if (c->d_xidx.empty()) c->d_xidx.push_back(0);
-    return FBLTS_OK;
+    return build_tiles(c);
 }
 
 }  // namespace
@@ -694,6 +813,10 @@ int fblts_get_counts(fblts_ctx *c, int64_t *out) {
     out[21] = c->lo.nOwnC;
     out[22] = c->lo.nOwnE;
     out[23] = (int64_t)c->graph_nodes;
+    out[24] = (int64_t)c->t_start.size() - 1;
+    out[25] = (int64_t)c->t_nHalo;
+    out[26] = (int64_t)c->t_nEcl;
+    out[27] = stage_tiled_smem_bytes_host(3, c->t_hmax, c->t_emax);
     return FBLTS_OK;
 }
 
@@ -784,6 +907,22 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
     put(s.sendbuf, c->xmax);
     put(s.recvbuf, c->xmax);
     put(s.xidx, c->d_xidx.size());
+    TileMesh &tm = c->dm.tm;
+    int32_t *tInfo, *tHalo, *tFedge;
+    uint32_t *tEcl;
+    uint16_t *tRow;
+    put(tInfo, c->t_info.size());
+    put(tHalo, std::max<size_t>(1, c->t_nHalo));
+    put(tFedge, std::max<size_t>(1, c->t_nFedge));
+    put(tEcl, std::max<size_t>(1, c->t_nEcl));
+    put(tRow, (size_t)c->hm.maxE * c->t_sRow);
+    if (base) {
+        tm.nTiles = (int32_t)c->t_start.size() - 1;
+        tm.strideRow = c->t_sRow;
+        tm.hmax = c->t_hmax;
+        tm.emax = c->t_emax;
+        tm.info = tInfo, tm.halo = tHalo, tm.fedge = tFedge, tm.ecl = tEcl, tm.row = tRow;
+    }
     if (base) {
         d.nC = L.nC, d.nE = L.nE, d.nV = L.nV, d.nOwnC = L.nOwnC, d.nOwnE = L.nOwnE;
         d.strideC = L.nC, d.strideE = c->sE, d.strideV = c->sV;
@@ -853,11 +992,24 @@ int fblts_bind_workspace(fblts_ctx *c, void *ptr, size_t bytes) {
     CUDA_TRY(c, up(c->ds.cellOld, L.cellGlob.data(), (size_t)L.nC * 4));
     CUDA_TRY(c, up(c->ds.edgeOld, L.edgeGlob.data(), (size_t)L.nE * 4));
     CUDA_TRY(c, up(c->ds.xidx, c->d_xidx.data(), c->d_xidx.size() * 4));
+    const TileMesh &tm = d.tm;
+    CUDA_TRY(c, up(tm.info, c->t_info.data(), c->t_info.size() * 4));
+    CUDA_TRY(c, up(tm.halo, c->t_halo.data(), c->t_halo.size() * 4));
+    CUDA_TRY(c, up(tm.fedge, c->t_fedge.data(), c->t_fedge.size() * 4));
+    CUDA_TRY(c, up(tm.ecl, c->t_ecl.data(), c->t_ecl.size() * 4));
+    CUDA_TRY(c, up(tm.row, c->t_row.data(), c->t_row.size() * 2));
+    if (stage_tiled_smem_bytes_host(3, c->t_hmax, c->t_emax) > TILE_SMEM_MAX) c->tiled = false;   // pathological tiles
+    CUDA_TRY(c, cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->cfg.device));
+    if (c->tiled) CUDA_TRY(c, (cudaError_t)stage_tiled_configure(d));
     CUDA_TRY(c, cudaStreamSynchronize(s));
     // host staging of the big device tables is no longer needed
     std::vector<int32_t>().swap(c->d_ec);
     std::vector<int32_t>().swap(c->d_eoe);
     std::vector<double>().swap(c->d_W);
+    std::vector<int32_t>().swap(c->t_halo);
+    std::vector<int32_t>().swap(c->t_fedge);
+    std::vector<uint32_t>().swap(c->t_ecl);
+    std::vector<uint16_t>().swap(c->t_row);
     c->phase = P_BOUND;
     return FBLTS_OK;
 }
@@ -926,6 +1078,18 @@ struct PhaseX {
     double *a2;
 };
 
+void stage_tiled(fblts_ctx *c, int stage, int cbegin, int cend, const StageArgs &a, cudaStream_t s) {
+    if (cend <= cbegin) return;
+    const int t0 = tile_at(c, cbegin), t1 = tile_at(c, cend);
+    int hmax = 0, emax = 0;                  // shared memory sized for the tiles of this launch
+    for (int t = t0; t < t1; ++t) {
+        const int32_t *r = &c->t_info[(size_t)t * TINFO], *n = r + TINFO;
+        hmax = std::max(hmax, n[1] - r[1]);
+        emax = std::max(emax, r[3] - r[2] + n[4] - r[4]);
+    }
+    launch_stage_tiled(c->dm, stage, t0, t1, hmax, emax, c->nsm, a, c->ds.err, s);
+}
+
 // Enqueue phase `ph` of the step reading hbuf[par], ubuf[par]; returns false when past the end.
 bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec, PhaseX *px) {
     const DevMesh &m = c->dm;
@@ -949,9 +1113,12 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
         pc.c = 1.0 - (double)(k + 1) / (double)M;
         return pc;
     };
+    const bool T = c->tiled;
     auto fine_s1 = [&](int k) {
         mark(K_FINE_S1);
-        launch_fine_s1(m, st, hN, hNew, k == 0 ? hN : hb(k - 1), k == 0 ? uN : ub(k - 1), sc, pred(k), k, s);
+        const double *hk = k == 0 ? hN : hb(k - 1), *uk = k == 0 ? uN : ub(k - 1);
+        launch_fine_s1(m, st, hN, hNew, hk, uk, sc, pred(k), k, s, !T);
+        if (T) stage_tiled(c, 1, m.cb.fl[1], m.cb.end, StageArgs{hk, hk, uk, st.S, st.h1, 0, 0, 0, sc.c1f, sc.g, K_FINE_S1, k}, s);
     };
     *px = PhaseX{-1, nullptr, -1, nullptr};
     const int nfine = c->have_fine ? 3 * M : 0;
@@ -963,15 +1130,22 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
             launch_slow_edge(m, st, hN, sc, s);
         }
         mark(K_COARSE_S1);
-        launch_coarse_s1(m, st, hN, uN, sc, s);
+        if (c->tiled) stage_tiled(c, 1, 0, m.cb.fl[5], StageArgs{hN, hN, uN, st.S, st.h1, 0, 0, 0, sc.c1, sc.g, K_COARSE_S1, -1}, s);
+        else launch_coarse_s1(m, st, hN, uN, sc, s);
         *px = PhaseX{X_C1, st.h1, -1, nullptr};
     } else if (ph == 1) {
         mark(K_COARSE_S2);
-        launch_coarse_s2(m, st, hN, uN, sc, s);
+        if (c->tiled)
+            stage_tiled(c, 2, 0, m.cb.fl[3],
+                        StageArgs{hN, st.h1, uN, st.S, st.h2, sc.c1, sc.b1, sc.omb1, sc.c2, sc.g, K_COARSE_S2, -1}, s);
+        else launch_coarse_s2(m, st, hN, uN, sc, s);
         *px = PhaseX{X_C1, st.h2, -1, nullptr};
     } else if (ph == 2) {
         mark(K_COARSE_S3);
-        launch_coarse_s3(m, st, hN, uN, hNew, sc, s);
+        if (c->tiled)
+            stage_tiled(c, 3, 0, m.cb.fl[1],
+                        StageArgs{hN, st.h2, uN, st.S, hNew, sc.c2, sc.b2, sc.omb2, sc.c3, sc.g, K_COARSE_S3, -1}, s);
+        else launch_coarse_s3(m, st, hN, uN, hNew, sc, s);
         *px = PhaseX{X_C1, hNew, -1, nullptr};
     } else if (ph - 3 < nfine) {
         const int q = ph - 3, k = q / 3, stg = q % 3;
@@ -988,12 +1162,19 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
             *px = PhaseX{X_C1, st.h1, -1, nullptr};
         } else if (stg == 1) {
             mark(K_FINE_S2);
-            launch_fine_s2(m, st, hN, hNew, k == 0 ? hN : hb(k - 1), k == 0 ? uN : ub(k - 1), sc, pred(k), k, s);
+            const double *hk = k == 0 ? hN : hb(k - 1), *uk = k == 0 ? uN : ub(k - 1);
+            launch_fine_s2(m, st, hN, hNew, hk, uk, sc, pred(k), k, s, !T);
+            if (T)
+                stage_tiled(c, 2, m.cb.fl[1], m.cb.end,
+                            StageArgs{hk, st.h1, uk, st.S, st.h2, sc.c1f, sc.b1, sc.omb1, sc.c2f, sc.g, K_FINE_S2, k}, s);
             *px = PhaseX{X_C1, st.h2, -1, nullptr};
         } else {
             mark(K_FINE_S3);
-            launch_fine_s3(m, st, hN, uN, hNew, k == 0 ? hN : hb(k - 1), k == 0 ? uN : ub(k - 1), hb(k), sc, pred(k),
-                           k, s);
+            const double *hk = k == 0 ? hN : hb(k - 1), *uk = k == 0 ? uN : ub(k - 1);
+            launch_fine_s3(m, st, hN, uN, hNew, hk, uk, hb(k), sc, pred(k), k, s, !T);
+            if (T)
+                stage_tiled(c, 3, m.cb.fl[1], m.cb.end,
+                            StageArgs{hk, st.h2, uk, st.S, hb(k), sc.c2f, sc.b2, sc.omb2, sc.c3f, sc.g, K_FINE_S3, k}, s);
             *px = PhaseX{X_C1, hb(k), -1, nullptr};
         }
     } else if (ph == 3 + nfine) {

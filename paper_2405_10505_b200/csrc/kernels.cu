@@ -23,6 +23,8 @@
 // recomputed inside the stage-s cell kernel from the two cells of e instead of
 // being stored; the FB averages h*, h**, h*** and the IF-1 predictions (eq. preds,
 // P:L683-742) are likewise recomputed from the stored stage thicknesses.
+#include <algorithm>
+
 #include "fblts_internal.h"
 
 namespace fblts {
@@ -31,6 +33,9 @@ constexpr int TPB = 256;
 // min resident blocks per SM requested for the register-heavy stage kernels (occupancy knob)
 #ifndef FBLTS_MINB
 #define FBLTS_MINB 6
+#endif
+#ifndef FBLTS_TILE_MINB
+#define FBLTS_TILE_MINB 4
 #endif
 
 static inline unsigned nblocks(long n) { return (unsigned)((n + TPB - 1) / TPB); }
@@ -219,6 +224,250 @@ __global__ void __launch_bounds__(TPB, FBLTS_MINB) k_coarse_stage(DevMesh m, con
     const double v = hNi + ch * psi;
     out[i] = v;
     if (!(v > 0.0)) report(err, STAGE == 1 ? K_COARSE_S1 : (STAGE == 2 ? K_COARSE_S2 : K_COARSE_S3), -1, i, v);
+}
+
+// ---------------------------------------------------------------- staged stage sweep (tiles)
+// The same arithmetic as k_coarse_stage / the DEEP fine stages, reorganised per tile of TILE
+// consecutive cells (fblts_internal.h TileMesh) into an edge phase and a cell phase over shared
+// memory, in a persistent double-buffered TMA pipeline:
+//   * each CTA walks the tiles tile0 + blockIdx.x + k * gridDim.x; while it computes tile k the
+//     other shared buffer fills with tile k+1: one thread issues 1-D bulk copies (TMA,
+//     cp.async.bulk, completion counted on the buffer's mbarrier) of the tile's contiguous data
+//     -- its own cells, its owned edge run, its local-edge cell pairs -- and every thread adds
+//     8-byte asynchronous copies (LDGSTS) of the indexed data, the halo cells and foreign edges,
+//     whose index lists were prefetched into registers during the previous tile's compute;
+//   * edge phase: every local edge computes its flux term ONCE,
+//        T_e = l_e * ((0.5 (H_c0 + H_c1)) * u_bar_e),
+//     u_bar_e = u_e (stage 1) or u_e + cu (Phi^fast_e(bb H + omb h_base) + S_e) (stages 2, 3);
+//   * cell phase: Psi_i = -(sum_j n_{e_j,i} T_{e_j}) / A_i in slot order, out_i = h_base,i + ch Psi_i.
+// Bit-identical to the per-cell evaluation: 0.5 (H_i + H_n) is commutative in IEEE arithmetic and
+// Phi^fast_e is always evaluated as (c0, c1), so both cells of an edge see the same T_e; each
+// cell's sum keeps its sequential slot order from +0.0.
+// Bulk copies need 16-byte aligned source, destination and size: a contiguous double range [a, b)
+// is copied from a & ~1 to (b + 1) & ~1 (at most one element of slack at each end, inside the
+// 256-byte padded workspace allocation) and addressed in shared memory with offset a & 1.
+constexpr int HPT = 2;   // halo-cell indices prefetched per thread (more: loaded synchronously)
+constexpr int FPT = 2;   // foreign-edge indices prefetched per thread
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    unsigned ok = 0;
+    do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(ok)
+                     : "r"(smem_u32(bar)), "r"(parity)
+                     : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <int STAGE>
+struct TileShape {
+    static constexpr int NCA = STAGE > 1 ? 3 : 1;   // cell arrays: hprev (, hbase, z_b)
+    static constexpr int NEA = STAGE > 1 ? 4 : 2;   // edge arrays: u, l_e (, S, d_e)
+};
+
+struct TileRec {
+    int c0, c1, h0, h1, eo0, eo1, f0, f1, l0;
+};
+__device__ __forceinline__ TileRec load_rec(const TileMesh &t, int tile) {
+    const int *p = t.info + (size_t)tile * TINFO;
+    TileRec r;
+    r.c0 = p[0], r.h0 = p[1], r.eo0 = p[2], r.eo1 = p[3], r.f0 = p[4], r.l0 = p[5];
+    r.c1 = p[TINFO + 0], r.h1 = p[TINFO + 1], r.f1 = p[TINFO + 4];
+    return r;
+}
+
+// Shared buffer of one tile (strides in elements, every array 16-byte aligned):
+// cells [NCA][CS2], edges [NEA][ES2] (doubles), cell pairs [ES4] (uint32); the views below are
+// shifted by the tile's alignment offsets so that local index 0 is the tile's first cell / edge.
+template <int STAGE>
+struct TileBuf {
+    double *hp, *hb, *z, *u, *l, *S, *d;
+    uint32_t *ecl;
+    __device__ __forceinline__ TileBuf(double *B, int CS2, int ES2, const TileRec &r) {
+        const int oc = r.c0 & 1, oe = r.eo0 & 1, ol = r.l0 & 3;
+        hp = B + oc, hb = B + CS2 + oc, z = B + 2 * CS2 + oc;
+        double *E = B + TileShape<STAGE>::NCA * CS2;
+        u = E + oe, l = E + ES2 + oe, S = E + 2 * ES2 + oe, d = E + 3 * ES2 + oe;
+        ecl = reinterpret_cast<uint32_t *>(E + TileShape<STAGE>::NEA * ES2) + ol;
+    }
+};
+
+// one elected thread: bulk copies of the tile's contiguous ranges into buffer B, counted on bar
+template <int STAGE>
+__device__ __forceinline__ void issue_bulk(const DevMesh &m, const StageArgs &a, const TileRec &r, double *B,
+                                           int CS2, int ES2, uint64_t *bar) {
+    constexpr int NCA = TileShape<STAGE>::NCA, NEA = TileShape<STAGE>::NEA;
+    const int ca = r.c0 & ~1, cb = (r.c1 + 1) & ~1;
+    const int ea = r.eo0 & ~1, eb = (r.eo1 + 1) & ~1;
+    const int nLE = r.eo1 - r.eo0 + r.f1 - r.f0;
+    const int la = r.l0 & ~3, lb = (r.l0 + nLE + 3) & ~3;
+    const unsigned cbytes = 8u * (cb - ca), ebytes = 8u * (eb - ea), lbytes = 4u * (lb - la);
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic writes of the last use first
+    mbar_expect_tx(bar, NCA * cbytes + (ebytes ? NEA * ebytes : 0u) + lbytes);
+    bulk_g2s(B, a.hprev + ca, cbytes, bar);
+    if (STAGE > 1) {
+        bulk_g2s(B + CS2, a.hbase + ca, cbytes, bar);
+        bulk_g2s(B + 2 * CS2, m.zb + ca, cbytes, bar);
+    }
+    double *E = B + NCA * CS2;
+    if (ebytes) {
+        bulk_g2s(E, a.ubase + ea, ebytes, bar);
+        bulk_g2s(E + ES2, m.dv + ea, ebytes, bar);
+        if (STAGE > 1) {
+            bulk_g2s(E + 2 * ES2, a.S + ea, ebytes, bar);
+            bulk_g2s(E + 3 * ES2, m.dc + ea, ebytes, bar);
+        }
+    }
+    bulk_g2s(E + NEA * ES2, m.tm.ecl + la, lbytes, bar);
+}
+
+template <int STAGE>
+__device__ __forceinline__ void issue_indexed(const DevMesh &m, const StageArgs &a, const TileRec &r,
+                                              const TileBuf<STAGE> &b, int tid, const int (&hx)[HPT],
+                                              const int (&fx)[FPT]) {
+    const int nH = r.h1 - r.h0, nF = r.f1 - r.f0, nOE = r.eo1 - r.eo0;
+    auto halo = [&](int q, int x) {
+        cp_async8(b.hp + HALO0 + q, a.hprev + x);
+        if (STAGE > 1) {
+            cp_async8(b.hb + HALO0 + q, a.hbase + x);
+            cp_async8(b.z + HALO0 + q, m.zb + x);
+        }
+    };
+    auto foreign = [&](int p, int e) {
+        cp_async8(b.u + p, a.ubase + e);
+        cp_async8(b.l + p, m.dv + e);
+        if (STAGE > 1) {
+            cp_async8(b.S + p, a.S + e);
+            cp_async8(b.d + p, m.dc + e);
+        }
+    };
+#pragma unroll
+    for (int k = 0; k < HPT; ++k)
+        if (k * TILE + tid < nH) halo(k * TILE + tid, hx[k]);
+    for (int q = HPT * TILE + tid; q < nH; q += TILE) halo(q, m.tm.halo[r.h0 + q]);
+#pragma unroll
+    for (int k = 0; k < FPT; ++k)
+        if (k * TILE + tid < nF) foreign(nOE + FGAP + k * TILE + tid, fx[k]);
+    for (int q = FPT * TILE + tid; q < nF; q += TILE) foreign(nOE + FGAP + q, m.tm.fedge[r.f0 + q]);
+}
+
+__device__ __forceinline__ void load_indices(const TileMesh &t, const TileRec &r, int tid, int (&hx)[HPT], int (&fx)[FPT]) {
+#pragma unroll
+    for (int k = 0; k < HPT; ++k) {
+        const int q = k * TILE + tid;
+        hx[k] = q < r.h1 - r.h0 ? t.halo[r.h0 + q] : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < FPT; ++k) {
+        const int q = k * TILE + tid;
+        fx[k] = q < r.f1 - r.f0 ? t.fedge[r.f0 + q] : 0;
+    }
+}
+
+template <int G, int STAGE>
+__global__ void __launch_bounds__(TILE, 2) k_stage_tiled(DevMesh m, int tile0, int tile1, int CS2, int ES2,
+                                                         StageArgs a, DevError *err) {
+    extern __shared__ __align__(16) double smem[];
+    constexpr int NCA = TileShape<STAGE>::NCA, NEA = TileShape<STAGE>::NEA;
+    const int BUF = NCA * CS2 + NEA * ES2 + ES2 / 2 + 2;   // doubles per buffer (+ ecl, 16-B multiple)
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);    // 2 mbarriers
+    double *buf0 = smem + 2;
+    const TileMesh &t = m.tm;
+    const int tid = threadIdx.x;
+    int tile = tile0 + blockIdx.x;
+    if (tile >= tile1) return;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    int hx[HPT], fx[FPT];
+    TileRec nx = load_rec(t, tile);
+    if (tid == 0) issue_bulk<STAGE>(m, a, nx, buf0, CS2, ES2, &bar[0]);
+    load_indices(t, nx, tid, hx, fx);
+    issue_indexed<STAGE>(m, a, nx, TileBuf<STAGE>(buf0, CS2, ES2, nx), tid, hx, fx);
+    unsigned phase[2] = {0u, 0u};
+    int buf = 0;
+    for (; tile < tile1; tile += gridDim.x, buf ^= 1) {
+        const TileRec cur = nx;
+        const int tn = tile + gridDim.x;
+        const bool more = tn < tile1;
+        if (more) nx = load_rec(t, tn);
+        mbar_wait(&bar[buf], phase[buf]);
+        phase[buf] ^= 1u;
+        cp_async_wait_all();
+        __syncthreads();                                   // tile `cur` staged; buffer buf^1 free
+        double *Bn = buf0 + (buf ^ 1) * BUF;
+        if (more) {
+            if (tid == 0) issue_bulk<STAGE>(m, a, nx, Bn, CS2, ES2, &bar[buf ^ 1]);
+            load_indices(t, nx, tid, hx, fx);              // consumed after this tile's compute
+        }
+        const TileBuf<STAGE> bc(buf0 + buf * BUF, CS2, ES2, cur);
+        // ---- compute tile `cur`
+        const int nOwn = cur.c1 - cur.c0;
+        const int i = cur.c0 + tid;
+        const bool own = tid < nOwn;
+        uint16_t r[G];
+        double A = 1.0;
+        if (own) {
+#pragma unroll
+            for (int j = 0; j < G; ++j) r[j] = j < m.maxE ? t.row[(size_t)j * t.strideRow + i] : TILE_SENT;
+            A = m.areaCell[i];
+        }
+        const int nOE = cur.eo1 - cur.eo0, nLE = nOE + cur.f1 - cur.f0;
+        for (int p = tid; p < nLE; p += TILE) {          // edge phase: T_e overwrites u_e
+            const uint32_t pr = bc.ecl[p];
+            const int q = p < nOE ? p : p + FGAP;
+            const int l0 = pr & 0xFFFF, l1 = pr >> 16;
+            const double H0 = bc.hp[l0], H1 = bc.hp[l1];
+            double ue = bc.u[q];
+            if (STAGE > 1) {
+                const double HS0 = a.bb * H0 + a.omb * bc.hb[l0];
+                const double HS1 = a.bb * H1 + a.omb * bc.hb[l1];
+                const double phi = phi_fast(a.g, HS0, bc.z[l0], HS1, bc.z[l1], bc.d[q]);
+                ue = ue + a.cu * (phi + bc.S[q]);
+            }
+            const double Fe = (0.5 * (H0 + H1)) * ue;
+            bc.u[q] = bc.l[q] * Fe;
+        }
+        __syncthreads();
+        if (own) {                                        // cell phase
+            const double hbi = STAGE == 1 ? bc.hp[tid] : bc.hb[tid];
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+                if (r[j] != TILE_SENT) {
+                    const double tt = bc.u[r[j] & 0x7FFF];
+                    acc = acc + ((r[j] >> 15) ? -tt : tt);
+                }
+            }
+            const double psi = -acc / A;
+            const double v = hbi + a.ch * psi;
+            a.out[i] = v;
+            if (!(v > 0.0)) report(err, a.kind, a.k, i, v);
+        }
+        if (more) issue_indexed<STAGE>(m, a, nx, TileBuf<STAGE>(Bn, CS2, ES2, nx), tid, hx, fx);
+    }
 }
 
 // coarse FB averages (tilde / bar data)
@@ -635,6 +884,50 @@ __global__ void k_diag_final(const double *__restrict__ part, int nb, double *__
         }                          \
     } while (0)
 
+// strides of one shared tile buffer (elements, 16-byte multiples) and the dynamic smem bytes
+static void tile_strides(int hmax, int emax, int &CS2, int &ES2) {
+    CS2 = (HALO0 + hmax + 1 + 1) & ~1;     // + alignment offset, rounded to an even count
+    ES2 = (emax + FGAP + 8 + 3) & ~3;       // + gap and slack; multiple of 4 (the uint32 pair array)
+}
+int stage_tiled_smem_bytes_host(int stage, int hmax, int emax) {
+    const int nca = stage > 1 ? 3 : 1, nea = stage > 1 ? 4 : 2;
+    int CS2, ES2;
+    tile_strides(hmax, emax, CS2, ES2);
+    return 8 * (2 + 2 * (nca * CS2 + nea * ES2 + ES2 / 2 + 2));
+}
+
+int stage_tiled_configure(const DevMesh &m) {
+    cudaError_t e = cudaSuccess;
+    auto set = [&](const void *f) {      // process-wide attributes: the limit, not one context's need
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, TILE_SMEM_MAX);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    };
+    FBLTS_DISPATCH_G(m.ecS, {
+        set((const void *)k_stage_tiled<G, 1>);
+        set((const void *)k_stage_tiled<G, 2>);
+        set((const void *)k_stage_tiled<G, 3>);
+    });
+    return (int)e;
+}
+
+void launch_stage_tiled(const DevMesh &m, int stage, int tile0, int tile1, int hmax, int emax, int nsm,
+                        const StageArgs &a, DevError *err, cudaStream_t s) {
+    if (tile1 <= tile0) return;
+    const int smem = stage_tiled_smem_bytes_host(stage, hmax, emax);
+    int CS, ES;
+    tile_strides(hmax, emax, CS, ES);
+    FBLTS_DISPATCH_G(m.ecS, {
+        const void *f = stage == 1 ? (const void *)k_stage_tiled<G, 1>
+                                   : (stage == 2 ? (const void *)k_stage_tiled<G, 2> : (const void *)k_stage_tiled<G, 3>);
+        int per = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, TILE, smem);
+        const int grid = std::max(1, std::min(tile1 - tile0, nsm * std::max(1, per)));
+        if (stage == 1) k_stage_tiled<G, 1><<<grid, TILE, smem, s>>>(m, tile0, tile1, CS, ES, a, err);
+        else if (stage == 2) k_stage_tiled<G, 2><<<grid, TILE, smem, s>>>(m, tile0, tile1, CS, ES, a, err);
+        else k_stage_tiled<G, 3><<<grid, TILE, smem, s>>>(m, tile0, tile1, CS, ES, a, err);
+    });
+}
+
 void launch_slow_pre(const DevMesh &m, const DevState &st, const double *h, const double *u, cudaStream_t s) {
     const unsigned nbV = nblocks(m.nV), nbC = nblocks(m.nC), nbE = nblocks(m.nE);
     FBLTS_DISPATCH_G(m.ecS, k_slow_pre<G><<<nbV + nbC + nbE, TPB, 0, s>>>(m, h, u, st.q, st.K, st.F, nbV, nbC));
@@ -685,35 +978,35 @@ static FineArrays fine_arrays(const DevState &st, const double *hN, const double
 }
 // Fine kernels: BAND instance over [b0, b1) (needs the region views), DEEP over [b1, end).
 void launch_fine_s1(const DevMesh &m, const DevState &st, const double *hN, const double *hNew, const double *hk,
-                    const double *uk, const StepConst &sc, const PredConst &pc, int k, cudaStream_t s) {
+                    const double *uk, const StepConst &sc, const PredConst &pc, int k, cudaStream_t s, bool deep) {
     const FineArrays a = fine_arrays(st, hN, hNew, hk);
     const int b0 = m.cb.f, b1 = m.cb.fl[1], end = m.cb.end;
     FBLTS_DISPATCH_G(m.ecS, {
         if (b1 > b0) k_fine_s1<G, true><<<nblocks(b1 - b0), TPB, 0, s>>>(m, a, uk, st.h1, sc, pc, k, b0, b1, st.err);
-        if (end > b1) k_fine_s1<G, false><<<nblocks(end - b1), TPB, 0, s>>>(m, a, uk, st.h1, sc, pc, k, b1, end, st.err);
+        if (deep && end > b1) k_fine_s1<G, false><<<nblocks(end - b1), TPB, 0, s>>>(m, a, uk, st.h1, sc, pc, k, b1, end, st.err);
     });
 }
 void launch_fine_s2(const DevMesh &m, const DevState &st, const double *hN, const double *hNew, const double *hk,
-                    const double *uk, const StepConst &sc, const PredConst &pc, int k, cudaStream_t s) {
+                    const double *uk, const StepConst &sc, const PredConst &pc, int k, cudaStream_t s, bool deep) {
     const FineArrays a = fine_arrays(st, hN, hNew, hk);
     const int b0 = m.cb.f, b1 = m.cb.fl[1], end = m.cb.end;
     FBLTS_DISPATCH_G(m.ecS, {
         if (b1 > b0)
             k_fine_s2<G, true><<<nblocks(b1 - b0), TPB, 0, s>>>(m, a, uk, st.S, st.h2, sc, pc, k, b0, b1, st.err);
-        if (end > b1)
+        if (deep && end > b1)
             k_fine_s2<G, false><<<nblocks(end - b1), TPB, 0, s>>>(m, a, uk, st.S, st.h2, sc, pc, k, b1, end, st.err);
     });
 }
 void launch_fine_s3(const DevMesh &m, const DevState &st, const double *hN, const double *uN, const double *hNew,
                     const double *hk, const double *uk, double *hnext, const StepConst &sc, const PredConst &pc,
-                    int k, cudaStream_t s) {
+                    int k, cudaStream_t s, bool deep) {
     const FineArrays a = fine_arrays(st, hN, hNew, hk);
     const int b0 = m.cb.if2, b1 = m.cb.fl[1], end = m.cb.end;
     FBLTS_DISPATCH_G(m.ecS, {
         if (b1 > b0)
             k_fine_s3<G, true><<<nblocks(b1 - b0), TPB, 0, s>>>(m, a, uN, uk, st.S, hnext, st.accH, sc, pc, k, b0,
                                                                  b1, st.err);
-        if (end > b1)
+        if (deep && end > b1)
             k_fine_s3<G, false><<<nblocks(end - b1), TPB, 0, s>>>(m, a, uN, uk, st.S, hnext, st.accH, sc, pc, k, b1,
                                                                    end, st.err);
     });

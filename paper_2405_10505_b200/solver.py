@@ -50,7 +50,9 @@ class Solver:
         c = abi.fblts_get_counts(self.ctx)
         return {"nCells": int(c[0]), "nEdges": int(c[1]), "nVertices": int(c[2]),
                 "cells_by_region": c[3:12].tolist(), "edges_by_region": c[12:21].tolist(),
-                "owned_cells": int(c[21]), "owned_edges": int(c[22]), "kernels_per_step": int(c[23])}
+                "owned_cells": int(c[21]), "owned_edges": int(c[22]), "kernels_per_step": int(c[23]),
+                "tiles": int(c[24]), "tile_halo_cells": int(c[25]), "tile_edges": int(c[26]),
+                "tile_smem_bytes": int(c[27])}
 
     # --- state and stepping
     def set_state(self, h, u, t=0.0):
