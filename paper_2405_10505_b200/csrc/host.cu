@@ -95,6 +95,7 @@ struct fblts_ctx {
     int t_sRow = 32, t_hmax = 0, t_emax = 0;
     size_t t_nHalo = 0, t_nFedge = 0, t_nEcl = 0;
     bool tiled = true;
+    bool split = false;        // FBLTS_SPLIT=1: separate launches for the thin interface blocks
     int nsm = 148;         // FBLTS_TILED=0 selects the unstaged kernels (development comparisons)
 };
 namespace {
@@ -254,6 +255,7 @@ int fblts_create(fblts_ctx **out, const fblts_config *cfg) {
     }
     c->stream = (cudaStream_t)cfg->stream;
     if (const char *ev = std::getenv("FBLTS_TILED")) c->tiled = std::atoi(ev) != 0;
+    if (const char *ev = std::getenv("FBLTS_SPLIT")) c->split = std::atoi(ev) != 0;
     // canonical constants (computed once in double, SURVEY c.1)
     StepConst &s = c->sc;
     const double dt = cfg->dt;
@@ -1078,7 +1080,7 @@ struct PhaseX {
     double *a2;
 };
 
-void stage_tiled(fblts_ctx *c, int stage, int cbegin, int cend, const StageArgs &a, cudaStream_t s) {
+void stage_tiled_run(fblts_ctx *c, int stage, int cbegin, int cend, const StageArgs &a, cudaStream_t s) {
     if (cend <= cbegin) return;
     const int t0 = tile_at(c, cbegin), t1 = tile_at(c, cend);
     int hmax = 0, emax = 0;                  // shared memory sized for the tiles of this launch
@@ -1088,6 +1090,20 @@ void stage_tiled(fblts_ctx *c, int stage, int cbegin, int cend, const StageArgs 
         emax = std::max(emax, r[3] - r[2] + n[4] - r[4]);
     }
     launch_stage_tiled(c->dm, stage, t0, t1, hmax, emax, c->nsm, a, c->ds.err, s);
+}
+// The thin interface blocks [IF-2 .. F^5] have long, narrow tiles (more halo cells and edges per
+// cell); they get their own launch so that the bulk blocks (int, F\F^5) size shared memory for
+// compact tiles.
+void stage_tiled(fblts_ctx *c, int stage, int cbegin, int cend, const StageArgs &a, cudaStream_t s) {
+    if (!c->split) return stage_tiled_run(c, stage, cbegin, cend, a, s);
+    const int cuts[2] = {c->dm.cb.if2, c->dm.cb.fl[5]};
+    int lo = cbegin;
+    for (int k = 0; k < 2; ++k)
+        if (cuts[k] > lo && cuts[k] < cend) {
+            stage_tiled_run(c, stage, lo, cuts[k], a, s);
+            lo = cuts[k];
+        }
+    stage_tiled_run(c, stage, lo, cend, a, s);
 }
 
 // Enqueue phase `ph` of the step reading hbuf[par], ubuf[par]; returns false when past the end.

@@ -35,8 +35,13 @@ constexpr int TPB = 256;
 #define FBLTS_MINB 6
 #endif
 #ifndef FBLTS_TILE_MINB
-#define FBLTS_TILE_MINB 4
+#define FBLTS_TILE_MINB 2
 #endif
+#ifndef FBLTS_TILE_NTHR
+#define FBLTS_TILE_NTHR 256
+#endif
+constexpr int NTHR = FBLTS_TILE_NTHR;   // threads per tile CTA (>= TILE)
+static_assert(NTHR >= TILE, "one thread per tile cell in the cell phase");
 
 static inline unsigned nblocks(long n) { return (unsigned)((n + TPB - 1) / TPB); }
 
@@ -362,29 +367,29 @@ __device__ __forceinline__ void issue_indexed(const DevMesh &m, const StageArgs 
     };
 #pragma unroll
     for (int k = 0; k < HPT; ++k)
-        if (k * TILE + tid < nH) halo(k * TILE + tid, hx[k]);
-    for (int q = HPT * TILE + tid; q < nH; q += TILE) halo(q, m.tm.halo[r.h0 + q]);
+        if (k * NTHR + tid < nH) halo(k * NTHR + tid, hx[k]);
+    for (int q = HPT * NTHR + tid; q < nH; q += NTHR) halo(q, m.tm.halo[r.h0 + q]);
 #pragma unroll
     for (int k = 0; k < FPT; ++k)
-        if (k * TILE + tid < nF) foreign(nOE + FGAP + k * TILE + tid, fx[k]);
-    for (int q = FPT * TILE + tid; q < nF; q += TILE) foreign(nOE + FGAP + q, m.tm.fedge[r.f0 + q]);
+        if (k * NTHR + tid < nF) foreign(nOE + FGAP + k * NTHR + tid, fx[k]);
+    for (int q = FPT * NTHR + tid; q < nF; q += NTHR) foreign(nOE + FGAP + q, m.tm.fedge[r.f0 + q]);
 }
 
 __device__ __forceinline__ void load_indices(const TileMesh &t, const TileRec &r, int tid, int (&hx)[HPT], int (&fx)[FPT]) {
 #pragma unroll
     for (int k = 0; k < HPT; ++k) {
-        const int q = k * TILE + tid;
+        const int q = k * NTHR + tid;
         hx[k] = q < r.h1 - r.h0 ? t.halo[r.h0 + q] : 0;
     }
 #pragma unroll
     for (int k = 0; k < FPT; ++k) {
-        const int q = k * TILE + tid;
+        const int q = k * NTHR + tid;
         fx[k] = q < r.f1 - r.f0 ? t.fedge[r.f0 + q] : 0;
     }
 }
 
 template <int G, int STAGE>
-__global__ void __launch_bounds__(TILE, 2) k_stage_tiled(DevMesh m, int tile0, int tile1, int CS2, int ES2,
+__global__ void __launch_bounds__(NTHR, FBLTS_TILE_MINB) k_stage_tiled(DevMesh m, int tile0, int tile1, int CS2, int ES2,
                                                          StageArgs a, DevError *err) {
     extern __shared__ __align__(16) double smem[];
     constexpr int NCA = TileShape<STAGE>::NCA, NEA = TileShape<STAGE>::NEA;
@@ -435,7 +440,7 @@ __global__ void __launch_bounds__(TILE, 2) k_stage_tiled(DevMesh m, int tile0, i
             A = m.areaCell[i];
         }
         const int nOE = cur.eo1 - cur.eo0, nLE = nOE + cur.f1 - cur.f0;
-        for (int p = tid; p < nLE; p += TILE) {          // edge phase: T_e overwrites u_e
+        for (int p = tid; p < nLE; p += NTHR) {          // edge phase: T_e overwrites u_e
             const uint32_t pr = bc.ecl[p];
             const int q = p < nOE ? p : p + FGAP;
             const int l0 = pr & 0xFFFF, l1 = pr >> 16;
@@ -920,11 +925,11 @@ void launch_stage_tiled(const DevMesh &m, int stage, int tile0, int tile1, int h
         const void *f = stage == 1 ? (const void *)k_stage_tiled<G, 1>
                                    : (stage == 2 ? (const void *)k_stage_tiled<G, 2> : (const void *)k_stage_tiled<G, 3>);
         int per = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, TILE, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, NTHR, smem);
         const int grid = std::max(1, std::min(tile1 - tile0, nsm * std::max(1, per)));
-        if (stage == 1) k_stage_tiled<G, 1><<<grid, TILE, smem, s>>>(m, tile0, tile1, CS, ES, a, err);
-        else if (stage == 2) k_stage_tiled<G, 2><<<grid, TILE, smem, s>>>(m, tile0, tile1, CS, ES, a, err);
-        else k_stage_tiled<G, 3><<<grid, TILE, smem, s>>>(m, tile0, tile1, CS, ES, a, err);
+        if (stage == 1) k_stage_tiled<G, 1><<<grid, NTHR, smem, s>>>(m, tile0, tile1, CS, ES, a, err);
+        else if (stage == 2) k_stage_tiled<G, 2><<<grid, NTHR, smem, s>>>(m, tile0, tile1, CS, ES, a, err);
+        else k_stage_tiled<G, 3><<<grid, NTHR, smem, s>>>(m, tile0, tile1, CS, ES, a, err);
     });
 }
 
