@@ -47,8 +47,10 @@ def subdivide(v, f, levels):
     return v, f
 
 
-def build_icosahedral_mesh(level: int, radius: float = EARTH_R) -> Mesh:
-    v, f = subdivide(*icosahedron(), level)
+def mesh_from_sphere_triangulation(v, f, radius: float = EARTH_R) -> Mesh:
+    """TRiSK mesh of the Voronoi dual of a Delaunay triangulation of the unit sphere: generators
+    v [n,3] (unit vectors), triangles f [m,3]; Voronoi vertices at the triangle circumcentres."""
+    f = np.array(f, dtype=np.int64, copy=True)
     # orient every triangle counter-clockwise seen from outside
     nrm = np.cross(v[f[:, 1]] - v[f[:, 0]], v[f[:, 2]] - v[f[:, 0]])
     flip = np.sum(nrm * v[f[:, 0]], axis=1) < 0
@@ -83,5 +85,9 @@ def build_icosahedral_mesh(level: int, radius: float = EARTH_R) -> Mesh:
         nxt = cur.copy()
         nxt[act] = rb[rec]
         cur = nxt
-    mesh = build_trisk_mesh(nbrs, verts, deg.astype(np.int32), v * radius, cc * radius, Sphere(radius))
-    return mesh
+    return build_trisk_mesh(nbrs, verts, deg.astype(np.int32), v * radius, cc * radius, Sphere(radius))
+
+
+def build_icosahedral_mesh(level: int, radius: float = EARTH_R) -> Mesh:
+    v, f = subdivide(*icosahedron(), level)
+    return mesh_from_sphere_triangulation(v, f, radius)
