@@ -43,6 +43,10 @@ def make_case(name, rank=0):
         return configs.config1()
     if name == "config3":
         return configs.config3()
+    if name == "config4":
+        return configs.config4()                         # ~10 min of host mesh generation (50 Lloyd iterations)
+    if name.startswith("config4_"):                      # config4_<k>: the recipe at dx_scale = k
+        return configs.config4(dx_scale=float(name.split("_")[1]))
     if name.startswith("config5_"):                      # config5_<n>: n x n block of the config-5 recipe
         n = int(name.split("_")[1])
         return configs.config5(nx=n, ny=n)

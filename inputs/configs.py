@@ -212,3 +212,60 @@ def config3(seed=3, dt=None, level=8, n_steps=500) -> Case:
     return Case(name="config3", mesh=mesh, h0=H + eta, u0=np.zeros(mesh.nEdges),
                 fine_mask=np.zeros(mesh.nCells, dtype=bool), tau_n=np.zeros(mesh.nEdges), M=1, dt=dt,
                 n_steps=n_steps, seed=seed)
+
+
+def config4(seed=4, dt=None, dx_scale=1.0, n_lloyd=50, M=8, n_steps=100, verbose=False) -> Case:
+    """BASELINE config 4: variable-resolution spherical centroidal Voronoi mesh (inputs/scvt.py):
+    seeded points, a fixed 50 Lloyd iterations under rho ~ dx^-4, dx = 30 km globally refined to
+    2 km in a seeded disk of 500 km diameter (tanh transition, 150 km); N from the resolution spec
+    (reading Q24, ~0.8 M cells).  Shelf bathymetry across the disk (Q24): along a seeded direction
+    s through the disk centre H_shelf = 5 + 3995 (1 + tanh(s / 50 km)) / 2, blended to 4000 m
+    outside the disk by w = (1 - tanh((d - 250 km) / 50 km)) / 2.  f = 2 Omega sin(phi) (Q28).  Fine
+    region = cells whose target dx < 15 km (Q24), M = 8, r = 2.  u = 0, a 1 m Gaussian surge
+    (sigma 50 km, great-circle) at a seeded point of the disk.  dt: 0.9 x the oracle-bisected
+    Courant limit nu_loc (configs/dt.json "config4", measured on the dx_scale = 8 reduction of the
+    same recipe) applied to this mesh's max_e sqrt(g max H) dt_e / d_e, with dt_e = dt / M on the
+    edges touching a fine cell (the F_E rule, reading Q7).
+
+    dx_scale multiplies the two resolutions (and the fine threshold) only: the disk, the
+    transition and the shelf keep their size, so a reduced case has the same geometry with
+    dx_scale^2 fewer background cells (dx_scale = 8: ~10 k cells, for the parity tests)."""
+    from .scvt import Refinement, build_scvt
+    rng = np.random.default_rng(seed)
+    centre = rng.standard_normal(3)
+    centre /= np.linalg.norm(centre)
+    ref = Refinement(centre, dx_coarse=30e3 * dx_scale, dx_fine=2e3 * dx_scale, beta=250e3, alpha=150e3)
+    mesh, _ = build_scvt(ref, rng, n_lloyd=n_lloyd, verbose=verbose)
+    R = mesh.radius
+    x = np.stack([mesh.xCell, mesh.yCell, mesh.zCell], axis=1) / R
+    # shelf across the disk along a seeded tangent direction t at the centre
+    t = np.cross(centre, rng.standard_normal(3))
+    t /= np.linalg.norm(t)
+    s = R * np.arcsin(np.clip(x @ t, -1.0, 1.0))
+    H_shelf = 5.0 + 3995.0 * 0.5 * (1.0 + np.tanh(s / 50e3))
+    d = ref.dist(x)
+    w = 0.5 * (1.0 - np.tanh((d - ref.beta) / 50e3))      # 1 inside the disk, 0 outside (shelf scale)
+    H = 4000.0 + (H_shelf - 4000.0) * w
+    mesh.bottomDepth = H
+    lat_v = np.arcsin(np.clip(mesh.zVertex / R, -1.0, 1.0))
+    mesh.fVertex = 2.0 * OMEGA * np.sin(lat_v)
+    fine = ref.dx(x) < 15e3 * dx_scale
+    # surge centre: uniform in the disk (radius beta) around the disk centre
+    a = rng.uniform(0.0, 2.0 * np.pi)
+    rr = ref.beta * np.sqrt(rng.uniform(0.0, 1.0))
+    e1 = np.cross(centre, t)
+    pc = np.cos(rr / R) * centre + np.sin(rr / R) * (np.cos(a) * t + np.sin(a) * e1)
+    ds = R * np.arccos(np.clip(x @ pc, -1.0, 1.0))
+    eta = 1.0 * np.exp(-(ds * ds) / (2.0 * 50e3 * 50e3))
+    if dt is None:
+        try:
+            with open(DT_TABLE) as f:
+                nu = float(json.load(f)["config4"]["nu_loc_limit"])
+        except (OSError, KeyError, ValueError):
+            nu = 1.0
+        c0, c1 = mesh.cellsOnEdge[:, 0], mesh.cellsOnEdge[:, 1]
+        ce = np.sqrt(G * np.maximum(H[c0], H[c1])) / mesh.dcEdge
+        ce = np.where(fine[c0] | fine[c1], ce / M, ce)
+        dt = 0.9 * nu / np.max(ce)
+    return Case(name="config4", mesh=mesh, h0=H + eta, u0=np.zeros(mesh.nEdges), fine_mask=fine,
+                tau_n=np.zeros(mesh.nEdges), M=M, dt=dt, n_steps=n_steps, seed=seed)

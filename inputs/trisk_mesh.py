@@ -108,6 +108,13 @@ class PlanarTorus:
         v = self.disp(a, c)
         return 0.5 * np.abs(u[..., 0] * v[..., 1] - u[..., 1] * v[..., 0])
 
+    def signed_tri_area(self, a, b, c):
+        """Signed area, positive for counter-clockwise (a,b,c); equals tri_area for CCW triangles."""
+        u = self.disp(a, b)
+        v = self.disp(a, c)
+        cr = u[..., 0] * v[..., 1] - u[..., 1] * v[..., 0]
+        return np.where(cr >= 0, 0.5 * np.abs(cr), -(0.5 * np.abs(cr)))
+
     def tangent_dir(self, p, a, b):
         d = self.disp(a, b)
         return d / np.linalg.norm(d, axis=-1, keepdims=True)
@@ -139,6 +146,14 @@ class Sphere:
         num = np.abs(np.sum(ua * np.cross(ub, uc), axis=-1))
         den = 1.0 + np.sum(ua * ub, axis=-1) + np.sum(ub * uc, axis=-1) + np.sum(uc * ua, axis=-1)
         return 2.0 * np.arctan2(num, den) * self.R ** 2
+
+    def signed_tri_area(self, a, b, c):
+        """Signed spherical area, positive for (a,b,c) counter-clockwise seen from outside; equals
+        tri_area for such triangles."""
+        ua, ub, uc = self._unit(a), self._unit(b), self._unit(c)
+        trip = np.sum(ua * np.cross(ub, uc), axis=-1)
+        area = self.tri_area(a, b, c)
+        return np.where(trip >= 0, area, -area)
 
     def tangent_dir(self, p, a, b):
         """Unit tangent at point p pointing along the great circle from a to b."""
@@ -226,7 +241,9 @@ def build_trisk_mesh(cell_nbrs: np.ndarray, cell_verts: np.ndarray, n_on_cell: n
         xa = edgePoint[ea]
         xb = edgePoint[eb]
         xv = vert_pos[vv]
-        kiteOnCell[cidx, j] = geom.tri_area(xi, xa, xv) + geom.tri_area(xi, xv, xb)
+        # signed (counter-clockwise positive) sub-triangles: where an obtuse Delaunay triangle puts
+        # the vertex beyond the edge, one part is negative and the kites still tile the domain
+        kiteOnCell[cidx, j] = geom.signed_tri_area(xi, xa, xv) + geom.signed_tri_area(xi, xv, xb)
     areaCell = np.zeros(nC, dtype=F64)
     for j in range(maxE):
         areaCell = areaCell + np.where(valid[:, j], kiteOnCell[:, j], 0.0)

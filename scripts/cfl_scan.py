@@ -69,6 +69,10 @@ def main(names):
             # the level-5 dual (10,242 cells) of the config-3 recipe; the Courant limit nu_loc
             # is applied to the level-8 mesh by inputs.configs.config3
             case = configs.config3(level=5, dt=1.0)
+        elif name == "config4":
+            # the dx_scale = 8 reduction of the config-4 recipe (~12 k cells, same disk, shelf and
+            # M = 8); the Courant limit nu_loc is applied to the full mesh by inputs.configs.config4
+            case = configs.config4(dx_scale=8, dt=1.0)
         elif name == "config5":
             # proxy: one 256-km tile of config 5 (same dc, profile, roughness recipe, M) in x,
             # 128 km in y; the full 4096^2 mesh is too large for 300 oracle steps per trial.

@@ -280,3 +280,13 @@ def test_parity_config5_full_size(Solver):
     fscale = float(np.sum(c.mesh.areaTriangle * np.abs(c.mesh.fVertex)))
     assert abs(d1[1] - d0[1]) <= DRIFT * fscale
     s.close()
+
+
+def test_parity_config4_reduced_100_steps(Solver):
+    """Config-4 recipe (variable-resolution SCVT sphere, shelf disk, M = 8, full Coriolis) at
+    dx_scale = 8 (~12 k cells, maxEdges 8), 100 coarse steps element by element."""
+    c = configs.config4(dx_scale=8)
+    ho, uo, _ = run_oracle(c, 100)
+    _, hg, ug, _ = run_gpu(Solver, c, 100)
+    eh, eu = assert_parity(hg, ug, ho, uo)
+    print(f"config4 (dx_scale 8): eps_h={eh:.3e} eps_u={eu:.3e}")
