@@ -24,10 +24,10 @@ enum KernelKind {
     K_FINE_S1, K_FINE_S2, K_FINE_S3, K_FINE_VEL, K_CORRECT, K_NUM
 };
 
-// Region boundaries of one region-major block: [0,if2) int, [if2,if1) IF-2,
+// Region boundaries of one region-major block: [begin,if2) int, [if2,if1) IF-2,
 // [if1,f) IF-1, [f,end) fine; fl[l] = end of F^l (l = 1..5), fl[0] = f.
 struct Bounds {
-    int32_t if2, if1, f, end;
+    int32_t begin, if2, if1, f, end;
     int32_t fl[6];
 };
 
@@ -89,7 +89,13 @@ struct DevMesh {
     const double *__restrict__ fV;     // [nV]
     const uint8_t *__restrict__ vOwn;  // [nV] 1 if this rank reports the vertex in the diagnostics
     const uint8_t *__restrict__ eOwn;  // [nE] 1 if this rank reports the edge in the diagnostics
-    Bounds cb, eb;                     // owned cell / edge region bounds (cb.end = nOwnC, eb.end = nOwnE)
+    // Owned cells form two region-major blocks: the BOUNDARY block [0, nB) (cells some peer holds
+    // in its ring-1 halo; all owned cells when there is one rank) and the INTERIOR block
+    // [nB, nOwnC), so that a stage can compute the boundary block, hand it to the halo exchange
+    // and compute the interior block while the exchange is in flight.
+    int32_t nB;
+    Bounds cb, cbI;                    // boundary / interior cell blocks (absolute indices)
+    Bounds eb;                         // edges touching owned cells (eb.end = nOwnE)
     Bounds cbh;                        // halo cell block [nOwnC, nC), region-major, absolute indices
     TileMesh tm;                       // tiles of the owned cells
 };
@@ -125,7 +131,7 @@ struct DevState {
     double *uN, *uNew, *uT, *S, *F;     // edges
     double *q;                          // vertices
     double *K;                          // cells
-    double *accH, *accU;                // IF cells [cb.if2, cb.f), IF edges [eb.if2, eb.f)
+    double *accH, *accU;                // accH indexed by owned cell (IF cells used), accU by e - eb.if2 (IF edges)
     double *stage;                      // staging for set/get_state (max(nC, nE) doubles)
     int32_t *cellOld, *edgeOld;         // new -> old permutation (device)
     double *diag;                       // reduction scratch
@@ -153,28 +159,30 @@ int stage_tiled_configure(const DevMesh &m);      // sets the dynamic shared-mem
 // Kernel launchers (kernels.cu).  All enqueue on `s`.
 void launch_slow_pre(const DevMesh &m, const DevState &st, const double *h, const double *u, cudaStream_t s);
 void launch_slow_edge(const DevMesh &m, const DevState &st, const double *h, const StepConst &sc, cudaStream_t s);
+// cell launchers act on one owned cell block b (DevMesh::cb or DevMesh::cbI)
 void launch_coarse_s1(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
-                      const StepConst &sc, cudaStream_t s);
+                      const StepConst &sc, cudaStream_t s, const Bounds &b);
 void launch_coarse_s2(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
-                      const StepConst &sc, cudaStream_t s);
+                      const StepConst &sc, cudaStream_t s, const Bounds &b);
 void launch_coarse_s3(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
-                      double *hNew, const StepConst &sc, cudaStream_t s);
+                      double *hNew, const StepConst &sc, cudaStream_t s, const Bounds &b);
 void launch_coarse_vel(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
                        const double *hNew, double *uNew, const StepConst &sc, cudaStream_t s);
 void launch_fine_s1(const DevMesh &m, const DevState &st, const double *hN, const double *hNew,
                     const double *hk, const double *uk, const StepConst &sc, const PredConst &pc,
-                    int k, cudaStream_t s, bool deep = true);
+                    int k, cudaStream_t s, const Bounds &b, bool deep = true);
 void launch_fine_s2(const DevMesh &m, const DevState &st, const double *hN, const double *hNew,
                     const double *hk, const double *uk, const StepConst &sc, const PredConst &pc,
-                    int k, cudaStream_t s, bool deep = true);
+                    int k, cudaStream_t s, const Bounds &b, bool deep = true);
 void launch_fine_s3(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
                     const double *hNew, const double *hk, const double *uk, double *hnext,
-                    const StepConst &sc, const PredConst &pc, int k, cudaStream_t s, bool deep = true);
+                    const StepConst &sc, const PredConst &pc, int k, cudaStream_t s, const Bounds &b,
+                    bool deep = true);
 void launch_fine_vel(const DevMesh &m, const DevState &st, const double *hN, const double *hNew,
                      const double *hk, const double *hnext, const double *uk, double *unext,
                      const StepConst &sc, const PredConst &pc, int k, cudaStream_t s);
 void launch_correct(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
-                    double *hNew, double *uNew, const StepConst &sc, cudaStream_t s);
+                    double *hNew, double *uNew, const StepConst &sc, cudaStream_t s, const Bounds &b, bool edges);
 void launch_permute_in(const int32_t *old_of_new, const double *src, double *dst, int n, cudaStream_t s);
 void launch_permute_out(const int32_t *old_of_new, const double *src, double *dst, int n, cudaStream_t s);
 // diagnostics: writes out[4] (device) = mass, Gamma, min h, max nu

@@ -50,8 +50,9 @@ enum { X_C1 = 0, X_C2 = 1, X_E = 2, X_NUM = 3 };
 
 struct Local {                  // this rank's subdomain in local (device) numbering
     int nOwnC = 0, nC = 0, nOwnE = 0, nE = 0, nV = 0;
+    int nB = 0;                                          // boundary block [0, nB) of the owned cells
     std::vector<int32_t> cellGlob, edgeGlob, vertGlob;   // local -> global
-    Bounds cb{}, cbh{}, eb{};
+    Bounds cb{}, cbI{}, cbh{}, eb{};
     int64_t ocount[9]{}, oecount[9]{};                   // owned cells / edges touching owned, per code
     std::vector<uint8_t> vOwn, eOwn;
     Xchg x[X_NUM];
@@ -63,6 +64,8 @@ struct fblts_ctx {
     fblts_config cfg{};
     cudaStream_t stream = nullptr;
     cudaStream_t cap = nullptr;
+    cudaStream_t comm = nullptr;            // halo-exchange stream (nranks > 1)
+    cudaEvent_t evFork = nullptr, evJoin = nullptr;
     std::string err;
     int phase = P_CREATED;
     HostMesh hm;
@@ -405,6 +408,7 @@ std::vector<int8_t> dist_from(const HostMesh &m, const std::vector<int32_t> &coc
 
 Bounds bounds_from(const int64_t *cnt, int begin, int end) {
     Bounds b{};
+    b.begin = begin;
     b.if2 = begin + (int)cnt[0];
     b.if1 = b.if2 + (int)cnt[1];
     b.f = b.if1 + (int)cnt[2];
@@ -419,9 +423,12 @@ Bounds bounds_from(const int64_t *cnt, int begin, int end) {
 int build_tiles(fblts_ctx *c) {
     const Local &L = c->lo;
     const int G = c->ecS, maxE = c->hm.maxE;
-    std::vector<int32_t> bnd = {0, L.cb.if2, L.cb.if1, L.cb.f};
-    for (int l = 1; l <= 5; ++l) bnd.push_back(L.cb.fl[l]);
-    bnd.push_back(L.nOwnC);
+    std::vector<int32_t> bnd;
+    for (const Bounds *b : {&L.cb, &L.cbI}) {
+        bnd.insert(bnd.end(), {b->begin, b->if2, b->if1, b->f});
+        for (int l = 1; l <= 5; ++l) bnd.push_back(b->fl[l]);
+        bnd.push_back(b->end);
+    }
     std::sort(bnd.begin(), bnd.end());
     bnd.erase(std::unique(bnd.begin(), bnd.end()), bnd.end());
     std::vector<int32_t> &ts = c->t_start;
@@ -525,7 +532,16 @@ int build_local(fblts_ctx *c, const std::vector<int32_t> &coc) {
         if (dme[i] == 0) own.push_back(i);
         else if (dme[i] <= 2) halo.push_back(i);
     }
+    // boundary block first (owned cells with a neighbour owned by another rank: what the peers'
+    // ring-1 halos hold), then the interior block; each region-major, SFC inside a region.  With
+    // one rank every owned cell is in the first block.
+    std::vector<uint8_t> isB(m.nC, R == 1 ? 1 : 0);
+    if (R > 1)
+        for (int i : own)
+            for (int j = 0; j < m.nEoC[i]; ++j)
+                if (part[coc[(size_t)i * m.maxE + j]] != me) isB[i] = 1;
     std::stable_sort(own.begin(), own.end(), [&](int a, int b) {
+        if (isB[a] != isB[b]) return isB[a] > isB[b];
         if (g.cell[a] != g.cell[b]) return g.cell[a] < g.cell[b];
         return key[a] < key[b];
     });
@@ -535,6 +551,8 @@ int build_local(fblts_ctx *c, const std::vector<int32_t> &coc) {
         return key[a] < key[b];
     });
     L.nOwnC = (int)own.size();
+    L.nB = 0;
+    for (int i : own) L.nB += isB[i];
     L.cellGlob = own;
     L.cellGlob.insert(L.cellGlob.end(), halo.begin(), halo.end());
     L.nC = (int)L.cellGlob.size();
@@ -609,10 +627,15 @@ int build_local(fblts_ctx *c, const std::vector<int32_t> &coc) {
     std::fill(L.ocount, L.ocount + 9, 0);
     std::fill(L.oecount, L.oecount + 9, 0);
     int64_t hcount[9] = {0};
-    for (int k = 0; k < L.nOwnC; ++k) L.ocount[g.cell[L.cellGlob[k]]]++;
+    int64_t bcount[9] = {0}, icount[9] = {0};
+    for (int k = 0; k < L.nOwnC; ++k) {
+        L.ocount[g.cell[L.cellGlob[k]]]++;
+        (k < L.nB ? bcount : icount)[g.cell[L.cellGlob[k]]]++;
+    }
     for (int k = L.nOwnC; k < L.nC; ++k) hcount[g.cell[L.cellGlob[k]]]++;
     for (int k = 0; k < L.nOwnE; ++k) L.oecount[g.edge[L.edgeGlob[k]]]++;
-    L.cb = bounds_from(L.ocount, 0, L.nOwnC);
+    L.cb = bounds_from(bcount, 0, L.nB);
+    L.cbI = bounds_from(icount, L.nB, L.nOwnC);
     L.cbh = bounds_from(hcount, L.nOwnC, L.nC);
     L.eb = bounds_from(L.oecount, 0, L.nOwnE);
     // diagnostics ownership: the rank owning cellsOnVertex[v][0] / cellsOnEdge[e][0]
@@ -620,7 +643,7 @@ int build_local(fblts_ctx *c, const std::vector<int32_t> &coc) {
     for (int v = 0; v < L.nV; ++v) L.vOwn[v] = part[m.cov[3 * L.vertGlob[v]]] == me;
     L.eOwn.assign(L.nE, 0);
     for (int e = 0; e < L.nOwnE; ++e) L.eOwn[e] = part[m.coe[2 * L.edgeGlob[e]]] == me;
-    c->have_fine = L.cb.f < L.nOwnC;
+    c->have_fine = g.ccount[3] + g.ccount[4] + g.ccount[5] + g.ccount[6] + g.ccount[7] + g.ccount[8] > 0;   // global
     // ---- device tables in local numbering (dummy edge index nE for ring-2 slots outside the subdomain)
     c->sE = pad32(L.nE);
     c->sV = pad32(L.nV);
@@ -899,7 +922,7 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
     put(s.S, L.nE);
     put(s.F, nE1);
     put(s.q, L.nV);
-    put(s.accH, std::max(1, L.cb.f - L.cb.if2));
+    put(s.accH, std::max(1, L.nOwnC));
     put(s.accU, std::max(1, L.eb.f - L.eb.if2));
     put(s.stage, std::max(m.nC, m.nE));
     put(s.cellOld, L.nC);
@@ -933,7 +956,7 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
         d.coe = coe, d.voe = voe, d.dv = dv, d.dc = dc, d.nEoE = nEoE, d.eoe = eoe, d.W = W, d.tau = tau;
         d.eov = eov, d.cov = cov, d.kite = kite, d.areaTri = areaTri, d.fV = fV;
         d.vOwn = vOwn, d.eOwn = eOwn;
-        d.cb = L.cb, d.eb = L.eb, d.cbh = L.cbh;
+        d.nB = L.nB, d.cb = L.cb, d.cbI = L.cbI, d.eb = L.eb, d.cbh = L.cbh;
         c->hbuf[0] = hA, c->hbuf[1] = hB, c->ubuf[0] = uA, c->ubuf[1] = uB;
         s.hN = hA, s.hNew = hB, s.uN = uA, s.uNew = uB;
         c->diag_out = s.diag + 296 * 6;
@@ -959,6 +982,11 @@ int fblts_bind_workspace(fblts_ctx *c, void *ptr, size_t bytes) {
     if ((uintptr_t)ptr % 256) return fail(c, FBLTS_ERR_INVALID_ARG, "bind_workspace: pointer not 256-B aligned");
     CUDA_TRY(c, cudaSetDevice(c->cfg.device));
     if (!c->cap) CUDA_TRY(c, cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
+    if (c->cfg.nranks > 1 && !c->comm) {
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->evFork, cudaEventDisableTiming));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->evJoin, cudaEventDisableTiming));
+    }
     if (c->cfg.nranks > 1 && !c->nccl && c->cfg.nccl_id) {   // no id: loopback group member
         const int rc = nccl_init(c);
         if (rc) return rc;
@@ -1092,11 +1120,11 @@ void stage_tiled_run(fblts_ctx *c, int stage, int cbegin, int cend, const StageA
     launch_stage_tiled(c->dm, stage, t0, t1, hmax, emax, c->nsm, a, c->ds.err, s);
 }
 // The thin interface blocks [IF-2 .. F^5] have long, narrow tiles (more halo cells and edges per
-// cell); they get their own launch so that the bulk blocks (int, F\F^5) size shared memory for
-// compact tiles.
-void stage_tiled(fblts_ctx *c, int stage, int cbegin, int cend, const StageArgs &a, cudaStream_t s) {
+// cell); with FBLTS_SPLIT=1 they get their own launch so that the bulk blocks (int, F\F^5) size
+// shared memory for compact tiles.
+void stage_tiled(fblts_ctx *c, int stage, const Bounds &B, int cbegin, int cend, const StageArgs &a, cudaStream_t s) {
     if (!c->split) return stage_tiled_run(c, stage, cbegin, cend, a, s);
-    const int cuts[2] = {c->dm.cb.if2, c->dm.cb.fl[5]};
+    const int cuts[2] = {B.if2, B.fl[5]};
     int lo = cbegin;
     for (int k = 0; k < 2; ++k)
         if (cuts[k] > lo && cuts[k] < cend) {
@@ -1106,13 +1134,19 @@ void stage_tiled(fblts_ctx *c, int stage, int cbegin, int cend, const StageArgs 
     stage_tiled_run(c, stage, lo, cend, a, s);
 }
 
-// Enqueue phase `ph` of the step reading hbuf[par], ubuf[par]; returns false when past the end.
-bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec, PhaseX *px) {
+// Enqueue part `part` of phase `ph` of the step reading hbuf[par], ubuf[par]; returns false when
+// past the end.  Part 0 = the phase's edge / slow kernels and its cell kernel on the BOUNDARY block
+// (DevMesh::cb); part 1 = the cell kernel on the INTERIOR block (DevMesh::cbI).  The phase's halo
+// exchange (PhaseX) reads only boundary-block cells, so with several ranks it runs between the
+// two parts, overlapped with part 1.
+bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec, PhaseX *px, int part) {
     const DevMesh &m = c->dm;
     DevState st = c->ds;
     const StepConst &sc = c->sc;
     const double *hN = c->hbuf[par], *uN = c->ubuf[par];
     double *hNew = c->hbuf[1 - par], *uNew = c->ubuf[1 - par];
+    const Bounds &B = part == 0 ? m.cb : m.cbI;
+    const bool cells = B.end > B.begin;       // anything to do in this block
     auto mark = [&](int k) {
         if (rec) rec->mark(k, s);
     };
@@ -1130,85 +1164,97 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
         return pc;
     };
     const bool T = c->tiled;
-    auto fine_s1 = [&](int k) {
-        mark(K_FINE_S1);
-        const double *hk = k == 0 ? hN : hb(k - 1), *uk = k == 0 ? uN : ub(k - 1);
-        launch_fine_s1(m, st, hN, hNew, hk, uk, sc, pred(k), k, s, !T);
-        if (T) stage_tiled(c, 1, m.cb.fl[1], m.cb.end, StageArgs{hk, hk, uk, st.S, st.h1, 0, 0, 0, sc.c1f, sc.g, K_FINE_S1, k}, s);
-    };
     *px = PhaseX{-1, nullptr, -1, nullptr};
     const int nfine = c->have_fine ? 3 * M : 0;
+    if (ph > 3 + nfine) return false;
+    bool any = false;
+    auto cell_mark = [&](int k) {      // part 1 adds time to the sweep part 0 counted (kind + 64)
+        if (cells) {
+            mark(part == 0 ? k : k + 64);
+            any = true;
+        }
+    };
     if (ph == 0) {
-        if (c->cfg.slow) {
+        if (part == 0 && c->cfg.slow) {
             mark(K_SLOW_PRE);
             launch_slow_pre(m, st, hN, uN, s);
             mark(K_SLOW_EDGE);
             launch_slow_edge(m, st, hN, sc, s);
+            any = true;
         }
-        mark(K_COARSE_S1);
-        if (c->tiled) stage_tiled(c, 1, 0, m.cb.fl[5], StageArgs{hN, hN, uN, st.S, st.h1, 0, 0, 0, sc.c1, sc.g, K_COARSE_S1, -1}, s);
-        else launch_coarse_s1(m, st, hN, uN, sc, s);
+        cell_mark(K_COARSE_S1);
+        if (T) stage_tiled(c, 1, B, B.begin, B.fl[5], StageArgs{hN, hN, uN, st.S, st.h1, 0, 0, 0, sc.c1, sc.g, K_COARSE_S1, -1}, s);
+        else launch_coarse_s1(m, st, hN, uN, sc, s, B);
         *px = PhaseX{X_C1, st.h1, -1, nullptr};
     } else if (ph == 1) {
-        mark(K_COARSE_S2);
-        if (c->tiled)
-            stage_tiled(c, 2, 0, m.cb.fl[3],
+        cell_mark(K_COARSE_S2);
+        if (T)
+            stage_tiled(c, 2, B, B.begin, B.fl[3],
                         StageArgs{hN, st.h1, uN, st.S, st.h2, sc.c1, sc.b1, sc.omb1, sc.c2, sc.g, K_COARSE_S2, -1}, s);
-        else launch_coarse_s2(m, st, hN, uN, sc, s);
+        else launch_coarse_s2(m, st, hN, uN, sc, s, B);
         *px = PhaseX{X_C1, st.h2, -1, nullptr};
     } else if (ph == 2) {
-        mark(K_COARSE_S3);
-        if (c->tiled)
-            stage_tiled(c, 3, 0, m.cb.fl[1],
+        cell_mark(K_COARSE_S3);
+        if (T)
+            stage_tiled(c, 3, B, B.begin, B.fl[1],
                         StageArgs{hN, st.h2, uN, st.S, hNew, sc.c2, sc.b2, sc.omb2, sc.c3, sc.g, K_COARSE_S3, -1}, s);
-        else launch_coarse_s3(m, st, hN, uN, hNew, sc, s);
+        else launch_coarse_s3(m, st, hN, uN, hNew, sc, s, B);
         *px = PhaseX{X_C1, hNew, -1, nullptr};
     } else if (ph - 3 < nfine) {
         const int q = ph - 3, k = q / 3, stg = q % 3;
+        const double *hk = k == 0 ? hN : hb(k - 1), *uk = k == 0 ? uN : ub(k - 1);
         if (stg == 0) {
-            if (k == 0) {
-                mark(K_COARSE_VEL);
-                launch_coarse_vel(m, st, hN, uN, hNew, uNew, sc, s);
-            } else {
-                mark(K_FINE_VEL);
-                launch_fine_vel(m, st, hN, hNew, k - 1 == 0 ? hN : hb(k - 2), hb(k - 1), k - 1 == 0 ? uN : ub(k - 2),
-                                ub(k - 1), sc, pred(k - 1), k - 1, s);
+            if (part == 0) {
+                if (k == 0) {
+                    mark(K_COARSE_VEL);
+                    launch_coarse_vel(m, st, hN, uN, hNew, uNew, sc, s);
+                } else {
+                    mark(K_FINE_VEL);
+                    launch_fine_vel(m, st, hN, hNew, k - 1 == 0 ? hN : hb(k - 2), hb(k - 1),
+                                    k - 1 == 0 ? uN : ub(k - 2), ub(k - 1), sc, pred(k - 1), k - 1, s);
+                }
+                any = true;
             }
-            fine_s1(k);
+            cell_mark(K_FINE_S1);
+            launch_fine_s1(m, st, hN, hNew, hk, uk, sc, pred(k), k, s, B, !T);
+            if (T) stage_tiled(c, 1, B, B.fl[1], B.end, StageArgs{hk, hk, uk, st.S, st.h1, 0, 0, 0, sc.c1f, sc.g, K_FINE_S1, k}, s);
             *px = PhaseX{X_C1, st.h1, -1, nullptr};
         } else if (stg == 1) {
-            mark(K_FINE_S2);
-            const double *hk = k == 0 ? hN : hb(k - 1), *uk = k == 0 ? uN : ub(k - 1);
-            launch_fine_s2(m, st, hN, hNew, hk, uk, sc, pred(k), k, s, !T);
+            cell_mark(K_FINE_S2);
+            launch_fine_s2(m, st, hN, hNew, hk, uk, sc, pred(k), k, s, B, !T);
             if (T)
-                stage_tiled(c, 2, m.cb.fl[1], m.cb.end,
+                stage_tiled(c, 2, B, B.fl[1], B.end,
                             StageArgs{hk, st.h1, uk, st.S, st.h2, sc.c1f, sc.b1, sc.omb1, sc.c2f, sc.g, K_FINE_S2, k}, s);
             *px = PhaseX{X_C1, st.h2, -1, nullptr};
         } else {
-            mark(K_FINE_S3);
-            const double *hk = k == 0 ? hN : hb(k - 1), *uk = k == 0 ? uN : ub(k - 1);
-            launch_fine_s3(m, st, hN, uN, hNew, hk, uk, hb(k), sc, pred(k), k, s, !T);
+            cell_mark(K_FINE_S3);
+            launch_fine_s3(m, st, hN, uN, hNew, hk, uk, hb(k), sc, pred(k), k, s, B, !T);
             if (T)
-                stage_tiled(c, 3, m.cb.fl[1], m.cb.end,
+                stage_tiled(c, 3, B, B.fl[1], B.end,
                             StageArgs{hk, st.h2, uk, st.S, hb(k), sc.c2f, sc.b2, sc.omb2, sc.c3f, sc.g, K_FINE_S3, k}, s);
             *px = PhaseX{X_C1, hb(k), -1, nullptr};
         }
-    } else if (ph == 3 + nfine) {
+    } else {                                     // ph == 3 + nfine: last velocity sweep, correction
         if (c->have_fine) {
-            mark(K_FINE_VEL);
-            launch_fine_vel(m, st, hN, hNew, M - 1 == 0 ? hN : hb(M - 2), hb(M - 1), M - 1 == 0 ? uN : ub(M - 2),
-                            ub(M - 1), sc, pred(M - 1), M - 1, s);
-            mark(K_CORRECT);
-            launch_correct(m, st, hN, uN, hNew, uNew, sc, s);
-        } else {
+            if (part == 0) {
+                mark(K_FINE_VEL);
+                launch_fine_vel(m, st, hN, hNew, M - 1 == 0 ? hN : hb(M - 2), hb(M - 1), M - 1 == 0 ? uN : ub(M - 2),
+                                ub(M - 1), sc, pred(M - 1), M - 1, s);
+                any = true;
+            }
+            if (cells || part == 0) {
+                mark(part == 0 ? K_CORRECT : K_CORRECT + 64);
+                any = true;
+            }
+            launch_correct(m, st, hN, uN, hNew, uNew, sc, s, B, part == 0);
+        } else if (part == 0) {
             mark(K_COARSE_VEL);
             launch_coarse_vel(m, st, hN, uN, hNew, uNew, sc, s);
+            any = true;
         }
         *px = PhaseX{X_C2, hNew, X_E, uNew};
-    } else {
-        return false;
     }
-    mark(-1);
+    if (any) mark(-1);
     return true;
 }
 
@@ -1249,14 +1295,30 @@ int allgather_nccl(fblts_ctx *c, const double *send6, double *recv) {
     return FBLTS_OK;
 }
 
-// One coarse step on one rank: every phase, with NCCL exchanges when nranks > 1.
+// One coarse step on one rank: every phase; with several ranks each stage's halo exchange runs on
+// the communication stream, forked after the phase's boundary-block kernel and joined before the
+// next phase, so it overlaps the interior-block kernel (the end-of-step exchange of rings 1-2 and
+// of the remote-owned edges needs the interior values and runs after it).
 int enqueue_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
-    PhaseX px;
-    for (int ph = 0; enqueue_phase(c, par, ph, s, rec, &px); ++ph) {
-        if (c->cfg.nranks == 1) continue;
-        int rc = exchange_nccl(c, px.x, px.a, s);
-        if (!rc && px.x2 >= 0) rc = exchange_nccl(c, px.x2, px.a2, s);
-        if (rc) return rc;
+    const bool multi = c->cfg.nranks > 1;
+    PhaseX px, px1;
+    for (int ph = 0; enqueue_phase(c, par, ph, s, rec, &px, 0); ++ph) {
+        const bool overlap = multi && px.x >= 0 && px.x2 < 0;
+        if (overlap) {
+            CUDA_TRY(c, cudaEventRecord(c->evFork, s));
+            CUDA_TRY(c, cudaStreamWaitEvent(c->comm, c->evFork, 0));
+            const int rc = exchange_nccl(c, px.x, px.a, c->comm);
+            if (rc) return rc;
+            CUDA_TRY(c, cudaEventRecord(c->evJoin, c->comm));
+        }
+        enqueue_phase(c, par, ph, s, rec, &px1, 1);
+        if (overlap) {
+            CUDA_TRY(c, cudaStreamWaitEvent(s, c->evJoin, 0));
+        } else if (multi) {
+            int rc = exchange_nccl(c, px.x, px.a, s);
+            if (!rc && px.x2 >= 0) rc = exchange_nccl(c, px.x2, px.a2, s);
+            if (rc) return rc;
+        }
     }
     return FBLTS_OK;
 }
@@ -1354,11 +1416,16 @@ int fblts_step_group(fblts_ctx **cs, int32_t n, int32_t n_coarse) {
     }
     cudaStream_t s = cs[0]->stream;
     for (int it = 0; it < n_coarse; ++it) {
-        std::vector<PhaseX> px(n);
+        std::vector<PhaseX> px(n), px1(n);
         for (int ph = 0;; ++ph) {
             bool any = false;
-            for (int r = 0; r < n; ++r) any = enqueue_phase(cs[r], cs[r]->parity, ph, s, nullptr, &px[r]) || any;
+            for (int r = 0; r < n; ++r) any = enqueue_phase(cs[r], cs[r]->parity, ph, s, nullptr, &px[r], 0) || any;
             if (!any) break;
+            // stage exchanges depend on the boundary blocks only (as in the overlapped NCCL path);
+            // the end-of-step exchange follows the interior blocks
+            const bool stage_x = px[0].x2 < 0;
+            if (!stage_x)
+                for (int r = 0; r < n; ++r) enqueue_phase(cs[r], cs[r]->parity, ph, s, nullptr, &px1[r], 1);
             for (int pass = 0; pass < 2; ++pass) {
                 for (int r = 0; r < n; ++r) {
                     const int x = pass == 0 ? px[r].x : px[r].x2;
@@ -1383,6 +1450,8 @@ int fblts_step_group(fblts_ctx **cs, int32_t n, int32_t n_coarse) {
                     if (x >= 0) unpack(cs[r], x, pass == 0 ? px[r].a : px[r].a2, s);
                 }
             }
+            if (stage_x)
+                for (int r = 0; r < n; ++r) enqueue_phase(cs[r], cs[r]->parity, ph, s, nullptr, &px1[r], 1);
         }
         for (int r = 0; r < n; ++r) {
             cs[r]->parity ^= 1;
@@ -1477,8 +1546,8 @@ int fblts_profile(fblts_ctx *c, int32_t n, double *ms, int64_t *launches) {
             float t = 0.f;
             cudaEventElapsedTime(&t, rec.ev[j], rec.ev[j + 1]);
             if (rec.kind[j] >= 0) {
-                ms[rec.kind[j]] += t;
-                launches[rec.kind[j]] += 1;
+                ms[rec.kind[j] & 63] += t;
+                if (rec.kind[j] < 64) launches[rec.kind[j]] += 1;
             }
         }
         for (auto e : rec.ev) cudaEventDestroy(e);
@@ -1493,6 +1562,9 @@ void fblts_destroy(fblts_ctx *c) {
     for (auto &e : c->exec)
         if (e) cudaGraphExecDestroy(e);
     if (c->cap) cudaStreamDestroy(c->cap);
+    if (c->comm) cudaStreamDestroy(c->comm);
+    if (c->evFork) cudaEventDestroy(c->evFork);
+    if (c->evJoin) cudaEventDestroy(c->evJoin);
     nccl_destroy(c);
     delete c;
 }

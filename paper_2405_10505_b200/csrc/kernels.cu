@@ -45,10 +45,10 @@ static_assert(NTHR >= TILE, "one thread per tile cell in the cell phase");
 
 static inline unsigned nblocks(long n) { return (unsigned)((n + TPB - 1) / TPB); }
 
-// cell class: 2 = F, 1 = IF-1, 0 = other coarse (IF-2 or int); owned block [0, nOwnC) and halo
-// block [nOwnC, nC) are each region-major
+// cell class: 2 = F, 1 = IF-1, 0 = other coarse (IF-2 or int); the boundary [0, nB), interior
+// [nB, nOwnC) and halo [nOwnC, nC) blocks are each region-major
 __device__ __forceinline__ int ccls(const DevMesh &m, int x) {
-    const Bounds &b = x < m.nOwnC ? m.cb : m.cbh;
+    const Bounds &b = x < m.nB ? m.cb : (x < m.nOwnC ? m.cbI : m.cbh);
     return x >= b.f ? 2 : (x >= b.if1 ? 1 : 0);
 }
 // edge class: 3 = F_E, 2 = IF-1_E, 1 = IF-2_E, 0 = int_E
@@ -100,52 +100,56 @@ __device__ __forceinline__ void load_row(const DevMesh &m, int i, int2 (&r)[G]) 
 // One launch, three index spaces: vertices (q_v), cells (K_i), edges (F_e).
 // q_v = (zeta_v + f_v) / h_v,  zeta_v = (sum t d u)/A_v,  h_v = (sum kite h)/A_v
 // K_i = (sum 0.25 l d u u) / A_i   (Q18);   F_e = (0.5 (h_c0 + h_c1)) u_e   (Q1)
+// The three index spaces are interleaved group by group: CTA 3g + r handles role r (0 vertices,
+// 1 cells, 2 edges) of group g, i.e. the g-th of nG equal slices of each (vertices and edges are
+// numbered by owner cell, so slice g of every space covers the same part of the mesh) -- u, d_e and
+// h are then read from DRAM about once and re-read from L2 by the other two roles.
 template <int G>
 __global__ void __launch_bounds__(TPB) k_slow_pre(DevMesh m, const double *__restrict__ h,
                                                   const double *__restrict__ u, double *__restrict__ q,
-                                                  double *__restrict__ K, double *__restrict__ F,
-                                                  unsigned nbV, unsigned nbC) {
-    const unsigned b = blockIdx.x;
-    if (b < nbV) {
-        const int v = b * TPB + threadIdx.x;
-        if (v >= m.nV) return;
-        double circ = 0.0;
+                                                  double *__restrict__ K, double *__restrict__ F, int nG) {
+    const int g = blockIdx.x / 3, role = blockIdx.x % 3;
+    const int n = role == 0 ? m.nV : (role == 1 ? m.nC : m.nE);
+    const int lo = (int)((long long)n * g / nG), hi = (int)((long long)n * (g + 1) / nG);
+    for (int x = lo + threadIdx.x; x < hi; x += TPB) {
+        if (role == 0) {
+            const int v = x;
+            double circ = 0.0;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            bool pos;
-            const int e = decode(m.eov[k * m.strideV + v], pos);
-            const double t = m.dc[e] * u[e];
-            circ = circ + (pos ? t : -t);
-        }
-        const double A = m.areaTri[v];
-        const double zeta = circ / A;
-        double hv = 0.0;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) hv = hv + m.kite[k * m.strideV + v] * h[m.cov[k * m.strideV + v]];
-        hv = hv / A;
-        q[v] = (zeta + m.fV[v]) / hv;
-    } else if (b < nbV + nbC) {
-        const int i = (b - nbV) * TPB + threadIdx.x;
-        if (i >= m.nC) return;
-        int2 r[G];
-        load_row<G>(m, i, r);
-        const int n = m.nEoC[i];
-        double acc = 0.0;
-#pragma unroll
-        for (int j = 0; j < G; ++j) {
-            if (j < n) {
+            for (int k = 0; k < 3; ++k) {
                 bool pos;
-                const int e = decode(r[j].x, pos);
-                const double ue = u[e];
-                acc = acc + 0.25 * m.dv[e] * m.dc[e] * ue * ue;
+                const int e = decode(m.eov[k * m.strideV + v], pos);
+                const double t = m.dc[e] * u[e];
+                circ = circ + (pos ? t : -t);
             }
+            const double A = m.areaTri[v];
+            const double zeta = circ / A;
+            double hv = 0.0;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) hv = hv + m.kite[k * m.strideV + v] * h[m.cov[k * m.strideV + v]];
+            hv = hv / A;
+            q[v] = (zeta + m.fV[v]) / hv;
+        } else if (role == 1) {
+            const int i = x;
+            int2 r[G];
+            load_row<G>(m, i, r);
+            const int ne = m.nEoC[i];
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+                if (j < ne) {
+                    bool pos;
+                    const int e = decode(r[j].x, pos);
+                    const double ue = u[e];
+                    acc = acc + 0.25 * m.dv[e] * m.dc[e] * ue * ue;
+                }
+            }
+            K[i] = acc / m.areaCell[i];
+        } else {
+            const int e = x;
+            const int2 c = m.coe[e];
+            F[e] = (0.5 * (h[c.x] + h[c.y])) * u[e];
         }
-        K[i] = acc / m.areaCell[i];
-    } else {
-        const int e = (b - nbV - nbC) * TPB + threadIdx.x;
-        if (e >= m.nE) return;
-        const int2 c = m.coe[e];
-        F[e] = (0.5 * (h[c.x] + h[c.y])) * u[e];
     }
 }
 
@@ -189,8 +193,8 @@ __global__ void __launch_bounds__(TPB, FBLTS_MINB) k_coarse_stage(DevMesh m, con
                                                       const double *__restrict__ hprev,
                                                       const double *__restrict__ uN,
                                                       const double *__restrict__ S, double *__restrict__ out,
-                                                      StepConst sc, int end, DevError *err) {
-    const int i = blockIdx.x * TPB + threadIdx.x;
+                                                      StepConst sc, int begin, int end, DevError *err) {
+    const int i = begin + blockIdx.x * TPB + threadIdx.x;
     if (i >= end) return;
     int2 r[G];
     load_row<G>(m, i, r);
@@ -655,7 +659,7 @@ template <int G, bool BAND>
 __global__ void __launch_bounds__(TPB, BAND ? 1 : FBLTS_MINB) k_fine_s3(DevMesh m, FineArrays a, const double *__restrict__ uN,
                                                  const double *__restrict__ uk, const double *__restrict__ S,
                                                  double *__restrict__ hnext, double *__restrict__ accH,
-                                                 StepConst sc, PredConst p, int k, int begin, int end,
+                                                 StepConst sc, PredConst p, int k, int begin, int fstart, int end,
                                                  DevError *err) {
     const int i = begin + blockIdx.x * TPB + threadIdx.x;
     if (i >= end) return;
@@ -699,14 +703,13 @@ __global__ void __launch_bounds__(TPB, BAND ? 1 : FBLTS_MINB) k_fine_s3(DevMesh 
         }
     }
     const double psi = -acc / m.areaCell[i];
-    if (!BAND || i >= m.cb.f) {
+    if (!BAND || i >= fstart) {
         const double v = a.hk[i] + sc.c3f * psi;
         hnext[i] = v;
         if (!(v > 0.0)) report(err, K_FINE_S3, k, i, v);
     } else {
-        const int ai = i - m.cb.if2;
-        const double prev = k == 0 ? 0.0 : accH[ai];
-        accH[ai] = prev + psi;
+        const double prev = k == 0 ? 0.0 : accH[i];
+        accH[i] = prev + psi;
     }
 }
 
@@ -737,12 +740,12 @@ __global__ void __launch_bounds__(TPB) k_fine_vel(DevMesh m, FineArrays a, const
 __global__ void __launch_bounds__(TPB) k_correct(DevMesh m, const double *__restrict__ hN,
                                                  const double *__restrict__ uN, const double *__restrict__ accH,
                                                  const double *__restrict__ accU, double *__restrict__ hNew,
-                                                 double *__restrict__ uNew, StepConst sc, unsigned nbC,
+                                                 double *__restrict__ uNew, StepConst sc, int c0, int c1, unsigned nbC,
                                                  DevError *err) {
     if (blockIdx.x < nbC) {
-        const int i = m.cb.if2 + blockIdx.x * TPB + threadIdx.x;
-        if (i >= m.cb.f) return;
-        const double v = hN[i] + sc.c3f * accH[i - m.cb.if2];
+        const int i = c0 + blockIdx.x * TPB + threadIdx.x;
+        if (i >= c1) return;
+        const double v = hN[i] + sc.c3f * accH[i];
         hNew[i] = v;
         if (!(v > 0.0)) report(err, K_CORRECT, -1, i, v);
     } else {
@@ -805,7 +808,7 @@ __global__ void __launch_bounds__(TPB) k_diag_partial(DevMesh m, const double *_
     const int T = gridDim.x * TPB;
     DD mass{0.0, 0.0}, gam{0.0, 0.0};
     double hmin = (double)INFINITY, numax = 0.0;
-    for (int i = tid; i < m.cb.end; i += T) {
+    for (int i = tid; i < m.nOwnC; i += T) {
         dd_add(mass, m.areaCell[i] * h[i]);
         hmin = fmin(hmin, h[i]);
     }
@@ -934,8 +937,8 @@ void launch_stage_tiled(const DevMesh &m, int stage, int tile0, int tile1, int h
 }
 
 void launch_slow_pre(const DevMesh &m, const DevState &st, const double *h, const double *u, cudaStream_t s) {
-    const unsigned nbV = nblocks(m.nV), nbC = nblocks(m.nC), nbE = nblocks(m.nE);
-    FBLTS_DISPATCH_G(m.ecS, k_slow_pre<G><<<nbV + nbC + nbE, TPB, 0, s>>>(m, h, u, st.q, st.K, st.F, nbV, nbC));
+    const int nG = (int)nblocks(std::max(1, m.nC));             // one group per 256 cells
+    FBLTS_DISPATCH_G(m.ecS, k_slow_pre<G><<<3u * nG, TPB, 0, s>>>(m, h, u, st.q, st.K, st.F, nG));
 }
 void launch_slow_edge(const DevMesh &m, const DevState &st, const double *h, const StepConst &sc, cudaStream_t s) {
     if (m.nOwnE <= 0) return;
@@ -947,25 +950,25 @@ void launch_slow_edge(const DevMesh &m, const DevState &st, const double *h, con
         k_slow_edge<30><<<nblocks(m.nOwnE), TPB, 0, s>>>(m, h, st.q, st.K, st.F, st.S, sc.rho0);
 }
 void launch_coarse_s1(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
-                      const StepConst &sc, cudaStream_t s) {
-    const int end = m.cb.fl[5];
-    if (end > 0)
-        FBLTS_DISPATCH_G(m.ecS, k_coarse_stage<G, 1><<<nblocks(end), TPB, 0, s>>>(m, hN, hN, uN, st.S, st.h1, sc,
-                                                                                   end, st.err));
+                      const StepConst &sc, cudaStream_t s, const Bounds &b) {
+    const int beg = b.begin, end = b.fl[5];
+    if (end > beg)
+        FBLTS_DISPATCH_G(m.ecS, k_coarse_stage<G, 1><<<nblocks(end - beg), TPB, 0, s>>>(m, hN, hN, uN, st.S, st.h1,
+                                                                                         sc, beg, end, st.err));
 }
 void launch_coarse_s2(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
-                      const StepConst &sc, cudaStream_t s) {
-    const int end = m.cb.fl[3];
-    if (end > 0)
-        FBLTS_DISPATCH_G(m.ecS, k_coarse_stage<G, 2><<<nblocks(end), TPB, 0, s>>>(m, hN, st.h1, uN, st.S, st.h2, sc,
-                                                                                   end, st.err));
+                      const StepConst &sc, cudaStream_t s, const Bounds &b) {
+    const int beg = b.begin, end = b.fl[3];
+    if (end > beg)
+        FBLTS_DISPATCH_G(m.ecS, k_coarse_stage<G, 2><<<nblocks(end - beg), TPB, 0, s>>>(m, hN, st.h1, uN, st.S, st.h2,
+                                                                                         sc, beg, end, st.err));
 }
 void launch_coarse_s3(const DevMesh &m, const DevState &st, const double *hN, const double *uN, double *hNew,
-                      const StepConst &sc, cudaStream_t s) {
-    const int end = m.cb.fl[1];
-    if (end > 0)
-        FBLTS_DISPATCH_G(m.ecS, k_coarse_stage<G, 3><<<nblocks(end), TPB, 0, s>>>(m, hN, st.h2, uN, st.S, hNew, sc,
-                                                                                   end, st.err));
+                      const StepConst &sc, cudaStream_t s, const Bounds &b) {
+    const int beg = b.begin, end = b.fl[1];
+    if (end > beg)
+        FBLTS_DISPATCH_G(m.ecS, k_coarse_stage<G, 3><<<nblocks(end - beg), TPB, 0, s>>>(m, hN, st.h2, uN, st.S, hNew,
+                                                                                         sc, beg, end, st.err));
 }
 void launch_coarse_vel(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
                        const double *hNew, double *uNew, const StepConst &sc, cudaStream_t s) {
@@ -983,18 +986,20 @@ static FineArrays fine_arrays(const DevState &st, const double *hN, const double
 }
 // Fine kernels: BAND instance over [b0, b1) (needs the region views), DEEP over [b1, end).
 void launch_fine_s1(const DevMesh &m, const DevState &st, const double *hN, const double *hNew, const double *hk,
-                    const double *uk, const StepConst &sc, const PredConst &pc, int k, cudaStream_t s, bool deep) {
+                    const double *uk, const StepConst &sc, const PredConst &pc, int k, cudaStream_t s,
+                    const Bounds &b, bool deep) {
     const FineArrays a = fine_arrays(st, hN, hNew, hk);
-    const int b0 = m.cb.f, b1 = m.cb.fl[1], end = m.cb.end;
+    const int b0 = b.f, b1 = b.fl[1], end = b.end;
     FBLTS_DISPATCH_G(m.ecS, {
         if (b1 > b0) k_fine_s1<G, true><<<nblocks(b1 - b0), TPB, 0, s>>>(m, a, uk, st.h1, sc, pc, k, b0, b1, st.err);
         if (deep && end > b1) k_fine_s1<G, false><<<nblocks(end - b1), TPB, 0, s>>>(m, a, uk, st.h1, sc, pc, k, b1, end, st.err);
     });
 }
 void launch_fine_s2(const DevMesh &m, const DevState &st, const double *hN, const double *hNew, const double *hk,
-                    const double *uk, const StepConst &sc, const PredConst &pc, int k, cudaStream_t s, bool deep) {
+                    const double *uk, const StepConst &sc, const PredConst &pc, int k, cudaStream_t s,
+                    const Bounds &b, bool deep) {
     const FineArrays a = fine_arrays(st, hN, hNew, hk);
-    const int b0 = m.cb.f, b1 = m.cb.fl[1], end = m.cb.end;
+    const int b0 = b.f, b1 = b.fl[1], end = b.end;
     FBLTS_DISPATCH_G(m.ecS, {
         if (b1 > b0)
             k_fine_s2<G, true><<<nblocks(b1 - b0), TPB, 0, s>>>(m, a, uk, st.S, st.h2, sc, pc, k, b0, b1, st.err);
@@ -1004,16 +1009,16 @@ void launch_fine_s2(const DevMesh &m, const DevState &st, const double *hN, cons
 }
 void launch_fine_s3(const DevMesh &m, const DevState &st, const double *hN, const double *uN, const double *hNew,
                     const double *hk, const double *uk, double *hnext, const StepConst &sc, const PredConst &pc,
-                    int k, cudaStream_t s, bool deep) {
+                    int k, cudaStream_t s, const Bounds &b, bool deep) {
     const FineArrays a = fine_arrays(st, hN, hNew, hk);
-    const int b0 = m.cb.if2, b1 = m.cb.fl[1], end = m.cb.end;
+    const int b0 = b.if2, b1 = b.fl[1], end = b.end;
     FBLTS_DISPATCH_G(m.ecS, {
         if (b1 > b0)
             k_fine_s3<G, true><<<nblocks(b1 - b0), TPB, 0, s>>>(m, a, uN, uk, st.S, hnext, st.accH, sc, pc, k, b0,
-                                                                 b1, st.err);
+                                                                 b.f, b1, st.err);
         if (deep && end > b1)
             k_fine_s3<G, false><<<nblocks(end - b1), TPB, 0, s>>>(m, a, uN, uk, st.S, hnext, st.accH, sc, pc, k, b1,
-                                                                   end, st.err);
+                                                                   b1, end, st.err);
     });
 }
 void launch_fine_vel(const DevMesh &m, const DevState &st, const double *hN, const double *hNew, const double *hk,
@@ -1027,9 +1032,10 @@ void launch_fine_vel(const DevMesh &m, const DevState &st, const double *hN, con
         k_fine_vel<false><<<nblocks(end - b1), TPB, 0, s>>>(m, a, hnext, uk, st.S, unext, st.accU, sc, pc, k, b1, end);
 }
 void launch_correct(const DevMesh &m, const DevState &st, const double *hN, const double *uN, double *hNew,
-                    double *uNew, const StepConst &sc, cudaStream_t s) {
-    const unsigned nbC = nblocks(m.cb.f - m.cb.if2), nbE = nblocks(m.eb.f - m.eb.if2);
-    if (nbC + nbE > 0) k_correct<<<nbC + nbE, TPB, 0, s>>>(m, hN, uN, st.accH, st.accU, hNew, uNew, sc, nbC, st.err);
+                    double *uNew, const StepConst &sc, cudaStream_t s, const Bounds &b, bool edges) {
+    const unsigned nbC = nblocks(b.f - b.if2), nbE = edges ? nblocks(m.eb.f - m.eb.if2) : 0u;
+    if (nbC + nbE > 0)
+        k_correct<<<nbC + nbE, TPB, 0, s>>>(m, hN, uN, st.accH, st.accU, hNew, uNew, sc, b.if2, b.f, nbC, st.err);
 }
 void launch_permute_in(const int32_t *old, const double *src, double *dst, int n, cudaStream_t s) {
     if (n > 0) k_permute_in<<<nblocks(n), TPB, 0, s>>>(old, src, dst, n);
