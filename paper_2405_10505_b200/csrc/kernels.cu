@@ -100,56 +100,52 @@ __device__ __forceinline__ void load_row(const DevMesh &m, int i, int2 (&r)[G]) 
 // One launch, three index spaces: vertices (q_v), cells (K_i), edges (F_e).
 // q_v = (zeta_v + f_v) / h_v,  zeta_v = (sum t d u)/A_v,  h_v = (sum kite h)/A_v
 // K_i = (sum 0.25 l d u u) / A_i   (Q18);   F_e = (0.5 (h_c0 + h_c1)) u_e   (Q1)
-// The three index spaces are interleaved group by group: CTA 3g + r handles role r (0 vertices,
-// 1 cells, 2 edges) of group g, i.e. the g-th of nG equal slices of each (vertices and edges are
-// numbered by owner cell, so slice g of every space covers the same part of the mesh) -- u, d_e and
-// h are then read from DRAM about once and re-read from L2 by the other two roles.
 template <int G>
 __global__ void __launch_bounds__(TPB) k_slow_pre(DevMesh m, const double *__restrict__ h,
                                                   const double *__restrict__ u, double *__restrict__ q,
-                                                  double *__restrict__ K, double *__restrict__ F, int nG) {
-    const int g = blockIdx.x / 3, role = blockIdx.x % 3;
-    const int n = role == 0 ? m.nV : (role == 1 ? m.nC : m.nE);
-    const int lo = (int)((long long)n * g / nG), hi = (int)((long long)n * (g + 1) / nG);
-    for (int x = lo + threadIdx.x; x < hi; x += TPB) {
-        if (role == 0) {
-            const int v = x;
-            double circ = 0.0;
+                                                  double *__restrict__ K, double *__restrict__ F,
+                                                  unsigned nbV, unsigned nbC) {
+    const unsigned b = blockIdx.x;
+    if (b < nbV) {
+        const int v = b * TPB + threadIdx.x;
+        if (v >= m.nV) return;
+        double circ = 0.0;
 #pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                bool pos;
-                const int e = decode(m.eov[k * m.strideV + v], pos);
-                const double t = m.dc[e] * u[e];
-                circ = circ + (pos ? t : -t);
-            }
-            const double A = m.areaTri[v];
-            const double zeta = circ / A;
-            double hv = 0.0;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) hv = hv + m.kite[k * m.strideV + v] * h[m.cov[k * m.strideV + v]];
-            hv = hv / A;
-            q[v] = (zeta + m.fV[v]) / hv;
-        } else if (role == 1) {
-            const int i = x;
-            int2 r[G];
-            load_row<G>(m, i, r);
-            const int ne = m.nEoC[i];
-            double acc = 0.0;
-#pragma unroll
-            for (int j = 0; j < G; ++j) {
-                if (j < ne) {
-                    bool pos;
-                    const int e = decode(r[j].x, pos);
-                    const double ue = u[e];
-                    acc = acc + 0.25 * m.dv[e] * m.dc[e] * ue * ue;
-                }
-            }
-            K[i] = acc / m.areaCell[i];
-        } else {
-            const int e = x;
-            const int2 c = m.coe[e];
-            F[e] = (0.5 * (h[c.x] + h[c.y])) * u[e];
+        for (int k = 0; k < 3; ++k) {
+            bool pos;
+            const int e = decode(m.eov[k * m.strideV + v], pos);
+            const double t = m.dc[e] * u[e];
+            circ = circ + (pos ? t : -t);
         }
+        const double A = m.areaTri[v];
+        const double zeta = circ / A;
+        double hv = 0.0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) hv = hv + m.kite[k * m.strideV + v] * h[m.cov[k * m.strideV + v]];
+        hv = hv / A;
+        q[v] = (zeta + m.fV[v]) / hv;
+    } else if (b < nbV + nbC) {
+        const int i = (b - nbV) * TPB + threadIdx.x;
+        if (i >= m.nC) return;
+        int2 r[G];
+        load_row<G>(m, i, r);
+        const int n = m.nEoC[i];
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+            if (j < n) {
+                bool pos;
+                const int e = decode(r[j].x, pos);
+                const double ue = u[e];
+                acc = acc + 0.25 * m.dv[e] * m.dc[e] * ue * ue;
+            }
+        }
+        K[i] = acc / m.areaCell[i];
+    } else {
+        const int e = (b - nbV - nbC) * TPB + threadIdx.x;
+        if (e >= m.nE) return;
+        const int2 c = m.coe[e];
+        F[e] = (0.5 * (h[c.x] + h[c.y])) * u[e];
     }
 }
 
@@ -937,8 +933,8 @@ void launch_stage_tiled(const DevMesh &m, int stage, int tile0, int tile1, int h
 }
 
 void launch_slow_pre(const DevMesh &m, const DevState &st, const double *h, const double *u, cudaStream_t s) {
-    const int nG = (int)nblocks(std::max(1, m.nC));             // one group per 256 cells
-    FBLTS_DISPATCH_G(m.ecS, k_slow_pre<G><<<3u * nG, TPB, 0, s>>>(m, h, u, st.q, st.K, st.F, nG));
+    const unsigned nbV = nblocks(m.nV), nbC = nblocks(m.nC), nbE = nblocks(m.nE);
+    FBLTS_DISPATCH_G(m.ecS, k_slow_pre<G><<<nbV + nbC + nbE, TPB, 0, s>>>(m, h, u, st.q, st.K, st.F, nbV, nbC));
 }
 void launch_slow_edge(const DevMesh &m, const DevState &st, const double *h, const StepConst &sc, cudaStream_t s) {
     if (m.nOwnE <= 0) return;
