@@ -150,26 +150,37 @@ __global__ void __launch_bounds__(TPB) k_slow_pre(DevMesh m, const double *__res
 }
 
 // S_e = q_hat_e F_perp_e - (K_c1 - K_c0) / d_e + G_e   (Q2, Q5, Q19)
+#ifndef FBLTS_SLOW_CHUNK
+#define FBLTS_SLOW_CHUNK 5
+#endif
+#ifndef FBLTS_SLOW_MINB
+#define FBLTS_SLOW_MINB 6
+#endif
 template <int MAXE2>
-__global__ void __launch_bounds__(TPB) k_slow_edge(DevMesh m, const double *__restrict__ h,
+__global__ void __launch_bounds__(TPB, FBLTS_SLOW_MINB) k_slow_edge(DevMesh m, const double *__restrict__ h,
                                                    const double *__restrict__ q, const double *__restrict__ K,
                                                    const double *__restrict__ F, double *__restrict__ S,
                                                    double rho0) {
     const int e = blockIdx.x * TPB + threadIdx.x;
     if (e >= m.nOwnE) return;
     const int n = m.nEoE[e];
-    double w[MAXE2], f[MAXE2];
-#pragma unroll
-    for (int j = 0; j < MAXE2; ++j) {
-        if (j < n) {
-            w[j] = m.W[j * m.strideE + e];
-            f[j] = F[m.eoe[j * m.strideE + e]];
-        }
-    }
+    // F_perp = sum_j W_j F_eoe_j in slot order, gathered in chunks of CH slots (register budget)
+    constexpr int CH = FBLTS_SLOW_CHUNK < MAXE2 ? FBLTS_SLOW_CHUNK : MAXE2;
     double fp = 0.0;
 #pragma unroll
-    for (int j = 0; j < MAXE2; ++j)
-        if (j < n) fp = fp + w[j] * f[j];
+    for (int j0 = 0; j0 < MAXE2; j0 += CH) {
+        double w[CH], f[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+            if (j0 + j < n && j0 + j < MAXE2) {
+                w[j] = m.W[(j0 + j) * m.strideE + e];
+                f[j] = F[m.eoe[(j0 + j) * m.strideE + e]];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+            if (j0 + j < n && j0 + j < MAXE2) fp = fp + w[j] * f[j];
+    }
     const int2 v = m.voe[e];
     const int2 c = m.coe[e];
     const double qh = 0.5 * (q[v.x] + q[v.y]);
