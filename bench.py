@@ -61,10 +61,13 @@ def cpu_sample_case():
 
 
 # ------------------------------------------------------------------ byte model
-def byte_model(counts, maxE=6, maxE2=10):
-    """Algorithmic bytes per launch of each kernel kind (the method's arrays, each element once per
-    sweep; recomputable intermediates and padding not counted).  On a hex mesh the stage kernels
-    give SURVEY 8(d)'s 188 B/cell (s >= 2)."""
+def byte_model(counts, M, fused, maxE=6, maxE2=10):
+    """Algorithmic bytes PER STEP of each kernel kind (the method's arrays, each element once per
+    sweep; recomputable intermediates and padding not counted), summed over that kind's launches in
+    one coarse step.  On a hex mesh the stage sweeps give SURVEY 8(d)'s 188 B/cell (s >= 2).
+    `fused`: the deep fine velocity sweep of subcycle k-1 runs inside the deep stage-1 sweep of
+    subcycle k (kind fine_vel_s1, k = 1..M-1); fine_s1 then holds the band stage 1 (every k) and the
+    deep stage 1 of k = 0, fine_vel the band velocity sweeps and the last full one."""
     C, E = counts["owned_cells"], counts["owned_edges"]          # this rank's share
     V = counts["nVertices"] * C // max(1, counts["nCells"])
     cc, ec = counts["cells_by_region"], counts["edges_by_region"]
@@ -77,6 +80,8 @@ def byte_model(counts, maxE=6, maxE2=10):
     edge_s = 8 + 8 + 8 + 8                   # u_base, S, l_e, d_e
     vel_e = 8 + 8 + 8 + 8 + 8                # cellsOnEdge, u_base, S, d_e, write
     vel_c = 8 * 4                            # h3, h2, h_base, z_b
+    fs1 = lambda lo: cells(lo, 8) * (slotC + 8 + 8 + 8) + edges(lo, 8) * edge_s1
+    fvel = lambda lo: edges(lo, 8) * vel_e + cells(lo, 8) * vel_c
     b = {}
     b["slow_pre"] = V * (12 + 12 + 24 + 8 + 8) + C * (4 + 4 * maxE + 8 + 8) + E * (8 + 8 + 8 + 8)
     b["slow_edge"] = E * (4 + 4 * maxE2 + 8 * maxE2 + 8 + 8 + 8 + 8 + 8) + V * 8 + C * 8 + C * 8
@@ -84,11 +89,20 @@ def byte_model(counts, maxE=6, maxE2=10):
     b["coarse_s2"] = cells(0, 5) * cell_s + edges(0, 5) * edge_s
     b["coarse_s3"] = cells(0, 3) * cell_s + edges(0, 3) * edge_s
     b["coarse_vel"] = edges(0, 0) * vel_e + cells(0, 1) * vel_c
-    b["fine_s1"] = cells(3, 8) * (slotC + 8 + 8 + 8) + edges(3, 8) * edge_s1
-    b["fine_s2"] = cells(3, 8) * (slotC + 8 + 8 + 8 + 8 + 8 - 8) + edges(3, 8) * edge_s
-    b["fine_s3"] = cells(1, 8) * (slotC + 8 + 8 + 8 + 8 + 8 - 8) + edges(1, 8) * edge_s
-    b["fine_vel"] = edges(1, 8) * vel_e + cells(1, 8) * vel_c
+    b["fine_s2"] = M * (cells(3, 8) * (slotC + 8 + 8 + 8 + 8 + 8 - 8) + edges(3, 8) * edge_s)
+    b["fine_s3"] = M * (cells(1, 8) * (slotC + 8 + 8 + 8 + 8 + 8 - 8) + edges(1, 8) * edge_s)
     b["correct_if"] = cells(1, 2) * 24 + edges(1, 2) * 24
+    if fused:
+        band_s1 = fs1(3) - fs1(4)
+        band_vel = fvel(1) - fvel(4)
+        b["fine_s1"] = M * band_s1 + fs1(4)
+        b["fine_vel"] = (M - 1) * band_vel + fvel(1)
+        # deep vel(k-1) + s1(k): cells row, h^{n,k}, h2, h^{n,k-1}, z_b, A, write h1; edges u, S, l, d, write u
+        b["fine_vel_s1"] = (M - 1) * (cells(4, 8) * (slotC + 8 * 6) + edges(4, 8) * 40)
+    else:
+        b["fine_s1"] = M * fs1(3)
+        b["fine_vel"] = M * fvel(1)
+        b["fine_vel_s1"] = 0
     return b
 
 
@@ -269,19 +283,18 @@ def arm_native(args):
     # ---------------- instrumented replay: per-kernel device time (events on the same stream)
     n_prof = max(1, min(args.steps, 5))
     prof = s.profile(n_prof)
-    bytes_per_launch = {}
-    bm = byte_model(counts)
-    for k, (tms, n) in prof.items():
-        if n:
-            bytes_per_launch[k] = bm[k]
-    dom = max((k for k in prof if prof[k][1]), key=lambda k: prof[k][0])
-    dom_ms = prof[dom][0] / prof[dom][1]
+    fused = prof.get("fine_vel_s1", (0.0, 0))[1] > 0
+    bm = byte_model(counts, c.M, fused)                     # bytes per step per kind
+    t_step = {k: tms / n_prof for k, (tms, n) in prof.items() if n}
+    dom = max(t_step, key=lambda k: t_step[k])
+    launches_dom = prof[dom][1] / n_prof
+    dom_ms = t_step[dom] / launches_dom                     # average launch duration
     peak, peak_src = load_peaks()
-    achieved = bm[dom] / (dom_ms * 1e-3) / 1e9
+    achieved = bm[dom] / (t_step[dom] * 1e-3) / 1e9
     traffic = load_traffic().get(args.config, {}).get(dom)
     launches_per_step = s.counts()["kernels_per_step"]         # nodes of the captured step graph
-    step_bytes = sum(bm[k] * n for k, (_, n) in prof.items()) / n_prof
-    prof_total = sum(t for (t, _) in prof.values())
+    step_bytes = sum(bm[k] for k in t_step)
+    prof_total = sum(t_step.values())
 
     # ---------------- end to end through the public API with HOST buffers
     e2e = None
@@ -334,12 +347,12 @@ def arm_native(args):
                    f"{world} GPUs, dual-set SFC partition of one mesh, NCCL halo exchange per stage",
                    "setup_s": round(t_setup, 1)},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "bytes_per_launch": bm[dom],
-                     "launch_ms": dom_ms, "share_of_step": prof[dom][0] / prof_total, "peak_source": peak_src,
+                     "frac": achieved / peak, "traffic": traffic, "bytes_per_launch": bm[dom] / launches_dom,
+                     "launch_ms": dom_ms, "share_of_step": t_step[dom] / prof_total, "peak_source": peak_src,
                      "step_achieved": step_bytes / (ms_step * 1e-3) / 1e9,
                      "step_frac": step_bytes / (ms_step * 1e-3) / 1e9 / peak},
-        "kernels": {k: {"ms_per_launch": tms / n, "launches_per_step": n / n_prof,
-                        "GBps": bm[k] / (tms / n * 1e-3) / 1e9}
+        "kernels": {k: {"ms_per_launch": tms / n, "launches_per_step": n / n_prof, "ms_per_step": tms / n_prof,
+                        "GBps": bm[k] / (tms / n_prof * 1e-3) / 1e9}
                     for k, (tms, n) in prof.items() if n},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(round(launches_per_step * args.steps)),
         "clocks": clocks,

@@ -23,7 +23,7 @@ _lib = C.CDLL(LIB_PATH)
 FBLTS_OK = 0
 ERRORS = {-1: "INVALID_ARG", -2: "MESH", -3: "LABELS", -4: "STATE", -5: "CUDA", -6: "NCCL", -7: "POSITIVITY",
           -8: "ORDER"}
-NUM_KERNELS = 11
+NUM_KERNELS = 12
 
 _i32p = C.POINTER(C.c_int32)
 _f64p = C.POINTER(C.c_double)

@@ -21,7 +21,7 @@ namespace fblts {
 
 enum KernelKind {
     K_SLOW_PRE = 0, K_SLOW_EDGE, K_COARSE_S1, K_COARSE_S2, K_COARSE_S3, K_COARSE_VEL,
-    K_FINE_S1, K_FINE_S2, K_FINE_S3, K_FINE_VEL, K_CORRECT, K_NUM
+    K_FINE_S1, K_FINE_S2, K_FINE_S3, K_FINE_VEL, K_CORRECT, K_FINE_VS1, K_NUM
 };
 
 // Region boundaries of one region-major block: [begin,if2) int, [if2,if1) IF-2,
@@ -145,11 +145,17 @@ struct DevState {
 //   u_bar_e = ubase_e                                   (STAGE 1)
 //   u_bar_e = ubase_e + cu (Phi^fast_e(bb hprev + omb hbase) + S_e)   (STAGE 2, 3)
 // which is the coarse stage s (hbase = h^n) and the fine stage s inside F (hbase = h^{n,k}).
+// STAGE 4 fuses the deep fine velocity stage 3 of subcycle k-1 into stage 1 of subcycle k:
+//   u^{n,k}_e = u^{n,k-1}_e + cu (Phi^fast_e(h***) + S_e),  h*** = bb h^{n,k} + omb h2 + bb h^{n,k-1}
+//   (written to unew on the tile's owned edge run), then out_i = h^{n,k}_i + ch Psi_i(u^{n,k}, h^{n,k})
+// with hprev = h^{n,k}, hbase = h^{n,k-1}, h2 = stage-2 thickness of subcycle k-1, ubase = u^{n,k-1}.
 struct StageArgs {
     const double *hbase, *hprev, *ubase, *S;
     double *out;
     double cu, bb, omb, ch, g;
     int32_t kind, k;
+    const double *h2 = nullptr;   // STAGE 4
+    double *unew = nullptr;       // STAGE 4
 };
 void launch_stage_tiled(const DevMesh &m, int stage, int tile0, int tile1, int hmax, int emax, int nsm,
                         const StageArgs &a, DevError *err, cudaStream_t s);
@@ -180,7 +186,7 @@ void launch_fine_s3(const DevMesh &m, const DevState &st, const double *hN, cons
                     bool deep = true);
 void launch_fine_vel(const DevMesh &m, const DevState &st, const double *hN, const double *hNew,
                      const double *hk, const double *hnext, const double *uk, double *unext,
-                     const StepConst &sc, const PredConst &pc, int k, cudaStream_t s);
+                     const StepConst &sc, const PredConst &pc, int k, cudaStream_t s, bool deep = true);
 void launch_correct(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
                     double *hNew, double *uNew, const StepConst &sc, cudaStream_t s, const Bounds &b, bool edges);
 void launch_permute_in(const int32_t *old_of_new, const double *src, double *dst, int n, cudaStream_t s);

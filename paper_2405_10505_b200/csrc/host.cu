@@ -23,7 +23,7 @@ using namespace fblts;
 namespace {
 
 const char *kKernelNames[K_NUM] = {"slow_pre",  "slow_edge", "coarse_s1", "coarse_s2", "coarse_s3", "coarse_vel",
-                                   "fine_s1",   "fine_s2",   "fine_s3",   "fine_vel",  "correct_if"};
+                                   "fine_s1",   "fine_s2",   "fine_s3",   "fine_vel",  "correct_if", "fine_vel_s1"};
 
 enum Phase { P_CREATED = 0, P_MESH, P_REGIONS, P_BOUND, P_STATE };
 
@@ -97,8 +97,11 @@ struct fblts_ctx {
     std::vector<uint16_t> t_row;
     int t_sRow = 32, t_hmax = 0, t_emax = 0;
     size_t t_nHalo = 0, t_nFedge = 0, t_nEcl = 0;
+    bool deep_runs_ok = false;
+    std::vector<int32_t> e_owner;          // local owner cell of every local edge (build_local)
     bool tiled = true;
     bool split = false;        // FBLTS_SPLIT=1: separate launches for the thin interface blocks
+    bool fuse_vel = true;      // deep fine velocity stage fused into the next stage 1 (FBLTS_FUSE=0: off)
     int nsm = 148;         // FBLTS_TILED=0 selects the unstaged kernels (development comparisons)
 };
 namespace {
@@ -259,6 +262,7 @@ int fblts_create(fblts_ctx **out, const fblts_config *cfg) {
     c->stream = (cudaStream_t)cfg->stream;
     if (const char *ev = std::getenv("FBLTS_TILED")) c->tiled = std::atoi(ev) != 0;
     if (const char *ev = std::getenv("FBLTS_SPLIT")) c->split = std::atoi(ev) != 0;
+    if (const char *ev = std::getenv("FBLTS_FUSE")) c->fuse_vel = std::atoi(ev) != 0;
     // canonical constants (computed once in double, SURVEY c.1)
     StepConst &s = c->sc;
     const double dt = cfg->dt;
@@ -461,15 +465,21 @@ int build_tiles(fblts_ctx *c) {
         hl.erase(std::unique(hl.begin(), hl.end()), hl.end());
         std::sort(el.begin(), el.end());
         el.erase(std::unique(el.begin(), el.end()), el.end());
-        // longest run of consecutive edge indices = the owned range, the rest are foreign
+        // owned run: the longest run of consecutive indices among the edges whose owner cell is in
+        // the tile (all of them with one rank); every other local edge is foreign
         size_t best = 0, bestLen = 0;
+        auto owned = [&](size_t k) { return c->e_owner[el[k]] >= c0 && c->e_owner[el[k]] < c1; };
         for (size_t k = 0; k < el.size();) {
+            if (!owned(k)) {
+                ++k;
+                continue;
+            }
             size_t k2 = k + 1;
-            while (k2 < el.size() && el[k2] == el[k2 - 1] + 1) ++k2;
+            while (k2 < el.size() && owned(k2) && el[k2] == el[k2 - 1] + 1) ++k2;
             if (k2 - k > bestLen) best = k, bestLen = k2 - k;
             k = k2;
         }
-        const int eo0 = el.empty() ? 0 : el[best], eo1 = eo0 + (int)bestLen;
+        const int eo0 = bestLen ? el[best] : 0, eo1 = eo0 + (int)bestLen;
         for (int e : el)
             if (e < eo0 || e >= eo1) fl.push_back(e);
         const int nLE = (int)el.size();
@@ -504,6 +514,25 @@ int build_tiles(fblts_ctx *c) {
     int32_t *rec = &c->t_info[(size_t)nT * TINFO];
     rec[0] = L.nOwnC, rec[1] = (int32_t)c->t_halo.size(), rec[4] = (int32_t)c->t_fedge.size();
     rec[5] = (int32_t)c->t_ecl.size();
+    // the fused deep velocity + stage-1 sweep writes each deep edge from the tile whose owned run
+    // holds it: usable only if those runs tile [eb.fl[1], eb.end) exactly
+    {
+        std::vector<std::pair<int, int>> runs;
+        for (int t = 0; t < nT; ++t) {
+            const int c0 = ts[t];
+            const bool deep = (c0 >= L.cb.fl[1] && c0 < L.cb.end) || (c0 >= L.cbI.fl[1] && c0 < L.cbI.end);
+            const int32_t *rec = &c->t_info[(size_t)t * TINFO];
+            if (deep && rec[3] > rec[2]) runs.push_back({rec[2], rec[3]});
+        }
+        std::sort(runs.begin(), runs.end());
+        int at = L.eb.fl[1];
+        bool ok = true;
+        for (auto &r : runs) {
+            if (r.first != at) ok = false;
+            at = r.second;
+        }
+        c->deep_runs_ok = ok && at == L.eb.end;
+    }
     c->t_nHalo = c->t_halo.size();
     c->t_nFedge = c->t_fedge.size();
     c->t_nEcl = c->t_ecl.size();
@@ -591,12 +620,14 @@ int build_local(fblts_ctx *c, const std::vector<int32_t> &coc) {
         return eowner(a) < eowner(b);
     });
     std::stable_sort(eRest.begin(), eRest.end(), [&](int a, int b) { return eowner(a) < eowner(b); });
+    c->e_owner.resize(eOwnL.size() + eRest.size());
     L.nOwnE = (int)eOwnL.size();
     L.edgeGlob = eOwnL;
     L.edgeGlob.insert(L.edgeGlob.end(), eRest.begin(), eRest.end());
     L.nE = (int)L.edgeGlob.size();
     std::vector<int32_t> edgeLoc(m.nE, -1);
     for (int e = 0; e < L.nE; ++e) edgeLoc[L.edgeGlob[e]] = e;
+    for (int e = 0; e < L.nE; ++e) c->e_owner[e] = eowner(L.edgeGlob[e]);   // local owner cell (tiles)
     // ---- vertices: those of the edges touching owned cells, by owner cell
     std::vector<int32_t> verts;
     std::vector<int8_t> vmark(m.nV, 0);
@@ -1204,6 +1235,9 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
         const int q = ph - 3, k = q / 3, stg = q % 3;
         const double *hk = k == 0 ? hN : hb(k - 1), *uk = k == 0 ? uN : ub(k - 1);
         if (stg == 0) {
+            // k >= 1 with the fusion: the band velocity sweep runs alone and the deep velocity sweep
+            // of subcycle k-1 is folded into the deep stage-1 sweep of subcycle k (STAGE 4)
+            const bool fused = k > 0 && T && c->fuse_vel && c->deep_runs_ok;
             if (part == 0) {
                 if (k == 0) {
                     mark(K_COARSE_VEL);
@@ -1211,13 +1245,22 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
                 } else {
                     mark(K_FINE_VEL);
                     launch_fine_vel(m, st, hN, hNew, k - 1 == 0 ? hN : hb(k - 2), hb(k - 1),
-                                    k - 1 == 0 ? uN : ub(k - 2), ub(k - 1), sc, pred(k - 1), k - 1, s);
+                                    k - 1 == 0 ? uN : ub(k - 2), ub(k - 1), sc, pred(k - 1), k - 1, s, !fused);
                 }
                 any = true;
             }
             cell_mark(K_FINE_S1);
             launch_fine_s1(m, st, hN, hNew, hk, uk, sc, pred(k), k, s, B, !T);
-            if (T) stage_tiled(c, 1, B, B.fl[1], B.end, StageArgs{hk, hk, uk, st.S, st.h1, 0, 0, 0, sc.c1f, sc.g, K_FINE_S1, k}, s);
+            if (fused) {
+                cell_mark(K_FINE_VS1);
+                StageArgs va{k - 1 == 0 ? hN : hb(k - 2), hk, k - 1 == 0 ? uN : ub(k - 2), st.S, st.h1,
+                             sc.c3f, sc.b3, sc.om2b3, sc.c1f, sc.g, K_FINE_VS1, k};
+                va.h2 = st.h2;
+                va.unew = ub(k - 1);
+                stage_tiled(c, 4, B, B.fl[1], B.end, va, s);
+            } else if (T) {
+                stage_tiled(c, 1, B, B.fl[1], B.end, StageArgs{hk, hk, uk, st.S, st.h1, 0, 0, 0, sc.c1f, sc.g, K_FINE_S1, k}, s);
+            }
             *px = PhaseX{X_C1, st.h1, -1, nullptr};
         } else if (stg == 1) {
             cell_mark(K_FINE_S2);

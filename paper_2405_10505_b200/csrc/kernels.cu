@@ -296,8 +296,8 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
 
 template <int STAGE>
 struct TileShape {
-    static constexpr int NCA = STAGE > 1 ? 3 : 1;   // cell arrays: hprev (, hbase, z_b)
-    static constexpr int NEA = STAGE > 1 ? 4 : 2;   // edge arrays: u, l_e (, S, d_e)
+    static constexpr int NCA = STAGE == 4 ? 4 : (STAGE > 1 ? 3 : 1);   // cell arrays: hprev (, hbase, z_b (, h2))
+    static constexpr int NEA = STAGE > 1 ? 4 : 2;                       // edge arrays: u, l_e (, S, d_e)
 };
 
 struct TileRec {
@@ -316,11 +316,11 @@ __device__ __forceinline__ TileRec load_rec(const TileMesh &t, int tile) {
 // shifted by the tile's alignment offsets so that local index 0 is the tile's first cell / edge.
 template <int STAGE>
 struct TileBuf {
-    double *hp, *hb, *z, *u, *l, *S, *d;
+    double *hp, *hb, *z, *h2, *u, *l, *S, *d;
     uint32_t *ecl;
     __device__ __forceinline__ TileBuf(double *B, int CS2, int ES2, const TileRec &r) {
         const int oc = r.c0 & 1, oe = r.eo0 & 1, ol = r.l0 & 3;
-        hp = B + oc, hb = B + CS2 + oc, z = B + 2 * CS2 + oc;
+        hp = B + oc, hb = B + CS2 + oc, z = B + 2 * CS2 + oc, h2 = B + 3 * CS2 + oc;
         double *E = B + TileShape<STAGE>::NCA * CS2;
         u = E + oe, l = E + ES2 + oe, S = E + 2 * ES2 + oe, d = E + 3 * ES2 + oe;
         ecl = reinterpret_cast<uint32_t *>(E + TileShape<STAGE>::NEA * ES2) + ol;
@@ -344,6 +344,7 @@ __device__ __forceinline__ void issue_bulk(const DevMesh &m, const StageArgs &a,
         bulk_g2s(B + CS2, a.hbase + ca, cbytes, bar);
         bulk_g2s(B + 2 * CS2, m.zb + ca, cbytes, bar);
     }
+    if (STAGE == 4) bulk_g2s(B + 3 * CS2, a.h2 + ca, cbytes, bar);
     double *E = B + NCA * CS2;
     if (ebytes) {
         bulk_g2s(E, a.ubase + ea, ebytes, bar);
@@ -367,6 +368,7 @@ __device__ __forceinline__ void issue_indexed(const DevMesh &m, const StageArgs 
             cp_async8(b.hb + HALO0 + q, a.hbase + x);
             cp_async8(b.z + HALO0 + q, m.zb + x);
         }
+        if (STAGE == 4) cp_async8(b.h2 + HALO0 + q, a.h2 + x);
     };
     auto foreign = [&](int p, int e) {
         cp_async8(b.u + p, a.ubase + e);
@@ -451,24 +453,41 @@ __global__ void __launch_bounds__(NTHR, FBLTS_TILE_MINB) k_stage_tiled(DevMesh m
             A = m.areaCell[i];
         }
         const int nOE = cur.eo1 - cur.eo0, nLE = nOE + cur.f1 - cur.f0;
-        for (int p = tid; p < nLE; p += NTHR) {          // edge phase: T_e overwrites u_e
-            const uint32_t pr = bc.ecl[p];
-            const int q = p < nOE ? p : p + FGAP;
-            const int l0 = pr & 0xFFFF, l1 = pr >> 16;
-            const double H0 = bc.hp[l0], H1 = bc.hp[l1];
-            double ue = bc.u[q];
-            if (STAGE > 1) {
-                const double HS0 = a.bb * H0 + a.omb * bc.hb[l0];
-                const double HS1 = a.bb * H1 + a.omb * bc.hb[l1];
-                const double phi = phi_fast(a.g, HS0, bc.z[l0], HS1, bc.z[l1], bc.d[q]);
-                ue = ue + a.cu * (phi + bc.S[q]);
+#ifndef FBLTS_EDGE_UNROLL
+#define FBLTS_EDGE_UNROLL 1
+#endif
+        // edge phase: T_e overwrites u_e; EU independent edges per thread in flight (fp64 latency)
+        constexpr int EU = FBLTS_EDGE_UNROLL;
+        for (int p0 = tid; p0 < nLE; p0 += EU * NTHR) {
+#pragma unroll
+            for (int uu = 0; uu < EU; ++uu) {
+                const int p = p0 + uu * NTHR;
+                if (p < nLE) {
+                    const uint32_t pr = bc.ecl[p];
+                    const int q = p < nOE ? p : p + FGAP;
+                    const int l0 = pr & 0xFFFF, l1 = pr >> 16;
+                    const double H0 = bc.hp[l0], H1 = bc.hp[l1];
+                    double ue = bc.u[q];
+                    if (STAGE == 2 || STAGE == 3) {
+                        const double HS0 = a.bb * H0 + a.omb * bc.hb[l0];
+                        const double HS1 = a.bb * H1 + a.omb * bc.hb[l1];
+                        const double phi = phi_fast(a.g, HS0, bc.z[l0], HS1, bc.z[l1], bc.d[q]);
+                        ue = ue + a.cu * (phi + bc.S[q]);
+                    } else if (STAGE == 4) {            // u^{n,k} (fine velocity stage 3, subeqn fine_s3)
+                        const double HS0 = a.bb * H0 + a.omb * bc.h2[l0] + a.bb * bc.hb[l0];
+                        const double HS1 = a.bb * H1 + a.omb * bc.h2[l1] + a.bb * bc.hb[l1];
+                        const double phi = phi_fast(a.g, HS0, bc.z[l0], HS1, bc.z[l1], bc.d[q]);
+                        ue = ue + a.cu * (phi + bc.S[q]);
+                        if (p < nOE) a.unew[cur.eo0 + p] = ue;
+                    }
+                    const double Fe = (0.5 * (H0 + H1)) * ue;
+                    bc.u[q] = bc.l[q] * Fe;
+                }
             }
-            const double Fe = (0.5 * (H0 + H1)) * ue;
-            bc.u[q] = bc.l[q] * Fe;
         }
         __syncthreads();
         if (own) {                                        // cell phase
-            const double hbi = STAGE == 1 ? bc.hp[tid] : bc.hb[tid];
+            const double hbi = (STAGE == 1 || STAGE == 4) ? bc.hp[tid] : bc.hb[tid];
             double acc = 0.0;
 #pragma unroll
             for (int j = 0; j < G; ++j) {
@@ -905,7 +924,7 @@ static void tile_strides(int hmax, int emax, int &CS2, int &ES2) {
     ES2 = (emax + FGAP + 8 + 3) & ~3;       // + gap and slack; multiple of 4 (the uint32 pair array)
 }
 int stage_tiled_smem_bytes_host(int stage, int hmax, int emax) {
-    const int nca = stage > 1 ? 3 : 1, nea = stage > 1 ? 4 : 2;
+    const int nca = stage == 4 ? 4 : (stage > 1 ? 3 : 1), nea = stage > 1 ? 4 : 2;
     int CS2, ES2;
     tile_strides(hmax, emax, CS2, ES2);
     return 8 * (2 + 2 * (nca * CS2 + nea * ES2 + ES2 / 2 + 2));
@@ -921,6 +940,7 @@ int stage_tiled_configure(const DevMesh &m) {
         set((const void *)k_stage_tiled<G, 1>);
         set((const void *)k_stage_tiled<G, 2>);
         set((const void *)k_stage_tiled<G, 3>);
+        set((const void *)k_stage_tiled<G, 4>);
     });
     return (int)e;
 }
@@ -932,14 +952,17 @@ void launch_stage_tiled(const DevMesh &m, int stage, int tile0, int tile1, int h
     int CS, ES;
     tile_strides(hmax, emax, CS, ES);
     FBLTS_DISPATCH_G(m.ecS, {
-        const void *f = stage == 1 ? (const void *)k_stage_tiled<G, 1>
-                                   : (stage == 2 ? (const void *)k_stage_tiled<G, 2> : (const void *)k_stage_tiled<G, 3>);
+        const void *f = stage == 1   ? (const void *)k_stage_tiled<G, 1>
+                        : stage == 2 ? (const void *)k_stage_tiled<G, 2>
+                        : stage == 3 ? (const void *)k_stage_tiled<G, 3>
+                                     : (const void *)k_stage_tiled<G, 4>;
         int per = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, NTHR, smem);
         const int grid = std::max(1, std::min(tile1 - tile0, nsm * std::max(1, per)));
         if (stage == 1) k_stage_tiled<G, 1><<<grid, NTHR, smem, s>>>(m, tile0, tile1, CS, ES, a, err);
         else if (stage == 2) k_stage_tiled<G, 2><<<grid, NTHR, smem, s>>>(m, tile0, tile1, CS, ES, a, err);
-        else k_stage_tiled<G, 3><<<grid, NTHR, smem, s>>>(m, tile0, tile1, CS, ES, a, err);
+        else if (stage == 3) k_stage_tiled<G, 3><<<grid, NTHR, smem, s>>>(m, tile0, tile1, CS, ES, a, err);
+        else k_stage_tiled<G, 4><<<grid, NTHR, smem, s>>>(m, tile0, tile1, CS, ES, a, err);
     });
 }
 
@@ -1030,12 +1053,12 @@ void launch_fine_s3(const DevMesh &m, const DevState &st, const double *hN, cons
 }
 void launch_fine_vel(const DevMesh &m, const DevState &st, const double *hN, const double *hNew, const double *hk,
                      const double *hnext, const double *uk, double *unext, const StepConst &sc,
-                     const PredConst &pc, int k, cudaStream_t s) {
+                     const PredConst &pc, int k, cudaStream_t s, bool deep) {
     const FineArrays a = fine_arrays(st, hN, hNew, hk);
     const int b0 = m.eb.if2, b1 = m.eb.fl[1], end = m.eb.end;
     if (b1 > b0)
         k_fine_vel<true><<<nblocks(b1 - b0), TPB, 0, s>>>(m, a, hnext, uk, st.S, unext, st.accU, sc, pc, k, b0, b1);
-    if (end > b1)
+    if (deep && end > b1)
         k_fine_vel<false><<<nblocks(end - b1), TPB, 0, s>>>(m, a, hnext, uk, st.S, unext, st.accU, sc, pc, k, b1, end);
 }
 void launch_correct(const DevMesh &m, const DevState &st, const double *hN, const double *uN, double *hNew,
