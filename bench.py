@@ -326,6 +326,33 @@ def arm_native(args):
                "d2h_bytes_per_step": 32 + state_bytes / args.steps,
                "how": "set_state(pinned host h,u) + K x (step(1) + diagnostics()) + get_state(pinned host)"}
 
+    # ---------------- the same workload as global FB-RK(3,2) at the fine step (no LTS), same GPU:
+    # the paper's speedup framing (FB-LTS vs a global scheme at the step the fine region needs,
+    # P:L1367-1403) measured on the device; FB-LTS advances dt per coarse step, the global scheme
+    # dt / M per step, so the speedup at equal simulated time is M * T_global / T_lts.
+    lts_vs_global = None
+    if world == 1 and not args.no_global and c.M > 1:
+        s.close()
+        del s
+        torch.cuda.empty_cache()
+        sg = Solver(c.mesh, np.zeros(c.mesh.nCells, dtype=bool), c.dt / c.M, 1, g=c.g, beta=c.beta, rho0=c.rho0,
+                    slow=c.slow, tau_n=c.tau_n)
+        sg.set_state(c.h0, c.u0, 0.0)
+        sg.step(3)
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        sg.step(args.steps)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        sg.sync()
+        tg = g0.elapsed_time(g1) / args.steps
+        lts_vs_global = {"global_fbrk32_ms_per_step": tg, "global_dt": c.dt / c.M,
+                         "global_cell_updates_per_s": c.mesh.nCells / (tg * 1e-3),
+                         "lts_speedup_at_equal_simulated_time": c.M * tg / ms_step,
+                         "how": "same mesh and state, no fine cells, dt/M, K steps, CUDA events"}
+        sg.close()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = run_cpu_baseline()
@@ -355,6 +382,7 @@ def arm_native(args):
                         "GBps": bm[k] / (tms / n_prof * 1e-3) / 1e9}
                     for k, (tms, n) in prof.items() if n},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(round(launches_per_step * args.steps)),
+        "lts_vs_global": lts_vs_global,
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)
@@ -371,6 +399,7 @@ def main():
     ap.add_argument("--config", default="config5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-global", action="store_true", help="skip the global FB-RK(3,2) comparison run")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -6,7 +6,7 @@ CFG=config5
 if [ "$1" == "--config" ]; then CFG=$2; shift 2; fi
 for V in "$@"; do
   FBLTS_NVCC_EXTRA="$V" python -m paper_2405_10505_b200.build --force > /dev/null 2>&1 || { echo "build failed: $V"; continue; }
-  timeout 300 python bench.py --config $CFG --no-cpu-baseline --no-e2e --steps 10 > gpurun_out/ab.log 2>&1
+  timeout 300 python bench.py --config $CFG --no-cpu-baseline --no-e2e --no-global --steps 10 > gpurun_out/ab.log 2>&1
   echo "=== variant [$V] ${FBLTS_TILED:+TILED=$FBLTS_TILED}"
   python - <<'PY'
 import json

@@ -5,7 +5,7 @@ if [ "$1" == "--config" ]; then CFG=$2; shift 2; fi
 for V in "$@"; do
   EXTRA="${V%%|*}"; ENVS="${V#*|}"; [ "$ENVS" == "$V" ] && ENVS=""
   FBLTS_NVCC_EXTRA="$EXTRA" python -m paper_2405_10505_b200.build --force > /dev/null 2>&1 || { echo "build failed: $V"; continue; }
-  env $ENVS timeout 300 python bench.py --config $CFG --no-cpu-baseline --no-e2e --steps 10 > gpurun_out/ab.log 2>&1
+  env $ENVS timeout 300 python bench.py --config $CFG --no-cpu-baseline --no-e2e --no-global --steps 10 > gpurun_out/ab.log 2>&1
   echo "=== variant [$EXTRA] env [$ENVS]"
   python - <<'PY'
 import json

@@ -290,3 +290,52 @@ def test_parity_config4_reduced_100_steps(Solver):
     _, hg, ug, _ = run_gpu(Solver, c, 100)
     eh, eu = assert_parity(hg, ug, ho, uo)
     print(f"config4 (dx_scale 8): eps_h={eh:.3e} eps_u={eu:.3e}")
+
+
+def test_lake_at_rest_on_gpu(Solver):
+    """P6 through the GPU path: u = 0, h + z_b = const over random (integer) bathymetry, f != 0,
+    slow terms on, fine region in the deep part: after 20 coarse steps the GPU state equals the
+    oracle's bit for bit and moves only at roundoff (the literal FB average rounds)."""
+    from inputs.hexmesh import build_periodic_hex_mesh
+    m = build_periodic_hex_mesh(48, 40, 2000.0)
+    rng = np.random.default_rng(6)
+    H = np.round(50.0 + 3000.0 * rng.random(m.nCells))
+    m.bottomDepth = H
+    m.fVertex = np.full(m.nVertices, 1e-4)
+    h0, u0 = H + 1.0, np.zeros(m.nEdges)
+    fine = H > 1500.0
+    c = configs.Case(name="lake", mesh=m, h0=h0, u0=u0, fine_mask=fine, tau_n=np.zeros(m.nEdges), M=4,
+                     dt=10.0, n_steps=20)
+    ho, uo, _ = run_oracle(c, 20)
+    _, hg, ug, _ = run_gpu(Solver, c, 20)
+    assert np.array_equal(hg, ho) and np.array_equal(ug, uo)
+    assert np.max(np.abs(ug)) <= 1e-12 and np.max(np.abs(hg - h0) / h0) <= 1e-13
+
+
+def test_zero_steps_is_identity(Solver):
+    """step(0) enqueues nothing: the state read back is the state set (original order)."""
+    c = configs.config1()
+    s = Solver(c.mesh, c.fine_mask, c.dt, c.M)
+    s.set_state(c.h0, c.u0, 5.0)
+    s.step(0)
+    h, u, t = s.state()
+    assert np.array_equal(h, c.h0) and np.array_equal(u, c.u0) and t == 5.0
+    s.close()
+
+
+def test_unfused_and_unstaged_paths_agree(Solver, monkeypatch):
+    """The staged tile kernels, the fused deep velocity + stage-1 sweep and the unstaged per-cell
+    kernels are three evaluations of the same formulas: all bitwise equal (and equal to the oracle)."""
+    c = configs.small_shelf(nx=64, ny=48, seed=9, dt=25.0)
+    ho, uo, _ = run_oracle(c, 20)
+    res = []
+    for env in ({}, {"FBLTS_FUSE": "0"}, {"FBLTS_TILED": "0"}, {"FBLTS_SPLIT": "1"}):
+        for k in ("FBLTS_FUSE", "FBLTS_TILED", "FBLTS_SPLIT"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        s, hg, ug, _ = run_gpu(Solver, c, 20)
+        s.close()
+        res.append((hg, ug))
+    for hg, ug in res:
+        assert np.array_equal(hg, ho) and np.array_equal(ug, uo)
