@@ -106,6 +106,20 @@ def byte_model(counts, M, fused, maxE=6, maxE2=10):
     return b
 
 
+def rk4_dt(c, name):
+    """0.9 x the RK4 Courant limit nu_loc bisected with the oracle on this config (or its proxy),
+    applied to this mesh's max_e sqrt(g max H) / d_e; (None, why) if no scan is recorded."""
+    try:
+        with open(os.path.join(ROOT, "configs", "dt.json")) as f:
+            nu = float(json.load(f)[f"{name}_rk4"]["nu_loc_limit"])
+    except (OSError, KeyError, ValueError):
+        return None, f"no {name}_rk4 entry in configs/dt.json"
+    H = c.mesh.bottomDepth
+    c0, c1 = c.mesh.cellsOnEdge[:, 0], c.mesh.cellsOnEdge[:, 1]
+    cmax = float(np.max(np.sqrt(c.g * np.maximum(H[c0], H[c1])) / c.mesh.dcEdge))
+    return 0.9 * nu / cmax, f"0.9 x nu_loc {nu:.4f} (configs/dt.json {name}_rk4)"
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -352,6 +366,27 @@ def arm_native(args):
                          "lts_speedup_at_equal_simulated_time": c.M * tg / ms_step,
                          "how": "same mesh and state, no fine cells, dt/M, K steps, CUDA events"}
         sg.close()
+        del sg
+        torch.cuda.empty_cache()
+        # the paper's reference scheme: classical RK4 on the unsplit system at ITS stable step
+        # (0.9 x the oracle-bisected Courant limit, configs/dt.json "<config>_rk4")
+        dt4, src4 = rk4_dt(c, args.config)
+        if dt4 is not None:
+            sr = Solver(c.mesh, np.zeros(c.mesh.nCells, dtype=bool), dt4, 1, g=c.g, beta=c.beta, rho0=c.rho0,
+                        slow=c.slow, tau_n=c.tau_n, scheme="rk4")
+            sr.set_state(c.h0, c.u0, 0.0)
+            sr.step(3)
+            torch.cuda.synchronize()
+            r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            r0.record(stream)
+            sr.step(args.steps)
+            r1.record(stream)
+            torch.cuda.synchronize()
+            sr.sync()
+            tr = r0.elapsed_time(r1) / args.steps
+            sr.close()
+            lts_vs_global.update({"rk4_ms_per_step": tr, "rk4_dt": dt4, "rk4_dt_source": src4,
+                                  "lts_speedup_vs_rk4_at_equal_simulated_time": (c.dt / ms_step) / (dt4 / tr)})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

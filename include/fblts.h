@@ -111,7 +111,14 @@ typedef struct {
     int32_t nranks;      /* number of ranks (1 for single GPU) */
     const void *nccl_id; /* 128-byte ncclUniqueId shared by all ranks; NULL if nranks == 1, or for
                             the members of a one-process loopback group (fblts_step_group) */
+    int32_t scheme;      /* FBLTS_SCHEME_FBLTS (0): FB-LTS, split mode (global FB-RK(3,2) when there are
+                            no fine cells or M = 1); FBLTS_SCHEME_RK4 (1): classical four-stage RK4 on
+                            the unsplit system, global (M and the fine mask ignored), one
+                            rank -- the paper's reference scheme, for speedup comparisons */
 } fblts_config;
+
+#define FBLTS_SCHEME_FBLTS 0
+#define FBLTS_SCHEME_RK4   1
 
 /* Create a context.  *out receives the handle (NULL on failure).
  * Errors: INVALID_ARG (M < 1, dt <= 0, r < 1, bad rank/nranks), CUDA, NCCL. */

@@ -21,7 +21,7 @@ namespace fblts {
 
 enum KernelKind {
     K_SLOW_PRE = 0, K_SLOW_EDGE, K_COARSE_S1, K_COARSE_S2, K_COARSE_S3, K_COARSE_VEL,
-    K_FINE_S1, K_FINE_S2, K_FINE_S3, K_FINE_VEL, K_CORRECT, K_FINE_VS1, K_NUM
+    K_FINE_S1, K_FINE_S2, K_FINE_S3, K_FINE_VEL, K_CORRECT, K_FINE_VS1, K_RK4_STAGE, K_NUM
 };
 
 // Region boundaries of one region-major block: [begin,if2) int, [if2,if1) IF-2,
@@ -132,6 +132,7 @@ struct DevState {
     double *q;                          // vertices
     double *K;                          // cells
     double *accH, *accU;                // accH indexed by owned cell (IF cells used), accU by e - eb.if2 (IF edges)
+    double *rkU[2], *rkAccU;            // RK4 scheme: stage velocities (ping-pong) and the velocity sum
     double *stage;                      // staging for set/get_state (max(nC, nE) doubles)
     int32_t *cellOld, *edgeOld;         // new -> old permutation (device)
     double *diag;                       // reduction scratch
@@ -189,6 +190,13 @@ void launch_fine_vel(const DevMesh &m, const DevState &st, const double *hN, con
                      const StepConst &sc, const PredConst &pc, int k, cudaStream_t s, bool deep = true);
 void launch_correct(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
                     double *hNew, double *uNew, const StepConst &sc, cudaStream_t s, const Bounds &b, bool edges);
+// Classical RK4 on the unsplit system (fbrk32.rk4_step), stage `stage` = 1..4 on every owned
+// cell and edge: k = (Psi(us, hs), Phi^fast(hs) + S) with S = Phi^slow(us, hs) already in st.S;
+// acc = k (stage 1), acc + 2 k (2, 3), acc + k (4); next stage (h^n, u^n) + cnext k, and after stage 4
+// (h, u)^{n+1} = (h^n, u^n) + (dt/6) acc.
+void launch_rk4_stage(const DevMesh &m, const DevState &st, int stage, const double *hN, const double *uN,
+                      const double *hs, const double *us, double *hout, double *uout, double cnext,
+                      double dt6, double g, cudaStream_t s);
 void launch_permute_in(const int32_t *old_of_new, const double *src, double *dst, int n, cudaStream_t s);
 void launch_permute_out(const int32_t *old_of_new, const double *src, double *dst, int n, cudaStream_t s);
 // diagnostics: writes out[4] (device) = mass, Gamma, min h, max nu

@@ -23,7 +23,8 @@ using namespace fblts;
 namespace {
 
 const char *kKernelNames[K_NUM] = {"slow_pre",  "slow_edge", "coarse_s1", "coarse_s2", "coarse_s3", "coarse_vel",
-                                   "fine_s1",   "fine_s2",   "fine_s3",   "fine_vel",  "correct_if", "fine_vel_s1"};
+                                   "fine_s1",   "fine_s2",   "fine_s3",   "fine_vel",  "correct_if", "fine_vel_s1",
+                                   "rk4_stage"};
 
 enum Phase { P_CREATED = 0, P_MESH, P_REGIONS, P_BOUND, P_STATE };
 
@@ -251,6 +252,8 @@ int fblts_create(fblts_ctx **out, const fblts_config *cfg) {
     if (!(cfg->dt > 0.0) || cfg->M < 1 || cfg->r < 1 || !(cfg->g > 0.0) || !(cfg->rho0 > 0.0))
         return FBLTS_ERR_INVALID_ARG;
     if (cfg->nranks < 1 || cfg->nranks > 64 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return FBLTS_ERR_INVALID_ARG;
+    if (cfg->scheme != FBLTS_SCHEME_FBLTS && cfg->scheme != FBLTS_SCHEME_RK4) return FBLTS_ERR_INVALID_ARG;
+    if (cfg->scheme == FBLTS_SCHEME_RK4 && cfg->nranks != 1) return FBLTS_ERR_INVALID_ARG;   // reference scheme: one rank
     // No CUDA call here: mesh upload, labelling and renumbering are host work, so a context
     // can be created (and its labels inspected) on a machine without a GPU.
     fblts_ctx *c = new fblts_ctx();
@@ -955,6 +958,10 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
     put(s.q, L.nV);
     put(s.accH, std::max(1, L.nOwnC));
     put(s.accU, std::max(1, L.eb.f - L.eb.if2));
+    const size_t nrk = c->cfg.scheme == FBLTS_SCHEME_RK4 ? nE1 : 1;
+    put(s.rkU[0], nrk);
+    put(s.rkU[1], nrk);
+    put(s.rkAccU, nrk);
     put(s.stage, std::max(m.nC, m.nE));
     put(s.cellOld, L.nC);
     put(s.edgeOld, L.nE);
@@ -1342,7 +1349,37 @@ int allgather_nccl(fblts_ctx *c, const double *send6, double *recv) {
 // the communication stream, forked after the phase's boundary-block kernel and joined before the
 // next phase, so it overlaps the interior-block kernel (the end-of-step exchange of rings 1-2 and
 // of the remote-owned edges needs the interior values and runs after it).
+// One classical RK4 step (FBLTS_SCHEME_RK4, one rank): per stage the slow terms at the stage state,
+// then one launch for every cell and edge (stage tendency, running sum, next stage state).
+int enqueue_rk4_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
+    const DevMesh &m = c->dm;
+    DevState st = c->ds;
+    const double *hN = c->hbuf[par], *uN = c->ubuf[par];
+    double *hNew = c->hbuf[1 - par], *uNew = c->ubuf[1 - par];
+    const double dt = c->cfg.dt;
+    const double cn[4] = {dt / 2, dt / 2, dt, 0.0};
+    const double *hs = hN, *us = uN;
+    double *hb[2] = {st.h1, st.h2};
+    for (int stage = 1; stage <= 4; ++stage) {
+        if (c->cfg.slow) {
+            if (rec) rec->mark(K_SLOW_PRE, s);
+            launch_slow_pre(m, st, hs, us, s);
+            if (rec) rec->mark(K_SLOW_EDGE, s);
+            launch_slow_edge(m, st, hs, c->sc, s);
+        }
+        double *ho = stage < 4 ? hb[stage % 2] : hNew;
+        double *uo = stage < 4 ? st.rkU[stage % 2] : uNew;
+        if (rec) rec->mark(K_RK4_STAGE, s);
+        launch_rk4_stage(m, st, stage, hN, uN, hs, us, ho, uo, cn[stage - 1], dt / 6, c->sc.g, s);
+        hs = ho;
+        us = uo;
+    }
+    if (rec) rec->mark(-1, s);
+    return FBLTS_OK;
+}
+
 int enqueue_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
+    if (c->cfg.scheme == FBLTS_SCHEME_RK4) return enqueue_rk4_step(c, par, s, rec);
     const bool multi = c->cfg.nranks > 1;
     PhaseX px, px1;
     for (int ph = 0; enqueue_phase(c, par, ph, s, rec, &px, 0); ++ph) {

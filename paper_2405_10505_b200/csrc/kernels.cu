@@ -781,6 +781,65 @@ __global__ void __launch_bounds__(TPB) k_correct(DevMesh m, const double *__rest
     }
 }
 
+// ---------------------------------------------------------------- RK4 reference scheme
+// Classical four-stage RK4 on the unsplit system y = (h, u), y' = (Psi(u, h), Phi^fast(h) + Phi^slow(u, h))
+// (oracle fbrk32.rk4_step): evaluated as numpy does, k1 + 2 k2 + 2 k3 + k4 left to right.
+template <int G>
+__global__ void __launch_bounds__(TPB) k_rk4_stage(DevMesh m, int stage, const double *__restrict__ hN,
+                                                   const double *__restrict__ uN, const double *__restrict__ hs,
+                                                   const double *__restrict__ us, const double *__restrict__ S,
+                                                   double *__restrict__ accH, double *__restrict__ accU,
+                                                   double *__restrict__ hout, double *__restrict__ uout,
+                                                   double cnext, double dt6, double g, unsigned nbC, DevError *err) {
+    double kx, base;
+    double *acc, *out;
+    int x;
+    if (blockIdx.x < nbC) {
+        x = blockIdx.x * TPB + threadIdx.x;
+        if (x >= m.nOwnC) return;
+        int2 r[G];
+        load_row<G>(m, x, r);
+        const int n = m.nEoC[x];
+        const double Hi = hs[x];
+        double a = 0.0;
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+            if (j < n) {
+                bool pos;
+                const int e = decode(r[j].x, pos);
+                a = a + psi_term(pos, Hi, hs[r[j].y], us[e], m.dv[e]);
+            }
+        }
+        kx = -a / m.areaCell[x];
+        base = hN[x];
+        acc = accH;
+        out = hout;
+    } else {
+        x = (blockIdx.x - nbC) * TPB + threadIdx.x;
+        if (x >= m.nOwnE) return;
+        const int2 c = m.coe[x];
+        kx = phi_fast(g, hs[c.x], m.zb[c.x], hs[c.y], m.zb[c.y], m.dc[x]) + S[x];
+        base = uN[x];
+        acc = accU;
+        out = uout;
+    }
+    double sum;
+    if (stage == 1) sum = kx;
+    else if (stage == 4) sum = acc[x] + kx;
+    else sum = acc[x] + 2.0 * kx;
+    if (stage < 4) {
+        acc[x] = sum;
+        const double v = base + cnext * kx;
+        out[x] = v;
+        if (blockIdx.x < nbC && !(v > 0.0)) report(err, K_RK4_STAGE, stage, x, v);
+    } else {
+        const double v = base + dt6 * sum;
+        out[x] = v;
+        if (blockIdx.x < nbC && !(v > 0.0)) report(err, K_RK4_STAGE, stage, x, v);
+    }
+}
+
+
 // ---------------------------------------------------------------- permutation, diagnostics
 __global__ void k_permute_in(const int32_t *__restrict__ old, const double *__restrict__ src,
                              double *__restrict__ dst, int n) {
@@ -1083,6 +1142,14 @@ void launch_diagnostics(const DevMesh &m, const DevState &st, const double *h, c
                         double *out_dev, cudaStream_t s) {
     k_diag_partial<<<DIAG_BLOCKS, TPB, 0, s>>>(m, h, u, sc, st.diag);
     k_diag_final<<<1, 32, 0, s>>>(st.diag, DIAG_BLOCKS, out_dev);
+}
+
+void launch_rk4_stage(const DevMesh &m, const DevState &st, int stage, const double *hN, const double *uN,
+                      const double *hs, const double *us, double *hout, double *uout, double cnext, double dt6,
+                      double g, cudaStream_t s) {
+    const unsigned nbC = nblocks(m.nOwnC), nbE = nblocks(m.nOwnE);
+    FBLTS_DISPATCH_G(m.ecS, k_rk4_stage<G><<<nbC + nbE, TPB, 0, s>>>(m, stage, hN, uN, hs, us, st.S, st.hT, st.rkAccU,
+                                                                      hout, uout, cnext, dt6, g, nbC, st.err));
 }
 
 }  // namespace fblts

@@ -21,34 +21,43 @@ from oracle import diagnostics as dg            # noqa: E402
 from oracle import fbrk32, lts                  # noqa: E402
 
 NU_MAX_FBRK = 3.8621532 / np.sqrt(6.0)
+NU_MAX_RK4 = 2.0 * np.sqrt(2.0) / np.sqrt(6.0)
 OUT = configs.DT_TABLE
 
 
-def stable(case, lab, dt, steps=300):
+def stable(case, lab, dt, steps=300, scheme="fblts"):
     phys = fbrk32.Phys(g=case.g, beta=case.beta, slow=case.slow, tau_n=case.tau_n, rho0=case.rho0)
     h, u = case.h0.copy(), case.u0.copy()
     with np.errstate(all="ignore"):
         for _ in range(steps):
-            h, u = lts.fblts_step(case.mesh, lab, h, u, dt, case.M, phys)
+            if scheme == "rk4":
+                h, u = fbrk32.rk4_step(case.mesh, h, u, dt, phys)
+            else:
+                h, u = lts.fblts_step(case.mesh, lab, h, u, dt, case.M, phys)
             if not (np.all(np.isfinite(u)) and np.all(np.isfinite(h))) or np.max(np.abs(u)) > 5.0:
                 return False
     return True
 
 
-def scan(name, case, iters=6):
+def scan(name, case, iters=6, scheme="fblts"):
+    """scheme "rk4": the global classical RK4 reference, bracket top at its imaginary-axis
+    limit 2 sqrt(2) / sqrt(6) of the hex gravity-wave Courant number."""
+    if scheme == "rk4":
+        case.fine_mask = np.zeros(case.mesh.nCells, dtype=bool)
+        case.M = 1
     lab = lts.label_regions(case.mesh, case.fine_mask)
     nu1 = dg.rest_courant(case.mesh, lab, 1.0, case.M, case.g)
-    top = NU_MAX_FBRK / nu1
+    top = (NU_MAX_RK4 if scheme == "rk4" else NU_MAX_FBRK) / nu1
     lo, hi = 0.5 * top, 1.0 * top
     t0 = time.time()
-    if not stable(case, lab, lo):
+    if not stable(case, lab, lo, scheme=scheme):
         raise RuntimeError(f"{name}: unstable at the bracket bottom {lo:.3f} s")
-    if stable(case, lab, hi):
+    if stable(case, lab, hi, scheme=scheme):
         lo = hi
     else:
         for _ in range(iters):
             mid = 0.5 * (lo + hi)
-            if stable(case, lab, mid):
+            if stable(case, lab, mid, scheme=scheme):
                 lo = mid
             else:
                 hi = mid
@@ -61,19 +70,21 @@ def scan(name, case, iters=6):
 
 def main(names):
     for name in names:
-        if name == "config1":
+        scheme = "rk4" if name.endswith("_rk4") else "fblts"
+        base = name[:-4] if scheme == "rk4" else name
+        if base == "config1":
             case = configs.config1(dt=1.0)
-        elif name == "config2":
+        elif base == "config2":
             case = configs.config2(dt=1.0)
-        elif name == "config3":
+        elif base == "config3":
             # the level-5 dual (10,242 cells) of the config-3 recipe; the Courant limit nu_loc
             # is applied to the level-8 mesh by inputs.configs.config3
             case = configs.config3(level=5, dt=1.0)
-        elif name == "config4":
+        elif base == "config4":
             # the dx_scale = 8 reduction of the config-4 recipe (~12 k cells, same disk, shelf and
             # M = 8); the Courant limit nu_loc is applied to the full mesh by inputs.configs.config4
             case = configs.config4(dx_scale=8, dt=1.0)
-        elif name == "config5":
+        elif base == "config5":
             # proxy: one 256-km tile of config 5 (same dc, profile, roughness recipe, M) in x,
             # 128 km in y; the full 4096^2 mesh is too large for 300 oracle steps per trial.
             # bump density kept: 8 bumps per 256 x 1773 km tile -> 1 bump on the 256 x 128 km proxy
@@ -81,8 +92,9 @@ def main(names):
                                       bumps_per_tile=1)
         else:
             raise SystemExit(f"unknown config {name}")
-        res = scan(name, case)
-        if name == "config5":
+        res = scan(name, case, scheme=scheme)
+        res["scheme"] = scheme
+        if base == "config5":
             res["proxy"] = "512x296 cells (one 256-km x-tile, 128 km in y, dc = 500 m, 1 bump, seed 5)"
         print(name, res, flush=True)
         table = json.load(open(OUT)) if os.path.exists(OUT) else {}

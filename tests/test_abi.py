@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(abi):
 
 def test_kernel_names(abi):
     names = [abi.fblts_kernel_name(k) for k in range(abi.NUM_KERNELS)]
-    assert names[0] == "slow_pre" and names[-1] == "fine_vel_s1" and len(set(names)) == abi.NUM_KERNELS
+    assert names[0] == "slow_pre" and names[-1] == "rk4_stage" and len(set(names)) == abi.NUM_KERNELS
 
 
 @pytest.mark.parametrize("which", ["cfg1", "shelf", "shelf_big"])
@@ -101,3 +101,10 @@ def test_call_order_and_args(abi):
         assert ei.value.code == -8
     finally:
         abi.fblts_destroy(ctx)
+
+
+def test_rk4_scheme_is_single_rank(abi):
+    """FBLTS_SCHEME_RK4 is the one-rank reference scheme: asking for it with two ranks is rejected."""
+    with pytest.raises(abi.FbltsError) as ei:
+        abi.fblts_create(10.0, 1, scheme="rk4", nranks=2, rank=0)
+    assert ei.value.code == -1
