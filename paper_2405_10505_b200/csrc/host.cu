@@ -1066,7 +1066,8 @@ int fblts_bind_workspace(fblts_ctx *c, void *ptr, size_t bytes) {
     CUDA_TRY(c, up(tm.fedge, c->t_fedge.data(), c->t_fedge.size() * 4));
     CUDA_TRY(c, up(tm.ecl, c->t_ecl.data(), c->t_ecl.size() * 4));
     CUDA_TRY(c, up(tm.row, c->t_row.data(), c->t_row.size() * 2));
-    if (stage_tiled_smem_bytes_host(3, c->t_hmax, c->t_emax) > TILE_SMEM_MAX) c->tiled = false;   // pathological tiles
+    if (stage_tiled_smem_bytes_host(4, c->t_hmax, c->t_emax) > TILE_SMEM_MAX) c->split = true;    // size launches per block
+    if (stage_tiled_smem_bytes_host(4, c->t_hmax, c->t_emax) > TILE_SMEM_MAX && !c->split) c->tiled = false;
     CUDA_TRY(c, cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->cfg.device));
     if (c->tiled) CUDA_TRY(c, (cudaError_t)stage_tiled_configure(d));
     CUDA_TRY(c, cudaStreamSynchronize(s));
@@ -1154,6 +1155,14 @@ void stage_tiled_run(fblts_ctx *c, int stage, int cbegin, int cend, const StageA
         const int32_t *r = &c->t_info[(size_t)t * TINFO], *n = r + TINFO;
         hmax = std::max(hmax, n[1] - r[1]);
         emax = std::max(emax, r[3] - r[2] + n[4] - r[4]);
+    }
+    if (stage_tiled_smem_bytes_host(stage, hmax, emax) > TILE_SMEM_MAX) {   // too large: halve the range
+        if (t1 - t0 > 1) {
+            const int mid = c->t_start[t0 + (t1 - t0) / 2];
+            stage_tiled_run(c, stage, cbegin, mid, a, s);
+            stage_tiled_run(c, stage, mid, cend, a, s);
+            return;
+        }
     }
     launch_stage_tiled(c->dm, stage, t0, t1, hmax, emax, c->nsm, a, c->ds.err, s);
 }

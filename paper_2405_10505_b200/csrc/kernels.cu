@@ -37,6 +37,10 @@ constexpr int TPB = 256;
 #ifndef FBLTS_TILE_MINB
 #define FBLTS_TILE_MINB 2
 #endif
+#ifndef FBLTS_TILE_NBUF
+#define FBLTS_TILE_NBUF 2
+#endif
+constexpr int NBUF = FBLTS_TILE_NBUF;   // tile buffers in the staging ring (>= 2)
 #ifndef FBLTS_TILE_NTHR
 #define FBLTS_TILE_NTHR 256
 #endif
@@ -269,8 +273,10 @@ __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)_
 __device__ __forceinline__ void cp_async8(void *dst, const void *src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_pending() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -407,37 +413,49 @@ __global__ void __launch_bounds__(NTHR, FBLTS_TILE_MINB) k_stage_tiled(DevMesh m
     extern __shared__ __align__(16) double smem[];
     constexpr int NCA = TileShape<STAGE>::NCA, NEA = TileShape<STAGE>::NEA;
     const int BUF = NCA * CS2 + NEA * ES2 + ES2 / 2 + 2;   // doubles per buffer (+ ecl, 16-B multiple)
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);    // 2 mbarriers
-    double *buf0 = smem + 2;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);    // NBUF mbarriers
+    double *buf0 = smem + ((NBUF + 1) & ~1);               // 16-byte aligned after the barriers
     const TileMesh &t = m.tm;
     const int tid = threadIdx.x;
     int tile = tile0 + blockIdx.x;
     if (tile >= tile1) return;
+    const int G0 = gridDim.x;
     if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+        for (int k = 0; k < NBUF; ++k) mbar_init(&bar[k], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
+    // ring of NBUF tile buffers: tiles k .. k+NBUF-2 are in flight while tile k is computed; the
+    // halo / foreign copies of a tile form one cp.async group (committed once per tile, even if
+    // empty), so waiting for "all but the newest NBUF-2 groups" waits exactly for the current tile
     int hx[HPT], fx[FPT];
-    TileRec nx = load_rec(t, tile);
-    if (tid == 0) issue_bulk<STAGE>(m, a, nx, buf0, CS2, ES2, &bar[0]);
-    load_indices(t, nx, tid, hx, fx);
-    issue_indexed<STAGE>(m, a, nx, TileBuf<STAGE>(buf0, CS2, ES2, nx), tid, hx, fx);
-    unsigned phase[2] = {0u, 0u};
+    for (int k = 0; k < NBUF - 1; ++k) {
+        const int tk = tile + k * G0;
+        if (tk < tile1) {
+            const TileRec rk = load_rec(t, tk);
+            double *Bk = buf0 + k * BUF;
+            if (tid == 0) issue_bulk<STAGE>(m, a, rk, Bk, CS2, ES2, &bar[k]);
+            load_indices(t, rk, tid, hx, fx);
+            issue_indexed<STAGE>(m, a, rk, TileBuf<STAGE>(Bk, CS2, ES2, rk), tid, hx, fx);
+        }
+        cp_async_commit();
+    }
+    unsigned phase = 0u;                                   // bit b: parity of buffer b's next completion
     int buf = 0;
-    for (; tile < tile1; tile += gridDim.x, buf ^= 1) {
-        const TileRec cur = nx;
-        const int tn = tile + gridDim.x;
+    for (; tile < tile1; tile += G0, buf = (buf + 1 == NBUF ? 0 : buf + 1)) {
+        const TileRec cur = load_rec(t, tile);
+        const int tn = tile + (NBUF - 1) * G0;             // the tile that reuses the previous buffer
         const bool more = tn < tile1;
+        TileRec nx{};
         if (more) nx = load_rec(t, tn);
-        mbar_wait(&bar[buf], phase[buf]);
-        phase[buf] ^= 1u;
-        cp_async_wait_all();
-        __syncthreads();                                   // tile `cur` staged; buffer buf^1 free
-        double *Bn = buf0 + (buf ^ 1) * BUF;
+        mbar_wait(&bar[buf], (phase >> buf) & 1u);
+        phase ^= 1u << buf;
+        cp_async_wait_pending<NBUF - 2>();
+        __syncthreads();                                   // tile `cur` staged; the previous buffer free
+        const int bn = buf == 0 ? NBUF - 1 : buf - 1;
+        double *Bn = buf0 + bn * BUF;
         if (more) {
-            if (tid == 0) issue_bulk<STAGE>(m, a, nx, Bn, CS2, ES2, &bar[buf ^ 1]);
+            if (tid == 0) issue_bulk<STAGE>(m, a, nx, Bn, CS2, ES2, &bar[bn]);
             load_indices(t, nx, tid, hx, fx);              // consumed after this tile's compute
         }
         const TileBuf<STAGE> bc(buf0 + buf * BUF, CS2, ES2, cur);
@@ -502,6 +520,7 @@ __global__ void __launch_bounds__(NTHR, FBLTS_TILE_MINB) k_stage_tiled(DevMesh m
             if (!(v > 0.0)) report(err, a.kind, a.k, i, v);
         }
         if (more) issue_indexed<STAGE>(m, a, nx, TileBuf<STAGE>(Bn, CS2, ES2, nx), tid, hx, fx);
+        cp_async_commit();
     }
 }
 
@@ -986,7 +1005,7 @@ int stage_tiled_smem_bytes_host(int stage, int hmax, int emax) {
     const int nca = stage == 4 ? 4 : (stage > 1 ? 3 : 1), nea = stage > 1 ? 4 : 2;
     int CS2, ES2;
     tile_strides(hmax, emax, CS2, ES2);
-    return 8 * (2 + 2 * (nca * CS2 + nea * ES2 + ES2 / 2 + 2));
+    return 8 * (((NBUF + 1) & ~1) + NBUF * (nca * CS2 + nea * ES2 + ES2 / 2 + 2));
 }
 
 int stage_tiled_configure(const DevMesh &m) {
