@@ -142,8 +142,17 @@ def predict_stage(co, x_new, x_stage, x_n):
     return co["a"] * x_new + co["b"] * x_stage + co["c"] * x_n
 
 
-def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper"):
+def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper", slow_refresh=False):
     """One FB-LTS coarse step in split mode, literal (P:L551-787 inside P:L1548-1561).
+
+    slow_refresh=True: the variant the paper proposes to lift the splitting's coarse-step cap
+    (SURVEY 8(f) N2): "calculate the slow tendencies at times t^{n,k} for
+    k = 0, ..., M-1 and use these values while advancing on fine cells".  Reading:
+    S^k = Phi^slow(u^{n,k}, h^{n,k}) on F_E, its stencil (edges F_E u IF-1_E, cells F u IF-1 u IF-2)
+    taking the fine data on F / F_E and the level-k prediction (eq. pred_old) on IF-1 / IF-1_E and
+    on IF-2 (the same formula from the tilde coarse data); S^k replaces S in the three fine
+    velocity stages on F_E; everything on C (coarse stages, predictions, correction summands)
+    keeps the frozen S.
 
     extents="paper": the shrinking F^5/F^4/F^3/F^2/F^1 extents of P:L557-661.
     extents="all_fine": the MPAS simplification of P:L1284-1286 (every coarse
@@ -238,6 +247,16 @@ def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper"):
         def eview(fine, pred, coarse):
             return np.where(F_E, fine, np.where(IF1_E, pred, coarse))
 
+        if slow_refresh:
+            # S^k on F_E from the state at t^{n,k} (NaN outside the stencil region poisons misuse)
+            Hk = np.where(F, hk, np.where(IF1 | IF2, predict_level(co, h3, h, k), np.nan))
+            Uk = np.where(F_E, uk, np.where(IF1_E, uP0, np.nan))
+            Sk = nan_e()
+            with np.errstate(invalid="ignore"):
+                Sk[F_E] = trisk.slow_tendency(mesh, Uk, Hk, phys)[F_E]
+        else:
+            Sk = S
+
         hk1, hsk1, hk2, hsk2, hkn, hs3k = nan_c(), nan_c(), nan_c(), nan_c(), nan_c(), nan_c()
         uk1, uk2, ukn = nan_e(), nan_e(), nan_e()
         H0 = cview(hk, hP0, h)
@@ -247,7 +266,7 @@ def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper"):
         hsk1[i] = b1 * hk1[i] + omb1 * hk[i]
         HS1 = cview(hsk1, hsP1, hs1)
         e, phi = PhiF(HS1, F_E)
-        uk1[e] = uk[e] + c1f * (phi + S[e])
+        uk1[e] = uk[e] + c1f * (phi + Sk[e])
         U1 = eview(uk1, uP1, u1)
         H1 = cview(hk1, hP1, h1)
         i, psi = Psi(U1, H1, F)                                         # eq. fine_s2
@@ -255,7 +274,7 @@ def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper"):
         hsk2[i] = b2 * hk2[i] + omb2 * hk[i]
         HS2 = cview(hsk2, hsP2, hs2)
         e, phi = PhiF(HS2, F_E)
-        uk2[e] = uk[e] + c2f * (phi + S[e])
+        uk2[e] = uk[e] + c2f * (phi + Sk[e])
         U2 = eview(uk2, uP2, u2)
         H2 = cview(hk2, hP2, h2)
         i, psi = Psi(U2, H2, IFc)                                       # correction summand (eq. if_correction)
@@ -265,7 +284,7 @@ def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper"):
         hs3k[i] = b3 * hkn[i] + om2b3 * hk2[i] + b3 * hk[i]
         HS3 = cview(hs3k, hsP3, hs3)
         e, phi = PhiF(HS3, F_E)
-        ukn[e] = uk[e] + c3f * (phi + S[e])
+        ukn[e] = uk[e] + c3f * (phi + Sk[e])
         e, phi = PhiF(HS3, IFe)                                         # correction summand (eq. if_correction)
         accU[e] = accU[e] + (phi + S[e])
         hk, uk = hkn, ukn
@@ -279,7 +298,7 @@ def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper"):
     return h_new, u_new
 
 
-def run(mesh, lab, h, u, dt, M, phys, n_steps, extents="paper"):
+def run(mesh, lab, h, u, dt, M, phys, n_steps, extents="paper", slow_refresh=False):
     for _ in range(n_steps):
-        h, u = fblts_step(mesh, lab, h, u, dt, M, phys, extents)
+        h, u = fblts_step(mesh, lab, h, u, dt, M, phys, extents, slow_refresh=slow_refresh)
     return h, u
