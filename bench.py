@@ -92,6 +92,12 @@ def byte_model(counts, M, fused, maxE=6, maxE2=10):
     b["fine_s2"] = M * (cells(3, 8) * (slotC + 8 + 8 + 8 + 8 + 8 - 8) + edges(3, 8) * edge_s)
     b["fine_s3"] = M * (cells(1, 8) * (slotC + 8 + 8 + 8 + 8 + 8 - 8) + edges(1, 8) * edge_s)
     b["correct_if"] = cells(1, 2) * 24 + edges(1, 2) * 24
+    # slow-term refresh (k = 1..M-1): views (cells IF..F write h, edges IF-1_E..F_E write u), the
+    # restricted slow_pre (cells IF-1..F, edges IF-1_E..F_E, vertices ~2 per cell) and slow_edge on F_E
+    Vf = 2 * cells(2, 8)
+    b["slow_refresh"] = (M - 1) * (cells(1, 8) * 24 + edges(2, 8) * 40
+                                   + Vf * 72 + cells(2, 8) * (4 + 4 * maxE + 16) + edges(2, 8) * 32
+                                   + edges(3, 8) * (4 + 12 * maxE2 + 48))
     if fused:
         band_s1 = fs1(3) - fs1(4)
         band_vel = fvel(1) - fvel(4)
@@ -260,7 +266,7 @@ def arm_native(args):
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     s = Solver(c.mesh, c.fine_mask, c.dt, c.M, g=c.g, beta=c.beta, rho0=c.rho0, slow=c.slow, tau_n=c.tau_n,
-               rank=rank, nranks=world, nccl_id=nccl_id)
+               rank=rank, nranks=world, nccl_id=nccl_id, slow_refresh=args.slow_refresh)
     s.set_state(c.h0, c.u0, 0.0)
     counts = s.counts()
     t_setup = time.perf_counter() - t_setup
@@ -400,7 +406,8 @@ def arm_native(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "scaling_note": "strong: the same config-5 mesh is partitioned over N GPUs (a weak-scaled 4096 x 4096N "
                         "mesh needs a distributed mesh upload, DESIGN.md section 7)" if world > 1 else None,
-        "config": {"workload": args.config, "cells": c.mesh.nCells, "edges": c.mesh.nEdges,
+        "config": {"workload": args.config, "slow_refresh": bool(args.slow_refresh),
+                   "cells": c.mesh.nCells, "edges": c.mesh.nEdges,
                    "vertices": c.mesh.nVertices, "M": c.M, "dt": c.dt,
                    "cells_by_region": counts["cells_by_region"],
                    "l2": "inputs larger than L2 (no flush needed)" if c.mesh.nCells > 2_000_000 else
@@ -435,6 +442,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-global", action="store_true", help="skip the global FB-RK(3,2) comparison run")
+    ap.add_argument("--slow-refresh", action="store_true",
+                    help="the slow-term refresh variant (S re-evaluated at every fine level, P:L1427-1431)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

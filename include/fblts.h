@@ -115,6 +115,9 @@ typedef struct {
                             no fine cells or M = 1); FBLTS_SCHEME_RK4 (1): classical four-stage RK4 on
                             the unsplit system, global (M and the fine mask ignored), one
                             rank -- the paper's reference scheme, for speedup comparisons */
+    int32_t slow_refresh;/* 1: the paper's proposed variant: the slow tendency is
+                            re-evaluated at every fine level t^{n,k} and used on the fine edges
+                            (DESIGN.md 3 for the reading); FB-LTS scheme, one rank.  0: frozen S */
 } fblts_config;
 
 #define FBLTS_SCHEME_FBLTS 0

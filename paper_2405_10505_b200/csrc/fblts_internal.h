@@ -21,7 +21,7 @@ namespace fblts {
 
 enum KernelKind {
     K_SLOW_PRE = 0, K_SLOW_EDGE, K_COARSE_S1, K_COARSE_S2, K_COARSE_S3, K_COARSE_VEL,
-    K_FINE_S1, K_FINE_S2, K_FINE_S3, K_FINE_VEL, K_CORRECT, K_FINE_VS1, K_RK4_STAGE, K_NUM
+    K_FINE_S1, K_FINE_S2, K_FINE_S3, K_FINE_VEL, K_CORRECT, K_FINE_VS1, K_RK4_STAGE, K_SLOW_REFRESH, K_NUM
 };
 
 // Region boundaries of one region-major block: [begin,if2) int, [if2,if1) IF-2,
@@ -133,6 +133,8 @@ struct DevState {
     double *K;                          // cells
     double *accH, *accU;                // accH indexed by owned cell (IF cells used), accU by e - eb.if2 (IF edges)
     double *rkU[2], *rkAccU;            // RK4 scheme: stage velocities (ping-pong) and the velocity sum
+    double *Sf;                         // slow tendency on F_E during the fine phase: S, or Sk (refresh)
+    double *Sk, *hv, *uv;               // slow-term refresh: S^k on F_E and the t^{n,k} views
     double *stage;                      // staging for set/get_state (max(nC, nE) doubles)
     int32_t *cellOld, *edgeOld;         // new -> old permutation (device)
     double *diag;                       // reduction scratch
@@ -166,6 +168,15 @@ int stage_tiled_configure(const DevMesh &m);      // sets the dynamic shared-mem
 // Kernel launchers (kernels.cu).  All enqueue on `s`.
 void launch_slow_pre(const DevMesh &m, const DevState &st, const double *h, const double *u, cudaStream_t s);
 void launch_slow_edge(const DevMesh &m, const DevState &st, const double *h, const StepConst &sc, cudaStream_t s);
+// restricted slow sweeps (vertices >= v0, cells >= c0, edges >= e0; S on edges [e0, e1) into out)
+void launch_slow_pre_range(const DevMesh &m, const DevState &st, const double *h, const double *u, int v0, int c0,
+                           int e0, cudaStream_t s);
+void launch_slow_edge_range(const DevMesh &m, const DevState &st, const double *h, double *out, int e0, int e1,
+                            const StepConst &sc, cudaStream_t s);
+// slow-term refresh views at t^{n,k} into st.hv (cells) and st.uv (edges)
+void launch_refresh_views(const DevMesh &m, const DevState &st, const double *hN, const double *hNew,
+                          const double *hk, const double *uN, const double *uk, const StepConst &sc,
+                          const PredConst &pc, cudaStream_t s);
 // cell launchers act on one owned cell block b (DevMesh::cb or DevMesh::cbI)
 void launch_coarse_s1(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
                       const StepConst &sc, cudaStream_t s, const Bounds &b);

@@ -24,7 +24,7 @@ namespace {
 
 const char *kKernelNames[K_NUM] = {"slow_pre",  "slow_edge", "coarse_s1", "coarse_s2", "coarse_s3", "coarse_vel",
                                    "fine_s1",   "fine_s2",   "fine_s3",   "fine_vel",  "correct_if", "fine_vel_s1",
-                                   "rk4_stage"};
+                                   "rk4_stage", "slow_refresh"};
 
 enum Phase { P_CREATED = 0, P_MESH, P_REGIONS, P_BOUND, P_STATE };
 
@@ -99,6 +99,7 @@ struct fblts_ctx {
     int t_sRow = 32, t_hmax = 0, t_emax = 0;
     size_t t_nHalo = 0, t_nFedge = 0, t_nEcl = 0;
     bool deep_runs_ok = false;
+    int vminF = 0;
     std::vector<int32_t> e_owner;          // local owner cell of every local edge (build_local)
     bool tiled = true;
     bool split = false;        // FBLTS_SPLIT=1: separate launches for the thin interface blocks
@@ -254,6 +255,7 @@ int fblts_create(fblts_ctx **out, const fblts_config *cfg) {
     if (cfg->nranks < 1 || cfg->nranks > 64 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return FBLTS_ERR_INVALID_ARG;
     if (cfg->scheme != FBLTS_SCHEME_FBLTS && cfg->scheme != FBLTS_SCHEME_RK4) return FBLTS_ERR_INVALID_ARG;
     if (cfg->scheme == FBLTS_SCHEME_RK4 && cfg->nranks != 1) return FBLTS_ERR_INVALID_ARG;   // reference scheme: one rank
+    if (cfg->slow_refresh && (cfg->nranks != 1 || cfg->scheme != FBLTS_SCHEME_FBLTS)) return FBLTS_ERR_INVALID_ARG;
     // No CUDA call here: mesh upload, labelling and renumbering are host work, so a context
     // can be created (and its labels inspected) on a machine without a GPU.
     fblts_ctx *c = new fblts_ctx();
@@ -677,6 +679,9 @@ int build_local(fblts_ctx *c, const std::vector<int32_t> &coc) {
     for (int v = 0; v < L.nV; ++v) L.vOwn[v] = part[m.cov[3 * L.vertGlob[v]]] == me;
     L.eOwn.assign(L.nE, 0);
     for (int e = 0; e < L.nOwnE; ++e) L.eOwn[e] = part[m.coe[2 * L.edgeGlob[e]]] == me;
+    c->vminF = L.nV;                          // first vertex of an F_E edge (slow-term refresh range)
+    for (int e = L.eb.f; e < L.nOwnE; ++e)
+        for (int k = 0; k < 2; ++k) c->vminF = std::min(c->vminF, vertLoc[m.voe[2 * L.edgeGlob[e] + k]]);
     c->have_fine = g.ccount[3] + g.ccount[4] + g.ccount[5] + g.ccount[6] + g.ccount[7] + g.ccount[8] > 0;   // global
     // ---- device tables in local numbering (dummy edge index nE for ring-2 slots outside the subdomain)
     c->sE = pad32(L.nE);
@@ -962,6 +967,11 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
     put(s.rkU[0], nrk);
     put(s.rkU[1], nrk);
     put(s.rkAccU, nrk);
+    const bool rf = c->cfg.slow_refresh != 0;
+    put(s.Sk, rf ? nE1 : 1);
+    put(s.uv, rf ? nE1 : 1);
+    put(s.hv, rf ? (size_t)std::max(1, L.nC) : 1);
+    if (base) s.Sf = rf ? s.Sk : s.S;
     put(s.stage, std::max(m.nC, m.nE));
     put(s.cellOld, L.nC);
     put(s.edgeOld, L.nE);
@@ -1269,7 +1279,7 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
             launch_fine_s1(m, st, hN, hNew, hk, uk, sc, pred(k), k, s, B, !T);
             if (fused) {
                 cell_mark(K_FINE_VS1);
-                StageArgs va{k - 1 == 0 ? hN : hb(k - 2), hk, k - 1 == 0 ? uN : ub(k - 2), st.S, st.h1,
+                StageArgs va{k - 1 == 0 ? hN : hb(k - 2), hk, k - 1 == 0 ? uN : ub(k - 2), st.Sf, st.h1,
                              sc.c3f, sc.b3, sc.om2b3, sc.c1f, sc.g, K_FINE_VS1, k};
                 va.h2 = st.h2;
                 va.unew = ub(k - 1);
@@ -1279,18 +1289,32 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
             }
             *px = PhaseX{X_C1, st.h1, -1, nullptr};
         } else if (stg == 1) {
+            if (part == 0 && c->cfg.slow_refresh && c->cfg.slow) {
+                // S^k on F_E from the state at t^{n,k}; S^0 = S (identical views)
+                mark(K_SLOW_REFRESH);
+                if (k == 0) {
+                    if (m.eb.end > m.eb.f)
+                        cudaMemcpyAsync(st.Sk + m.eb.f, st.S + m.eb.f, (size_t)(m.eb.end - m.eb.f) * 8,
+                                        cudaMemcpyDeviceToDevice, s);
+                } else {
+                    launch_refresh_views(m, st, hN, hNew, hk, uN, uk, sc, pred(k), s);
+                    launch_slow_pre_range(m, st, st.hv, st.uv, c->vminF, m.cb.if1, m.eb.if1, s);
+                    launch_slow_edge_range(m, st, st.hv, st.Sk, m.eb.f, m.eb.end, sc, s);
+                }
+                any = true;
+            }
             cell_mark(K_FINE_S2);
             launch_fine_s2(m, st, hN, hNew, hk, uk, sc, pred(k), k, s, B, !T);
             if (T)
                 stage_tiled(c, 2, B, B.fl[1], B.end,
-                            StageArgs{hk, st.h1, uk, st.S, st.h2, sc.c1f, sc.b1, sc.omb1, sc.c2f, sc.g, K_FINE_S2, k}, s);
+                            StageArgs{hk, st.h1, uk, st.Sf, st.h2, sc.c1f, sc.b1, sc.omb1, sc.c2f, sc.g, K_FINE_S2, k}, s);
             *px = PhaseX{X_C1, st.h2, -1, nullptr};
         } else {
             cell_mark(K_FINE_S3);
             launch_fine_s3(m, st, hN, uN, hNew, hk, uk, hb(k), sc, pred(k), k, s, B, !T);
             if (T)
                 stage_tiled(c, 3, B, B.fl[1], B.end,
-                            StageArgs{hk, st.h2, uk, st.S, hb(k), sc.c2f, sc.b2, sc.omb2, sc.c3f, sc.g, K_FINE_S3, k}, s);
+                            StageArgs{hk, st.h2, uk, st.Sf, hb(k), sc.c2f, sc.b2, sc.omb2, sc.c3f, sc.g, K_FINE_S3, k}, s);
             *px = PhaseX{X_C1, hb(k), -1, nullptr};
         }
     } else {                                     // ph == 3 + nfine: last velocity sweep, correction

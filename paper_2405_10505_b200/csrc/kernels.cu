@@ -108,10 +108,10 @@ template <int G>
 __global__ void __launch_bounds__(TPB) k_slow_pre(DevMesh m, const double *__restrict__ h,
                                                   const double *__restrict__ u, double *__restrict__ q,
                                                   double *__restrict__ K, double *__restrict__ F,
-                                                  unsigned nbV, unsigned nbC) {
+                                                  unsigned nbV, unsigned nbC, int v0, int c0, int e0) {
     const unsigned b = blockIdx.x;
     if (b < nbV) {
-        const int v = b * TPB + threadIdx.x;
+        const int v = v0 + b * TPB + threadIdx.x;
         if (v >= m.nV) return;
         double circ = 0.0;
 #pragma unroll
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(TPB) k_slow_pre(DevMesh m, const double *__res
         hv = hv / A;
         q[v] = (zeta + m.fV[v]) / hv;
     } else if (b < nbV + nbC) {
-        const int i = (b - nbV) * TPB + threadIdx.x;
+        const int i = c0 + (b - nbV) * TPB + threadIdx.x;
         if (i >= m.nC) return;
         int2 r[G];
         load_row<G>(m, i, r);
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(TPB) k_slow_pre(DevMesh m, const double *__res
         }
         K[i] = acc / m.areaCell[i];
     } else {
-        const int e = (b - nbV - nbC) * TPB + threadIdx.x;
+        const int e = e0 + (b - nbV - nbC) * TPB + threadIdx.x;
         if (e >= m.nE) return;
         const int2 c = m.coe[e];
         F[e] = (0.5 * (h[c.x] + h[c.y])) * u[e];
@@ -164,9 +164,9 @@ template <int MAXE2>
 __global__ void __launch_bounds__(TPB, FBLTS_SLOW_MINB) k_slow_edge(DevMesh m, const double *__restrict__ h,
                                                    const double *__restrict__ q, const double *__restrict__ K,
                                                    const double *__restrict__ F, double *__restrict__ S,
-                                                   double rho0) {
-    const int e = blockIdx.x * TPB + threadIdx.x;
-    if (e >= m.nOwnE) return;
+                                                   double rho0, int e0, int e1) {
+    const int e = e0 + blockIdx.x * TPB + threadIdx.x;
+    if (e >= e1) return;
     const int n = m.nEoE[e];
     // F_perp = sum_j W_j F_eoe_j in slot order, gathered in chunks of CH slots (register budget)
     constexpr int CH = FBLTS_SLOW_CHUNK < MAXE2 ? FBLTS_SLOW_CHUNK : MAXE2;
@@ -554,6 +554,7 @@ __global__ void __launch_bounds__(TPB) k_coarse_vel(DevMesh m, const double *__r
 // cell and edge touched is fine, so the views reduce to the fine arrays.
 struct FineArrays {
     const double *hN, *h1, *h2, *h3, *hk;   // h3 = coarse stage-3 output (hNew before the correction)
+    const double *Sf;                       // slow tendency used on F_E (S, or S^k with the refresh)
 };
 
 __device__ __forceinline__ double pred_level(const PredConst &p, const FineArrays &a, int x) {
@@ -683,7 +684,7 @@ __global__ void __launch_bounds__(TPB, BAND ? 1 : FBLTS_MINB) k_fine_s2(DevMesh 
             const double zbn = m.zb[nb];
             const double dc = m.dc[e];
             const double phi = pos ? phi_fast(sc.g, HSi, zbi, HSn, zbn, dc) : phi_fast(sc.g, HSn, zbn, HSi, zbi, dc);
-            const double ue = uk[e] + sc.c1f * (phi + S[e]);
+            const double ue = uk[e] + sc.c1f * (phi + a.Sf[e]);     // every edge of a fine cell is F_E
             acc = acc + psi_term(pos, Hi, Hn, ue, m.dv[e]);
         }
     }
@@ -729,7 +730,7 @@ __global__ void __launch_bounds__(TPB, BAND ? 1 : FBLTS_MINB) k_fine_s3(DevMesh 
             if (ec == 3) {
                 const double zbn = m.zb[nb];
                 const double phi = pos ? phi_fast(sc.g, HSi, zbi, HSn, zbn, dc) : phi_fast(sc.g, HSn, zbn, HSi, zbi, dc);
-                ue = uk[e] + sc.c2f * (phi + S[e]);
+                ue = uk[e] + sc.c2f * (phi + a.Sf[e]);
             } else {
                 const int c0 = pos ? i : nb, c1 = pos ? nb : i;
                 const double zb0 = m.zb[c0], zb1 = m.zb[c1];
@@ -772,7 +773,7 @@ __global__ void __launch_bounds__(TPB) k_fine_vel(DevMesh m, FineArrays a, const
     const double phi = phi_fast(sc.g, view3<BAND>(m, sc, p, a, hnext, c.x), m.zb[c.x],
                                 view3<BAND>(m, sc, p, a, hnext, c.y), m.zb[c.y], m.dc[e]);
     if (!BAND || e >= m.eb.f) {
-        unext[e] = uk[e] + sc.c3f * (phi + S[e]);
+        unext[e] = uk[e] + sc.c3f * (phi + a.Sf[e]);
     } else {
         const int ai = e - m.eb.if2;
         const double prev = k == 0 ? 0.0 : accU[ai];
@@ -1044,18 +1045,63 @@ void launch_stage_tiled(const DevMesh &m, int stage, int tile0, int tile1, int h
     });
 }
 
+// Views of the state at t^{n,k} for the slow-term refresh (reading DESIGN.md 3):
+// cells: F -> h^{n,k}, IF-1 / IF-2 -> (k/M) h~^{n+1} + (1 - k/M) h^n (eq. pred_old), others h^n;
+// edges: F_E -> u^{n,k}, IF-1_E -> (k/M) u~^{n+1} + (1 - k/M) u^n with u~^{n+1} recomputed as the
+// coarse velocity stage 3 does, others u^n (fillers outside the stencil of F_E).
+__global__ void __launch_bounds__(TPB) k_refresh_views(DevMesh m, FineArrays a, const double *__restrict__ uN,
+                                                       const double *__restrict__ uk, const double *__restrict__ S,
+                                                       double *__restrict__ hv, double *__restrict__ uv,
+                                                       StepConst sc, PredConst p, unsigned nbC) {
+    if (blockIdx.x < nbC) {
+        const int i = blockIdx.x * TPB + threadIdx.x;
+        if (i >= m.nOwnC) return;
+        const int cl = ccls(m, i);
+        const bool ifc = cl == 1 || (cl == 0 && i >= (i < m.nB ? m.cb.if2 : m.cbI.if2));
+        hv[i] = cl == 2 ? a.hk[i] : (ifc ? pred_level(p, a, i) : a.hN[i]);
+    } else {
+        const int e = (blockIdx.x - nbC) * TPB + threadIdx.x;
+        if (e >= m.nOwnE) return;
+        const int ec = ecls(m.eb, e);
+        if (ec == 3) {
+            uv[e] = uk[e];
+        } else if (ec == 2) {
+            const int2 c = m.coe[e];
+            const double phi3 = phi_fast(sc.g, hs3c(sc, a.h3, a.h2, a.hN, c.x), m.zb[c.x], hs3c(sc, a.h3, a.h2, a.hN, c.y),
+                                         m.zb[c.y], m.dc[e]);
+            const double u3 = uN[e] + sc.c3 * (phi3 + S[e]);
+            uv[e] = p.a * u3 + p.oma * uN[e];
+        } else {
+            uv[e] = uN[e];
+        }
+    }
+}
+
+
+void launch_slow_pre_range(const DevMesh &m, const DevState &st, const double *h, const double *u, int v0, int c0,
+                           int e0, cudaStream_t s) {
+    const unsigned nbV = nblocks(std::max(0, m.nV - v0)), nbC = nblocks(std::max(0, m.nC - c0)),
+                   nbE = nblocks(std::max(0, m.nE - e0));
+    if (nbV + nbC + nbE == 0) return;
+    FBLTS_DISPATCH_G(m.ecS, k_slow_pre<G><<<nbV + nbC + nbE, TPB, 0, s>>>(m, h, u, st.q, st.K, st.F, nbV, nbC, v0, c0,
+                                                                           e0));
+}
 void launch_slow_pre(const DevMesh &m, const DevState &st, const double *h, const double *u, cudaStream_t s) {
-    const unsigned nbV = nblocks(m.nV), nbC = nblocks(m.nC), nbE = nblocks(m.nE);
-    FBLTS_DISPATCH_G(m.ecS, k_slow_pre<G><<<nbV + nbC + nbE, TPB, 0, s>>>(m, h, u, st.q, st.K, st.F, nbV, nbC));
+    launch_slow_pre_range(m, st, h, u, 0, 0, 0, s);
+}
+void launch_slow_edge_range(const DevMesh &m, const DevState &st, const double *h, double *out, int e0, int e1,
+                            const StepConst &sc, cudaStream_t s) {
+    if (e1 <= e0) return;
+    const unsigned nb = nblocks(e1 - e0);
+    if (m.maxE2 <= 10)
+        k_slow_edge<10><<<nb, TPB, 0, s>>>(m, h, st.q, st.K, st.F, out, sc.rho0, e0, e1);
+    else if (m.maxE2 <= 14)
+        k_slow_edge<14><<<nb, TPB, 0, s>>>(m, h, st.q, st.K, st.F, out, sc.rho0, e0, e1);
+    else
+        k_slow_edge<30><<<nb, TPB, 0, s>>>(m, h, st.q, st.K, st.F, out, sc.rho0, e0, e1);
 }
 void launch_slow_edge(const DevMesh &m, const DevState &st, const double *h, const StepConst &sc, cudaStream_t s) {
-    if (m.nOwnE <= 0) return;
-    if (m.maxE2 <= 10)
-        k_slow_edge<10><<<nblocks(m.nOwnE), TPB, 0, s>>>(m, h, st.q, st.K, st.F, st.S, sc.rho0);
-    else if (m.maxE2 <= 14)
-        k_slow_edge<14><<<nblocks(m.nOwnE), TPB, 0, s>>>(m, h, st.q, st.K, st.F, st.S, sc.rho0);
-    else
-        k_slow_edge<30><<<nblocks(m.nOwnE), TPB, 0, s>>>(m, h, st.q, st.K, st.F, st.S, sc.rho0);
+    launch_slow_edge_range(m, st, h, st.S, 0, m.nOwnE, sc, s);
 }
 void launch_coarse_s1(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
                       const StepConst &sc, cudaStream_t s, const Bounds &b) {
@@ -1085,12 +1131,21 @@ void launch_coarse_vel(const DevMesh &m, const DevState &st, const double *hN, c
 }
 static FineArrays fine_arrays(const DevState &st, const double *hN, const double *hNew, const double *hk) {
     FineArrays a;
+    a.Sf = st.Sf;
     a.hN = hN;
     a.h1 = st.h1;
     a.h2 = st.h2;
     a.h3 = hNew;
     a.hk = hk;
     return a;
+}
+
+void launch_refresh_views(const DevMesh &m, const DevState &st, const double *hN, const double *hNew,
+                          const double *hk, const double *uN, const double *uk, const StepConst &sc,
+                          const PredConst &pc, cudaStream_t s) {
+    const FineArrays a = fine_arrays(st, hN, hNew, hk);
+    const unsigned nbC = nblocks(m.nOwnC), nbE = nblocks(m.nOwnE);
+    k_refresh_views<<<nbC + nbE, TPB, 0, s>>>(m, a, uN, uk, st.S, st.hv, st.uv, sc, pc, nbC);
 }
 // Fine kernels: BAND instance over [b0, b1) (needs the region views), DEEP over [b1, end).
 void launch_fine_s1(const DevMesh &m, const DevState &st, const double *hN, const double *hNew, const double *hk,

@@ -376,3 +376,20 @@ def test_rk4_with_forcing_matches_oracle(Solver):
     hg, ug, _ = s.state()
     s.close()
     assert np.array_equal(hg, h) and np.array_equal(ug, u)
+
+
+@pytest.mark.parametrize("which,M", [("config1", 4), ("shelf", 2), ("shelf", 3)])
+def test_slow_refresh_matches_oracle(Solver, which, M):
+    """The slow-term refresh variant: S^k re-evaluated at every fine
+    level on F_E through the C ABI equals the oracle's fblts_step(slow_refresh=True), 50 steps."""
+    c = configs.config1() if which == "config1" else configs.small_shelf(nx=64, ny=48, seed=5, dt=25.0)
+    lab = lts.label_regions(c.mesh, c.fine_mask)
+    ho, uo = lts.run(c.mesh, lab, c.h0, c.u0, c.dt, M, phys_of(c), 50, slow_refresh=True)
+    s = Solver(c.mesh, c.fine_mask, c.dt, M, g=c.g, beta=c.beta, rho0=c.rho0, slow=c.slow, tau_n=c.tau_n,
+               slow_refresh=True)
+    s.set_state(c.h0, c.u0)
+    s.step(50)
+    hg, ug, _ = s.state()
+    s.close()
+    eh, eu = assert_parity(hg, ug, ho, uo)
+    print(f"refresh {which} M={M}: eps_h={eh:.3e} eps_u={eu:.3e} bitwise={np.array_equal(hg, ho) and np.array_equal(ug, uo)}")
