@@ -269,3 +269,43 @@ def config4(seed=4, dt=None, dx_scale=1.0, n_lloyd=50, M=8, n_steps=100, verbose
         dt = 0.9 * nu / np.max(ce)
     return Case(name="config4", mesh=mesh, h0=H + eta, u0=np.zeros(mesh.nEdges), fine_mask=fine,
                 tau_n=np.zeros(mesh.nEdges), M=M, dt=dt, n_steps=n_steps, seed=seed)
+
+
+CD_BOTTOM = 2.5e-3            # bottom-drag coefficient C_D (synthetic hurricane runs, N4)
+CW_WIND = 1.225 / 1000.0 * 1.5e-3   # C_W = (rho_air / rho_0) C_d10 (constant-drag reading, N4)
+
+
+def hurricane_wind(mesh, centre, vmax=40.0, rmax=40e3, alpha=0.5, inflow_deg=20.0):
+    """Synthetic stationary hurricane wind u_W (no Sandy data): a Rankine-type
+    vortex, azimuthal speed V(r) = vmax r / rmax inside rmax and vmax (rmax / r)^alpha outside,
+    counter-clockwise (northern hemisphere), turned inward by inflow_deg.  Returns the per-edge
+    normal and tangential components (u_W . n_e, u_W . t_e) at the edge points; planar periodic
+    meshes use the minimum-image displacement from the centre.  INPUT GENERATION ONLY."""
+    p = mesh.edgePoint[:, :2]
+    d = p - np.asarray(centre)[None, :2]
+    if mesh.kind == "planar":
+        d[:, 0] -= mesh.Lx * np.round(d[:, 0] / mesh.Lx)
+        d[:, 1] -= mesh.Ly * np.round(d[:, 1] / mesh.Ly)
+    r = np.hypot(d[:, 0], d[:, 1])
+    V = np.where(r < rmax, vmax * r / rmax, vmax * (rmax / np.maximum(r, 1e-9)) ** alpha)
+    er = d / np.maximum(r, 1e-9)[:, None]
+    eth = np.stack([-er[:, 1], er[:, 0]], axis=1)
+    a = np.deg2rad(inflow_deg)
+    w = V[:, None] * (np.cos(a) * eth - np.sin(a) * er)
+    n = mesh.edgeNormal[:, :2]
+    t = np.stack([-n[:, 1], n[:, 0]], axis=1)          # t_e = k x n_e
+    return np.sum(w * n, axis=1), np.sum(w * t, axis=1)
+
+
+def hurricane_case(seed=8, nx=64, ny=48, dt=25.0, sal=0.1, **kw) -> Case:
+    """The reduced shelf case driven by a synthetic stationary hurricane over the shelf break:
+    bottom drag C_D, wind C_W |u_W - u| (u_W - u) / h, SAL coefficient sal in the fast term
+    (eq. hurricane_model / hurricane_fast_terms).  Case.hurricane holds the terms."""
+    c = small_shelf(seed=seed, nx=nx, ny=ny, dt=dt, **kw)
+    rng = np.random.default_rng(seed + 100)
+    centre = (0.5 * c.mesh.Lx + rng.uniform(-0.1, 0.1) * c.mesh.Lx, rng.uniform(0.3, 0.7) * c.mesh.Ly)
+    rmax = 0.06 * c.mesh.Lx
+    uw_n, uw_t = hurricane_wind(c.mesh, centre, rmax=rmax)
+    c.tau_n = np.zeros(c.mesh.nEdges)
+    c.hurricane = {"sal": sal, "cd": CD_BOTTOM, "cw": CW_WIND, "uw_n": uw_n, "uw_t": uw_t}
+    return c

@@ -19,12 +19,29 @@ class Phys:
     slow terms are on (False = gravity-wave model, P:L801-813, P:L1585);
     tau_n: per-edge wind-stress projection tau . n_e (N m^-2, reading Q19);
     rho0: reference density (kg m^-3).
+    Hurricane-model terms (eq. hurricane_model, synthetic forcing):
+    sal: self-attraction-and-loading coefficient beta of the fast term -g grad(xi - beta xi)
+    (eq. hurricane_fast_terms, P:L1222-1230), evaluated with g_fast = g (1 - sal);
+    cd: bottom-drag coefficient C_D; cw: wind coefficient C_W; uw_n, uw_t: per-edge normal and
+    tangential components of the wind velocity u_W (None: no drag / wind terms).
     """
     g: float = 9.81
     beta: tuple = BETA_PAPER
     slow: bool = True
     tau_n: np.ndarray | None = None
     rho0: float = 1000.0
+    sal: float = 0.0
+    cd: float = 0.0
+    cw: float = 0.0
+    uw_n: np.ndarray | None = None
+    uw_t: np.ndarray | None = None
+
+    def g_fast(self):
+        """g (1 - beta_SAL): the gravity of the fast term -g grad(xi - beta xi)."""
+        return self.g * (1.0 - self.sal)
+
+    def hurricane(self):
+        return self.uw_n is not None
 
     def with_tau(self, mesh):
         if self.tau_n is None:
@@ -79,13 +96,13 @@ def mesh_tendencies(mesh, phys, S=None):
 
     if S is not None:
         def Phi(u, h):
-            return trisk.fast_momentum(mesh, h, phys.g, edges) + S
+            return trisk.fast_momentum(mesh, h, phys.g_fast(), edges) + S
     else:
         def Phi(u, h):
-            f = trisk.fast_momentum(mesh, h, phys.g, edges)
+            f = trisk.fast_momentum(mesh, h, phys.g_fast(), edges)
             if not phys.slow:
                 return f + np.zeros(mesh.nEdges)
-            return f + trisk.slow_momentum(mesh, u, h, phys.tau_n, phys.rho0)
+            return f + trisk.slow_momentum(mesh, u, h, phys.tau_n, phys.rho0, phys)
     return Phi, Psi
 
 

@@ -162,7 +162,7 @@ def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper", slow_refresh=False
     Returns (h^{n+1}, u^{n+1}).
     """
     nC, nE = mesh.nCells, mesh.nEdges
-    g = phys.g
+    g = phys.g_fast()
     b1, b2, b3 = phys.beta
     omb1, omb2, om2b3 = 1.0 - b1, 1.0 - b2, 1.0 - 2.0 * b3
     c1, c2, c3 = dt / 3.0, dt / 2.0, dt

@@ -139,7 +139,29 @@ def kinetic_energy(mesh, U):
     return acc / mesh.areaCell
 
 
-def slow_momentum(mesh, U, H, tau_n, rho0):
+def tangential_velocity(mesh, U):
+    """v_e = sum_j W_{e,j} u_{eoe_j}: the TRiSK reconstruction of the velocity along +t_e with the
+    same weightsOnEdge as F_perp (Thuburn et al. 2009; exact for uniform flow on the regular hex,
+    pin P7), sequential in slot order from +0.0 (hurricane drag / wind terms, reading in DESIGN.md)."""
+    return perp_flux(mesh, U, np.arange(mesh.nEdges))
+
+
+def hurricane_terms(mesh, U, h_e, phys):
+    """Bottom drag and wind terms of eq. hurricane_model on every edge:
+        D_e = C_D |u|_e u_e / h_e,   W_e = C_W |u_W - u|_e (u_W,n - u_e) / h_e,
+    |u|_e = sqrt(u_e^2 + v_e^2), |u_W - u|_e = sqrt((u_W,n - u_e)^2 + (u_W,t - v_e)^2),
+    v_e the tangential reconstruction; returns (D, W) (the slow tendency subtracts D, adds W)."""
+    v = tangential_velocity(mesh, U)
+    speed = np.sqrt(U * U + v * v)
+    D = phys.cd * speed * U / h_e
+    dn = phys.uw_n - U
+    dt = phys.uw_t - v
+    ws = np.sqrt(dn * dn + dt * dt)
+    W = phys.cw * ws * dn / h_e
+    return D, W
+
+
+def slow_momentum(mesh, U, H, tau_n, rho0, phys=None):
     """Phi^slow_e(u, h) on every edge: the non-gravity-wave momentum terms.
 
     Split per P:L1548-1561 (the fast part is only -g grad(h + z_b)).  From
@@ -162,7 +184,11 @@ def slow_momentum(mesh, U, H, tau_n, rho0):
     c1 = mesh.cellsOnEdge[:, 1]
     h_e = 0.5 * (H[c0] + H[c1])
     G = tau_n / (rho0 * h_e)
-    return q_hat * Fperp - (K[c1] - K[c0]) / mesh.dcEdge + G
+    S = q_hat * Fperp - (K[c1] - K[c0]) / mesh.dcEdge + G
+    if phys is not None and phys.hurricane():
+        D, W = hurricane_terms(mesh, U, h_e, phys)
+        S = S - D + W
+    return S
 
 
 def slow_tendency(mesh, U, H, phys):
@@ -173,4 +199,4 @@ def slow_tendency(mesh, U, H, phys):
     """
     if not phys.slow:
         return np.zeros(mesh.nEdges)
-    return slow_momentum(mesh, U, H, phys.tau_n, phys.rho0)
+    return slow_momentum(mesh, U, H, phys.tau_n, phys.rho0, phys)
