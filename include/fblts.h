@@ -118,6 +118,9 @@ typedef struct {
     int32_t slow_refresh;/* 1: the paper's proposed variant: the slow tendency is
                             re-evaluated at every fine level t^{n,k} and used on the fine edges
                             (DESIGN.md 3 for the reading); FB-LTS scheme, one rank.  0: frozen S */
+    double  sal_beta;    /* self-attraction-and-loading coefficient beta of the hurricane model's fast
+                            term -g grad(xi - beta xi) (eq. hurricane_fast_terms),
+                            0 <= beta < 1; the fast term uses g (1 - beta).  0: plain model */
 } fblts_config;
 
 #define FBLTS_SCHEME_FBLTS 0
@@ -168,6 +171,15 @@ int fblts_bind_workspace(fblts_ctx *ctx, void *device_ptr, size_t bytes);
 /* Per-edge wind-stress projection tau . n_e [nEdges] (N m^-2), original order;
  * NULL = no forcing.  The slow term adds G_e = tau_n / (rho0 h_e^n) (reading Q19). */
 int fblts_set_forcing(fblts_ctx *ctx, const double *tau_n);
+
+/* Hurricane-model momentum terms in the slow tendency (eq. hurricane_model; SURVEY
+ * 8(f) N4 with a synthetic wind): bottom drag -C_D |u|_e u_e / h_e and wind
+ * +C_W |u_W - u|_e (u_W.n_e - u_e) / h_e, |u|_e from u_e and the tangential reconstruction
+ * v_e = sum_j weightsOnEdge[e][j] u[edgesOnEdge[e][j]], h_e = (h_c0 + h_c1) / 2.  uw_n / uw_t: host
+ * arrays [nEdges] (original order) of the wind's normal and tangential components, copied; both
+ * NULL switches the terms off.  cd, cw: finite, >= 0.  Frozen with the rest of the slow tendency
+ * (S at t^n).  Errors: INVALID_ARG (non-finite wind or coefficients), ORDER (before bind), CUDA. */
+int fblts_set_hurricane(fblts_ctx *ctx, const double *uw_n, const double *uw_t, double cd, double cw);
 
 /* Initial state, HOST arrays in original order: h [nCells] (m), u [nEdges] (m/s), t (s).
  * Errors: STATE (h <= 0 or non-finite at index i), ORDER. */

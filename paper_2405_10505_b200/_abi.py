@@ -44,7 +44,7 @@ class fblts_config(C.Structure):
     _fields_ = [("dt", C.c_double), ("g", C.c_double), ("beta", C.c_double * 3), ("rho0", C.c_double),
                 ("M", C.c_int32), ("r", C.c_int32), ("slow", C.c_int32), ("device", C.c_int32),
                 ("stream", C.c_void_p), ("rank", C.c_int32), ("nranks", C.c_int32), ("nccl_id", C.c_void_p),
-                ("scheme", C.c_int32), ("slow_refresh", C.c_int32)]
+                ("scheme", C.c_int32), ("slow_refresh", C.c_int32), ("sal_beta", C.c_double)]
 
 SCHEMES = {"fblts": 0, "rk4": 1}
 
@@ -71,6 +71,7 @@ _lib_counts = _sig("fblts_get_counts", C.c_int, _vp, C.POINTER(C.c_int64))
 _lib_wsize = _sig("fblts_workspace_size", C.c_int, _vp, C.POINTER(C.c_size_t))
 _lib_bind = _sig("fblts_bind_workspace", C.c_int, _vp, _vp, C.c_size_t)
 _lib_forcing = _sig("fblts_set_forcing", C.c_int, _vp, _f64p)
+_lib_hurricane = _sig("fblts_set_hurricane", C.c_int, _vp, _f64p, _f64p, C.c_double, C.c_double)
 _lib_set_state = _sig("fblts_set_state", C.c_int, _vp, _f64p, _f64p, C.c_double)
 _lib_step = _sig("fblts_step", C.c_int, _vp, C.c_int32)
 _lib_sync = _sig("fblts_sync", C.c_int, _vp)
@@ -88,7 +89,7 @@ _lib_diag_group = _sig("fblts_diagnostics_group", C.c_int, C.POINTER(_vp), C.c_i
 
 EXPORTED = ["fblts_create", "fblts_upload_mesh", "fblts_set_regions", "fblts_get_labels", "fblts_get_counts",
             "fblts_get_halo", "fblts_nccl_unique_id", "fblts_workspace_size", "fblts_bind_workspace",
-            "fblts_set_forcing", "fblts_set_state", "fblts_step", "fblts_step_group", "fblts_diagnostics_group",
+            "fblts_set_forcing", "fblts_set_hurricane", "fblts_set_state", "fblts_step", "fblts_step_group", "fblts_diagnostics_group",
             "fblts_sync", "fblts_get_state", "fblts_diagnostics", "fblts_profile", "fblts_kernel_name",
             "fblts_last_error", "fblts_destroy"]
 
@@ -109,13 +110,13 @@ def _arr(a, dtype):
 
 # ------------------------------------------------------------------ entry points
 def fblts_create(dt, M, g=9.81, beta=(0.531, 0.531, 0.313), rho0=1000.0, r=2, slow=True, device=0,
-                 stream=None, rank=0, nranks=1, nccl_id=None, scheme="fblts", slow_refresh=False):
+                 stream=None, rank=0, nranks=1, nccl_id=None, scheme="fblts", slow_refresh=False, sal=0.0):
     """nccl_id: 128 bytes from fblts_nccl_unique_id() on rank 0 (None: single rank or loopback group)."""
     idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id is not None else None
     cfg = fblts_config(dt=float(dt), g=float(g), beta=(C.c_double * 3)(*beta), rho0=float(rho0), M=int(M),
                        r=int(r), slow=1 if slow else 0, device=int(device), stream=stream, rank=int(rank),
                        nranks=int(nranks), nccl_id=C.cast(idbuf, C.c_void_p) if idbuf is not None else None,
-                       scheme=SCHEMES[scheme], slow_refresh=1 if slow_refresh else 0)
+                       scheme=SCHEMES[scheme], slow_refresh=1 if slow_refresh else 0, sal_beta=float(sal))
     ctx = _vp()
     rc = _lib_create(C.byref(ctx), C.byref(cfg))
     if rc != FBLTS_OK:
@@ -205,6 +206,15 @@ def fblts_set_forcing(ctx, tau_n):
     else:
         a = _arr(tau_n, np.float64)
         _check(ctx, _lib_forcing(ctx, _ptr(a, C.c_double)))
+
+
+def fblts_set_hurricane(ctx, uw_n, uw_t, cd, cw):
+    """Hurricane drag / wind terms (None winds: off); see include/fblts.h."""
+    if uw_n is None or uw_t is None:
+        _check(ctx, _lib_hurricane(ctx, None, None, 0.0, 0.0))
+    else:
+        a, b = _arr(uw_n, np.float64), _arr(uw_t, np.float64)
+        _check(ctx, _lib_hurricane(ctx, _ptr(a, C.c_double), _ptr(b, C.c_double), float(cd), float(cw)))
 
 
 def _host_ptr(x):

@@ -82,6 +82,8 @@ struct DevMesh {
     const int32_t *__restrict__ eoe;   // [maxE2][strideE]
     const double *__restrict__ W;      // [maxE2][strideE]
     const double *__restrict__ tau;    // [nE] tau . n_e
+    const double *__restrict__ uwn;    // [nE] wind u_W . n_e   (hurricane terms)
+    const double *__restrict__ uwt;    // [nE] wind u_W . t_e
     const int32_t *__restrict__ eov;   // [3][strideV] sign-encoded
     const int32_t *__restrict__ cov;   // [3][strideV]
     const double *__restrict__ kite;   // [3][strideV]
@@ -112,11 +114,13 @@ struct DevError {
 // Scalars of one coarse step, computed once on the host in double exactly as
 // the oracle does (SURVEY c.1 canonical constants).
 struct StepConst {
-    double g, rho0;
+    double g, rho0;                 // g = gravity of the fast term, g (1 - beta_SAL)
     double b1, b2, b3, omb1, omb2, om2b3;
     double c1, c2, c3;        // dt/3, dt/2, dt
     double c1f, c2f, c3f;     // dt/(3M), dt/(2M), dt/M
     int32_t M;
+    int32_t hur;              // hurricane drag / wind terms in the slow tendency (fblts_set_hurricane)
+    double cd, cw;            // C_D, C_W
 };
 
 // Prediction coefficients for subcycle k (eq. preds): a = k/M, oma = 1 - a,
@@ -167,12 +171,13 @@ int stage_tiled_configure(const DevMesh &m);      // sets the dynamic shared-mem
 
 // Kernel launchers (kernels.cu).  All enqueue on `s`.
 void launch_slow_pre(const DevMesh &m, const DevState &st, const double *h, const double *u, cudaStream_t s);
-void launch_slow_edge(const DevMesh &m, const DevState &st, const double *h, const StepConst &sc, cudaStream_t s);
+void launch_slow_edge(const DevMesh &m, const DevState &st, const double *h, const double *u, const StepConst &sc,
+                      cudaStream_t s);
 // restricted slow sweeps (vertices >= v0, cells >= c0, edges >= e0; S on edges [e0, e1) into out)
 void launch_slow_pre_range(const DevMesh &m, const DevState &st, const double *h, const double *u, int v0, int c0,
                            int e0, cudaStream_t s);
-void launch_slow_edge_range(const DevMesh &m, const DevState &st, const double *h, double *out, int e0, int e1,
-                            const StepConst &sc, cudaStream_t s);
+void launch_slow_edge_range(const DevMesh &m, const DevState &st, const double *h, const double *u, double *out,
+                            int e0, int e1, const StepConst &sc, cudaStream_t s);
 // slow-term refresh views at t^{n,k} into st.hv (cells) and st.uv (edges)
 void launch_refresh_views(const DevMesh &m, const DevState &st, const double *hN, const double *hNew,
                           const double *hk, const double *uN, const double *uk, const StepConst &sc,

@@ -252,6 +252,7 @@ int fblts_create(fblts_ctx **out, const fblts_config *cfg) {
     *out = nullptr;
     if (!(cfg->dt > 0.0) || cfg->M < 1 || cfg->r < 1 || !(cfg->g > 0.0) || !(cfg->rho0 > 0.0))
         return FBLTS_ERR_INVALID_ARG;
+    if (!(cfg->sal_beta >= 0.0 && cfg->sal_beta < 1.0)) return FBLTS_ERR_INVALID_ARG;
     if (cfg->nranks < 1 || cfg->nranks > 64 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return FBLTS_ERR_INVALID_ARG;
     if (cfg->scheme != FBLTS_SCHEME_FBLTS && cfg->scheme != FBLTS_SCHEME_RK4) return FBLTS_ERR_INVALID_ARG;
     if (cfg->scheme == FBLTS_SCHEME_RK4 && cfg->nranks != 1) return FBLTS_ERR_INVALID_ARG;   // reference scheme: one rank
@@ -272,7 +273,7 @@ int fblts_create(fblts_ctx **out, const fblts_config *cfg) {
     StepConst &s = c->sc;
     const double dt = cfg->dt;
     const double M = (double)cfg->M;
-    s.g = cfg->g;
+    s.g = cfg->g * (1.0 - cfg->sal_beta);      // fast term -g grad(xi - beta xi)
     s.rho0 = cfg->rho0;
     s.b1 = cfg->beta[0];
     s.b2 = cfg->beta[1];
@@ -938,6 +939,9 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
     put(dv, nE1);
     put(dc, nE1);
     put(tau, L.nE);
+    double *uwn, *uwt;
+    put(uwn, L.nE);
+    put(uwt, L.nE);
     put(nEoE, L.nE);
     put(eoe, (size_t)m.maxE2 * c->sE);
     put(W, (size_t)m.maxE2 * c->sE);
@@ -1002,6 +1006,7 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
         d.maxE = m.maxE, d.maxE2 = m.maxE2, d.ecS = c->ecS;
         d.nEoC = nEoC, d.ec = ec, d.areaCell = area, d.zb = zb;
         d.coe = coe, d.voe = voe, d.dv = dv, d.dc = dc, d.nEoE = nEoE, d.eoe = eoe, d.W = W, d.tau = tau;
+        d.uwn = uwn, d.uwt = uwt;
         d.eov = eov, d.cov = cov, d.kite = kite, d.areaTri = areaTri, d.fV = fV;
         d.vOwn = vOwn, d.eOwn = eOwn;
         d.nB = L.nB, d.cb = L.cb, d.cbI = L.cbI, d.eb = L.eb, d.cbh = L.cbh;
@@ -1106,6 +1111,38 @@ int fblts_set_forcing(fblts_ctx *c, const double *tau_n) {
         }
     CUDA_TRY(c, cudaMemcpyAsync((void *)c->dm.tau, t.data(), (size_t)L.nE * 8, cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return FBLTS_OK;
+}
+
+int fblts_set_hurricane(fblts_ctx *c, const double *uw_n, const double *uw_t, double cd, double cw) {
+    if (!c) return FBLTS_ERR_INVALID_ARG;
+    if (c->phase < P_BOUND) return fail(c, FBLTS_ERR_ORDER, "set_hurricane: bind the workspace first");
+    if (!uw_n || !uw_t) {
+        c->sc.hur = 0;
+        c->sc.cd = c->sc.cw = 0.0;
+    } else {
+        if (!(std::isfinite(cd) && std::isfinite(cw) && cd >= 0.0 && cw >= 0.0))
+            return fail(c, FBLTS_ERR_INVALID_ARG, "set_hurricane: C_D, C_W must be finite and >= 0");
+        const Local &L = c->lo;
+        std::vector<double> a(L.nE), b(L.nE);
+        for (int e = 0; e < L.nE; ++e) {
+            a[e] = uw_n[L.edgeGlob[e]];
+            b[e] = uw_t[L.edgeGlob[e]];
+            if (!std::isfinite(a[e]) || !std::isfinite(b[e]))
+                return fail(c, FBLTS_ERR_INVALID_ARG, "set_hurricane: wind[%d] not finite", L.edgeGlob[e]);
+        }
+        CUDA_TRY(c, cudaMemcpyAsync((void *)c->dm.uwn, a.data(), (size_t)L.nE * 8, cudaMemcpyHostToDevice, c->stream));
+        CUDA_TRY(c, cudaMemcpyAsync((void *)c->dm.uwt, b.data(), (size_t)L.nE * 8, cudaMemcpyHostToDevice, c->stream));
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+        c->sc.hur = 1;
+        c->sc.cd = cd;
+        c->sc.cw = cw;
+    }
+    for (int p = 0; p < 2; ++p)               // the step graphs bake the constants: re-capture
+        if (c->exec[p]) {
+            cudaGraphExecDestroy(c->exec[p]);
+            c->exec[p] = nullptr;
+        }
     return FBLTS_OK;
 }
 
@@ -1236,7 +1273,7 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
             mark(K_SLOW_PRE);
             launch_slow_pre(m, st, hN, uN, s);
             mark(K_SLOW_EDGE);
-            launch_slow_edge(m, st, hN, sc, s);
+            launch_slow_edge(m, st, hN, uN, sc, s);
             any = true;
         }
         cell_mark(K_COARSE_S1);
@@ -1299,7 +1336,7 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
                 } else {
                     launch_refresh_views(m, st, hN, hNew, hk, uN, uk, sc, pred(k), s);
                     launch_slow_pre_range(m, st, st.hv, st.uv, c->vminF, m.cb.if1, m.eb.if1, s);
-                    launch_slow_edge_range(m, st, st.hv, st.Sk, m.eb.f, m.eb.end, sc, s);
+                    launch_slow_edge_range(m, st, st.hv, st.uv, st.Sk, m.eb.f, m.eb.end, sc, s);
                 }
                 any = true;
             }
@@ -1398,7 +1435,7 @@ int enqueue_rk4_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
             if (rec) rec->mark(K_SLOW_PRE, s);
             launch_slow_pre(m, st, hs, us, s);
             if (rec) rec->mark(K_SLOW_EDGE, s);
-            launch_slow_edge(m, st, hs, c->sc, s);
+            launch_slow_edge(m, st, hs, us, c->sc, s);
         }
         double *ho = stage < 4 ? hb[stage % 2] : hNew;
         double *uo = stage < 4 ? st.rkU[stage % 2] : uNew;

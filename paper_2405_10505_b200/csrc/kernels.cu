@@ -160,37 +160,54 @@ __global__ void __launch_bounds__(TPB) k_slow_pre(DevMesh m, const double *__res
 #ifndef FBLTS_SLOW_MINB
 #define FBLTS_SLOW_MINB 6
 #endif
-template <int MAXE2>
+template <int MAXE2, bool HUR>
 __global__ void __launch_bounds__(TPB, FBLTS_SLOW_MINB) k_slow_edge(DevMesh m, const double *__restrict__ h,
                                                    const double *__restrict__ q, const double *__restrict__ K,
-                                                   const double *__restrict__ F, double *__restrict__ S,
-                                                   double rho0, int e0, int e1) {
+                                                   const double *__restrict__ F, const double *__restrict__ u,
+                                                   double *__restrict__ S, double rho0, double cd, double cw,
+                                                   int e0, int e1) {
     const int e = e0 + blockIdx.x * TPB + threadIdx.x;
     if (e >= e1) return;
     const int n = m.nEoE[e];
-    // F_perp = sum_j W_j F_eoe_j in slot order, gathered in chunks of CH slots (register budget)
+    // F_perp = sum_j W_j F_eoe_j in slot order, gathered in chunks of CH slots (register budget);
+    // with the hurricane terms also v_e = sum_j W_j u_eoe_j (tangential reconstruction)
     constexpr int CH = FBLTS_SLOW_CHUNK < MAXE2 ? FBLTS_SLOW_CHUNK : MAXE2;
-    double fp = 0.0;
+    double fp = 0.0, vt = 0.0;
 #pragma unroll
     for (int j0 = 0; j0 < MAXE2; j0 += CH) {
-        double w[CH], f[CH];
+        double w[CH], f[CH], ut[HUR ? CH : 1];
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
             if (j0 + j < n && j0 + j < MAXE2) {
+                const int ee = m.eoe[(j0 + j) * m.strideE + e];
                 w[j] = m.W[(j0 + j) * m.strideE + e];
-                f[j] = F[m.eoe[(j0 + j) * m.strideE + e]];
+                f[j] = F[ee];
+                if (HUR) ut[HUR ? j : 0] = u[ee];
             }
         }
 #pragma unroll
         for (int j = 0; j < CH; ++j)
-            if (j0 + j < n && j0 + j < MAXE2) fp = fp + w[j] * f[j];
+            if (j0 + j < n && j0 + j < MAXE2) {
+                fp = fp + w[j] * f[j];
+                if (HUR) vt = vt + w[j] * ut[HUR ? j : 0];
+            }
     }
     const int2 v = m.voe[e];
     const int2 c = m.coe[e];
     const double qh = 0.5 * (q[v.x] + q[v.y]);
     const double he = 0.5 * (h[c.x] + h[c.y]);
     const double G = m.tau[e] / (rho0 * he);
-    S[e] = qh * fp - (K[c.y] - K[c.x]) / m.dc[e] + G;
+    double s = qh * fp - (K[c.y] - K[c.x]) / m.dc[e] + G;
+    if (HUR) {   // bottom drag and wind (eq. hurricane_model)
+        const double ue = u[e];
+        const double speed = sqrt(ue * ue + vt * vt);
+        const double D = cd * speed * ue / he;
+        const double dn = m.uwn[e] - ue, dt = m.uwt[e] - vt;
+        const double ws = sqrt(dn * dn + dt * dt);
+        const double Wd = cw * ws * dn / he;
+        s = s - D + Wd;
+    }
+    S[e] = s;
 }
 
 // ---------------------------------------------------------------- coarse stages
@@ -1089,19 +1106,28 @@ void launch_slow_pre_range(const DevMesh &m, const DevState &st, const double *h
 void launch_slow_pre(const DevMesh &m, const DevState &st, const double *h, const double *u, cudaStream_t s) {
     launch_slow_pre_range(m, st, h, u, 0, 0, 0, s);
 }
-void launch_slow_edge_range(const DevMesh &m, const DevState &st, const double *h, double *out, int e0, int e1,
-                            const StepConst &sc, cudaStream_t s) {
+void launch_slow_edge_range(const DevMesh &m, const DevState &st, const double *h, const double *u, double *out,
+                            int e0, int e1, const StepConst &sc, cudaStream_t s) {
     if (e1 <= e0) return;
     const unsigned nb = nblocks(e1 - e0);
+#define FBLTS_SLOW_EDGE(ME2)                                                                                     \
+    do {                                                                                                         \
+        if (sc.hur)                                                                                              \
+            k_slow_edge<ME2, true><<<nb, TPB, 0, s>>>(m, h, st.q, st.K, st.F, u, out, sc.rho0, sc.cd, sc.cw, e0, e1);  \
+        else                                                                                                     \
+            k_slow_edge<ME2, false><<<nb, TPB, 0, s>>>(m, h, st.q, st.K, st.F, u, out, sc.rho0, sc.cd, sc.cw, e0, e1); \
+    } while (0)
     if (m.maxE2 <= 10)
-        k_slow_edge<10><<<nb, TPB, 0, s>>>(m, h, st.q, st.K, st.F, out, sc.rho0, e0, e1);
+        FBLTS_SLOW_EDGE(10);
     else if (m.maxE2 <= 14)
-        k_slow_edge<14><<<nb, TPB, 0, s>>>(m, h, st.q, st.K, st.F, out, sc.rho0, e0, e1);
+        FBLTS_SLOW_EDGE(14);
     else
-        k_slow_edge<30><<<nb, TPB, 0, s>>>(m, h, st.q, st.K, st.F, out, sc.rho0, e0, e1);
+        FBLTS_SLOW_EDGE(30);
+#undef FBLTS_SLOW_EDGE
 }
-void launch_slow_edge(const DevMesh &m, const DevState &st, const double *h, const StepConst &sc, cudaStream_t s) {
-    launch_slow_edge_range(m, st, h, st.S, 0, m.nOwnE, sc, s);
+void launch_slow_edge(const DevMesh &m, const DevState &st, const double *h, const double *u, const StepConst &sc,
+                      cudaStream_t s) {
+    launch_slow_edge_range(m, st, h, u, st.S, 0, m.nOwnE, sc, s);
 }
 void launch_coarse_s1(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
                       const StepConst &sc, cudaStream_t s, const Bounds &b) {
