@@ -142,7 +142,7 @@ def predict_stage(co, x_new, x_stage, x_n):
     return co["a"] * x_new + co["b"] * x_stage + co["c"] * x_n
 
 
-def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper", slow_refresh=False):
+def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper", slow_refresh=False, split=True):
     """One FB-LTS coarse step in split mode, literal (P:L551-787 inside P:L1548-1561).
 
     slow_refresh=True: the variant the paper proposes to lift the splitting's coarse-step cap
@@ -153,6 +153,13 @@ def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper", slow_refresh=False
     on IF-2 (the same formula from the tilde coarse data); S^k replaces S in the three fine
     velocity stages on F_E; everything on C (coarse stages, predictions, correction summands)
     keeps the frozen S.
+
+    split=False: the unsplit FB-LTS of P:L468-787: every velocity update uses the
+    full Phi(U, HS) = Phi^fast(HS) + Phi^slow(U, HS) (reading Q16: the FB-averaged thickness for every
+    h-dependence), with U the stage's velocity views -- coarse: u^n, u~1, u~2 on the paper's extents
+    Y1 = C_E u F^4_E, Y2 = C_E u F^2_E, Y3 = IF-1_E u int_E (whose slow stencils stay inside
+    X1 = C u F^5, X2 = C u F^3, X3 = C u F^1); fine: U0, U1, U2 of the view table (P:L784-785);
+    correction summand Phi(U2, HS3) on the IF edges.
 
     extents="paper": the shrinking F^5/F^4/F^3/F^2/F^1 extents of P:L557-661.
     extents="all_fine": the MPAS simplification of P:L1284-1286 (every coarse
@@ -190,7 +197,14 @@ def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper", slow_refresh=False
         return idx, trisk.fast_momentum(mesh, H, g, idx)
 
     # ---------- slow terms at t^n, frozen for the whole coarse step ----------
-    S = trisk.slow_tendency(mesh, u, h, phys)
+    S = trisk.slow_tendency(mesh, u, h, phys) if split else None
+
+    def Slow(U, HS, mask):
+        """Phi^slow(U, HS) on the edges of mask (unsplit); NaN in the views poisons misuse."""
+        if not phys.slow:
+            return np.zeros(int(np.count_nonzero(mask)))
+        with np.errstate(invalid="ignore"):
+            return trisk.slow_momentum(mesh, U, HS, phys.tau_n, phys.rho0, phys)[mask]
 
     # ---------- Phase 1: Coarse Advancement (P:L553-680) ----------
     h1, hs1, h2, hs2, h3, hs3 = nan_c(), nan_c(), nan_c(), nan_c(), nan_c(), nan_c()
@@ -199,17 +213,17 @@ def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper", slow_refresh=False
     h1[i] = h[i] + c1 * psi
     hs1[i] = b1 * h1[i] + omb1 * h[i]
     e, phi = PhiF(hs1, Y1)                                   # velocity stage 1 (eq. if_u_s1 / coarse_u_s1)
-    u1[e] = u[e] + c1 * (phi + S[e])
+    u1[e] = u[e] + c1 * (phi + (S[e] if split else Slow(u, hs1, Y1)))
     i, psi = Psi(u1, h1, X2)                                 # thickness stage 2 (eq. if_h_s2 / coarse_h_s2)
     h2[i] = h[i] + c2 * psi
     hs2[i] = b2 * h2[i] + omb2 * h[i]
     e, phi = PhiF(hs2, Y2)                                   # velocity stage 2 (eq. if_u_s2 / coarse_u_s2)
-    u2[e] = u[e] + c2 * (phi + S[e])
+    u2[e] = u[e] + c2 * (phi + (S[e] if split else Slow(u1, hs2, Y2)))
     i, psi = Psi(u2, h2, X3)                                 # thickness stage 3 (eq. if_h_s3 / coarse_h_s3)
     h3[i] = h[i] + c3 * psi
     hs3[i] = b3 * h3[i] + om2b3 * h2[i] + b3 * h[i]
     e, phi = PhiF(hs3, Y3)                                   # velocity stage 3
-    u3[e] = u[e] + c3 * (phi + S[e])
+    u3[e] = u[e] + c3 * (phi + (S[e] if split else Slow(u2, hs3, Y3)))
 
     h_new, u_new = nan_c(), nan_e()
     h_new[INTc] = h3[INTc]                                   # interior coarse data is final
@@ -247,7 +261,7 @@ def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper", slow_refresh=False
         def eview(fine, pred, coarse):
             return np.where(F_E, fine, np.where(IF1_E, pred, coarse))
 
-        if slow_refresh:
+        if slow_refresh and split:
             # S^k on F_E from the state at t^{n,k} (NaN outside the stencil region poisons misuse)
             Hk = np.where(F, hk, np.where(IF1 | IF2, predict_level(co, h3, h, k), np.nan))
             Uk = np.where(F_E, uk, np.where(IF1_E, uP0, np.nan))
@@ -266,7 +280,7 @@ def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper", slow_refresh=False
         hsk1[i] = b1 * hk1[i] + omb1 * hk[i]
         HS1 = cview(hsk1, hsP1, hs1)
         e, phi = PhiF(HS1, F_E)
-        uk1[e] = uk[e] + c1f * (phi + Sk[e])
+        uk1[e] = uk[e] + c1f * (phi + (Sk[e] if split else Slow(U0, HS1, F_E)))
         U1 = eview(uk1, uP1, u1)
         H1 = cview(hk1, hP1, h1)
         i, psi = Psi(U1, H1, F)                                         # eq. fine_s2
@@ -274,7 +288,7 @@ def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper", slow_refresh=False
         hsk2[i] = b2 * hk2[i] + omb2 * hk[i]
         HS2 = cview(hsk2, hsP2, hs2)
         e, phi = PhiF(HS2, F_E)
-        uk2[e] = uk[e] + c2f * (phi + Sk[e])
+        uk2[e] = uk[e] + c2f * (phi + (Sk[e] if split else Slow(U1, HS2, F_E)))
         U2 = eview(uk2, uP2, u2)
         H2 = cview(hk2, hP2, h2)
         i, psi = Psi(U2, H2, IFc)                                       # correction summand (eq. if_correction)
@@ -284,9 +298,9 @@ def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper", slow_refresh=False
         hs3k[i] = b3 * hkn[i] + om2b3 * hk2[i] + b3 * hk[i]
         HS3 = cview(hs3k, hsP3, hs3)
         e, phi = PhiF(HS3, F_E)
-        ukn[e] = uk[e] + c3f * (phi + Sk[e])
+        ukn[e] = uk[e] + c3f * (phi + (Sk[e] if split else Slow(U2, HS3, F_E)))
         e, phi = PhiF(HS3, IFe)                                         # correction summand (eq. if_correction)
-        accU[e] = accU[e] + (phi + S[e])
+        accU[e] = accU[e] + (phi + (S[e] if split else Slow(U2, HS3, IFe)))
         hk, uk = hkn, ukn
 
     h_new[F] = hk[F]                                                    # h^{n+1} := h^{n,M}
@@ -298,7 +312,7 @@ def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper", slow_refresh=False
     return h_new, u_new
 
 
-def run(mesh, lab, h, u, dt, M, phys, n_steps, extents="paper", slow_refresh=False):
+def run(mesh, lab, h, u, dt, M, phys, n_steps, extents="paper", slow_refresh=False, split=True):
     for _ in range(n_steps):
-        h, u = fblts_step(mesh, lab, h, u, dt, M, phys, extents, slow_refresh=slow_refresh)
+        h, u = fblts_step(mesh, lab, h, u, dt, M, phys, extents, slow_refresh=slow_refresh, split=split)
     return h, u
