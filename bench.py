@@ -112,6 +112,17 @@ def byte_model(counts, M, fused, maxE=6, maxE2=10):
     return b
 
 
+def _finite(x):
+    """JSON-safe copy: NaN / inf -> null."""
+    if isinstance(x, dict):
+        return {k: _finite(v) for k, v in x.items()}
+    if isinstance(x, (list, tuple)):
+        return [_finite(v) for v in x]
+    if isinstance(x, float) and not np.isfinite(x):
+        return None
+    return x
+
+
 def rk4_dt(c, name):
     """0.9 x the RK4 Courant limit nu_loc bisected with the oracle on this config (or its proxy),
     applied to this mesh's max_e sqrt(g max H) / d_e; (None, why) if no scan is recorded."""
@@ -266,7 +277,7 @@ def arm_native(args):
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     s = Solver(c.mesh, c.fine_mask, c.dt, c.M, g=c.g, beta=c.beta, rho0=c.rho0, slow=c.slow, tau_n=c.tau_n,
-               rank=rank, nranks=world, nccl_id=nccl_id, slow_refresh=args.slow_refresh)
+               rank=rank, nranks=world, nccl_id=nccl_id, slow_refresh=args.slow_refresh, unsplit=args.unsplit)
     s.set_state(c.h0, c.u0, 0.0)
     counts = s.counts()
     t_setup = time.perf_counter() - t_setup
@@ -305,6 +316,8 @@ def arm_native(args):
     prof = s.profile(n_prof)
     fused = prof.get("fine_vel_s1", (0.0, 0))[1] > 0
     bm = byte_model(counts, c.M, fused)                     # bytes per step per kind
+    if args.unsplit:                                        # different sweep structure: no per-kind byte model
+        bm = {k: float("nan") for k in bm}
     t_step = {k: tms / n_prof for k, (tms, n) in prof.items() if n}
     dom = max(t_step, key=lambda k: t_step[k])
     launches_dom = prof[dom][1] / n_prof
@@ -406,7 +419,7 @@ def arm_native(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "scaling_note": "strong: the same config-5 mesh is partitioned over N GPUs (a weak-scaled 4096 x 4096N "
                         "mesh needs a distributed mesh upload, DESIGN.md section 7)" if world > 1 else None,
-        "config": {"workload": args.config, "slow_refresh": bool(args.slow_refresh),
+        "config": {"workload": args.config, "slow_refresh": bool(args.slow_refresh), "unsplit": bool(args.unsplit),
                    "cells": c.mesh.nCells, "edges": c.mesh.nEdges,
                    "vertices": c.mesh.nVertices, "M": c.M, "dt": c.dt,
                    "cells_by_region": counts["cells_by_region"],
@@ -427,7 +440,7 @@ def arm_native(args):
         "lts_vs_global": lts_vs_global,
         "clocks": clocks,
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(_finite(line)), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
@@ -442,6 +455,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-global", action="store_true", help="skip the global FB-RK(3,2) comparison run")
+    ap.add_argument("--unsplit", action="store_true",
+                    help="unsplit FB-LTS (full Phi in every velocity update, P:L468-787; one GPU)")
     ap.add_argument("--slow-refresh", action="store_true",
                     help="the slow-term refresh variant (S re-evaluated at every fine level, P:L1427-1431)")
     args = ap.parse_args()

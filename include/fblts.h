@@ -121,6 +121,9 @@ typedef struct {
     double  sal_beta;    /* self-attraction-and-loading coefficient beta of the hurricane model's fast
                             term -g grad(xi - beta xi) (eq. hurricane_fast_terms),
                             0 <= beta < 1; the fast term uses g (1 - beta).  0: plain model */
+    int32_t unsplit;     /* 1: unsplit FB-LTS: the full Phi(U, HS) =
+                            Phi^fast + Phi^slow in every velocity update, stage velocities stored;
+                            one rank, FB-LTS scheme, no slow refresh.  0: split mode (the paper's runs) */
 } fblts_config;
 
 #define FBLTS_SCHEME_FBLTS 0

@@ -138,7 +138,10 @@ struct DevState {
     double *accH, *accU;                // accH indexed by owned cell (IF cells used), accU by e - eb.if2 (IF edges)
     double *rkU[2], *rkAccU;            // RK4 scheme: stage velocities (ping-pong) and the velocity sum
     double *Sf;                         // slow tendency on F_E during the fine phase: S, or Sk (refresh)
-    double *Sk, *hv, *uv;               // slow-term refresh: S^k on F_E and the t^{n,k} views
+    double *Sk, *hv, *uv;               // slow-term refresh: S^k on F_E and the t^{n,k} views;
+                                        // unsplit: stage slow tendency, HS array / view, U view
+    double *un[3];                      // unsplit: stored coarse stage velocities u~1, u~2, u~3
+    double *unk[2];                     // unsplit: stored fine stage velocities uk1, uk2
     double *stage;                      // staging for set/get_state (max(nC, nE) doubles)
     int32_t *cellOld, *edgeOld;         // new -> old permutation (device)
     double *diag;                       // reduction scratch
@@ -213,6 +216,17 @@ void launch_correct(const DevMesh &m, const DevState &st, const double *hN, cons
 void launch_rk4_stage(const DevMesh &m, const DevState &st, int stage, const double *hN, const double *uN,
                       const double *hs, const double *us, double *hout, double *uout, double cnext,
                       double dt6, double g, cudaStream_t s);
+// unsplit FB-LTS building blocks (kernels.cu, end)
+void launch_un_cstage(const DevMesh &m, const DevState &st, int stage, const double *hN, const double *H,
+                      const double *U, double *out, const StepConst &sc, int end, cudaStream_t s);
+void launch_un_vel(const DevMesh &m, const DevState &st, const double *base, double *out, double c, int e0, int e1,
+                   double *acc, int a0, int a1, int first, const StepConst &sc, cudaStream_t s);
+void launch_un_views(const DevMesh &m, const DevState &st, int stage, const double *hN, const double *hNew,
+                     const double *hk, const double *hnext, const double *uN, const double *ufine,
+                     const StepConst &sc, const PredConst &pc, cudaStream_t s);
+void launch_un_fstage(const DevMesh &m, const DevState &st, int stage, const double *hN, const double *hNew,
+                      const double *hk, const double *U, double *out, const StepConst &sc, const PredConst &pc,
+                      int k, cudaStream_t s);
 void launch_permute_in(const int32_t *old_of_new, const double *src, double *dst, int n, cudaStream_t s);
 void launch_permute_out(const int32_t *old_of_new, const double *src, double *dst, int n, cudaStream_t s);
 // diagnostics: writes out[4] (device) = mass, Gamma, min h, max nu

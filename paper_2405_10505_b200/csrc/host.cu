@@ -257,6 +257,8 @@ int fblts_create(fblts_ctx **out, const fblts_config *cfg) {
     if (cfg->scheme != FBLTS_SCHEME_FBLTS && cfg->scheme != FBLTS_SCHEME_RK4) return FBLTS_ERR_INVALID_ARG;
     if (cfg->scheme == FBLTS_SCHEME_RK4 && cfg->nranks != 1) return FBLTS_ERR_INVALID_ARG;   // reference scheme: one rank
     if (cfg->slow_refresh && (cfg->nranks != 1 || cfg->scheme != FBLTS_SCHEME_FBLTS)) return FBLTS_ERR_INVALID_ARG;
+    if (cfg->unsplit && (cfg->nranks != 1 || cfg->scheme != FBLTS_SCHEME_FBLTS || cfg->slow_refresh))
+        return FBLTS_ERR_INVALID_ARG;
     // No CUDA call here: mesh upload, labelling and renumbering are host work, so a context
     // can be created (and its labels inspected) on a machine without a GPU.
     fblts_ctx *c = new fblts_ctx();
@@ -971,11 +973,14 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
     put(s.rkU[0], nrk);
     put(s.rkU[1], nrk);
     put(s.rkAccU, nrk);
-    const bool rf = c->cfg.slow_refresh != 0;
+    const bool rf = c->cfg.slow_refresh != 0 || c->cfg.unsplit != 0;
     put(s.Sk, rf ? nE1 : 1);
     put(s.uv, rf ? nE1 : 1);
     put(s.hv, rf ? (size_t)std::max(1, L.nC) : 1);
-    if (base) s.Sf = rf ? s.Sk : s.S;
+    const size_t nun = c->cfg.unsplit ? nE1 : 1;
+    for (int q = 0; q < 3; ++q) put(s.un[q], nun);
+    for (int q = 0; q < 2; ++q) put(s.unk[q], nun);
+    if (base) s.Sf = c->cfg.slow_refresh ? s.Sk : s.S;
     put(s.stage, std::max(m.nC, m.nE));
     put(s.cellOld, L.nC);
     put(s.edgeOld, L.nE);
@@ -1448,8 +1453,92 @@ int enqueue_rk4_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
     return FBLTS_OK;
 }
 
+// One unsplit FB-LTS coarse step (config unsplit, one rank): per stage a thickness
+// sweep with the stored stage velocity, the FB-averaged thickness (coarse) or the stage's HS and U
+// views (fine), the slow sweeps on the stage's extent and the velocity sweep (oracle lts.py split=False).
+int enqueue_unsplit_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
+    const DevMesh &m = c->dm;
+    DevState st = c->ds;
+    const StepConst &sc = c->sc;
+    const double *hN = c->hbuf[par], *uN = c->ubuf[par];
+    double *hNew = c->hbuf[1 - par], *uNew = c->ubuf[1 - par];
+    const int M = sc.M;
+    auto mark = [&](int k) {
+        if (rec) rec->mark(k, s);
+    };
+    auto hb = [&](int k) { return ((M - 1 - k) % 2 == 0) ? hNew : st.hT; };
+    auto ub = [&](int k) { return ((M - 1 - k) % 2 == 0) ? uNew : st.uT; };
+    auto pred = [&](int k) {
+        PredConst pc;
+        pc.a = (double)k / (double)M;
+        pc.oma = 1.0 - pc.a;
+        pc.a1 = (double)(k + 1) / (double)M;
+        pc.oma1 = 1.0 - pc.a1;
+        pc.b = 1.0 / (double)M;
+        pc.c = 1.0 - (double)(k + 1) / (double)M;
+        return pc;
+    };
+    auto slow = [&](const double *U, int e0, int e1) {          // Phi^slow(U, st.hv) on [e0, e1) -> st.Sk
+        if (!c->cfg.slow) {
+            if (e1 > e0) cudaMemsetAsync(st.Sk + e0, 0, (size_t)(e1 - e0) * 8, s);
+            return;
+        }
+        mark(K_SLOW_PRE);
+        launch_slow_pre_range(m, st, st.hv, U, 0, 0, 0, s);
+        mark(K_SLOW_EDGE);
+        launch_slow_edge_range(m, st, st.hv, U, st.Sk, e0, e1, sc, s);
+    };
+    // ---- coarse phase: extents X1 = C u F^5, Y1 = C_E u F^4_E, X2 = C u F^3, Y2 = C_E u F^2_E,
+    //      X3 = C u F^1, Y3 = IF-1_E u int_E (IF-2_E computed as scratch)
+    const double *Hs[3] = {hN, st.h1, st.h2};
+    const double *Us[3] = {uN, st.un[0], st.un[1]};
+    double *Hout[3] = {st.h1, st.h2, hNew};
+    const int Xend[3] = {m.cb.fl[5], m.cb.fl[3], m.cb.fl[1]}, Yend[3] = {m.eb.fl[4], m.eb.fl[2], m.eb.f};
+    const double cs[3] = {sc.c1, sc.c2, sc.c3};
+    const int kinds[3] = {K_COARSE_S1, K_COARSE_S2, K_COARSE_S3};
+    for (int q = 0; q < 3; ++q) {
+        mark(kinds[q]);
+        launch_un_cstage(m, st, q + 1, hN, Hs[q], Us[q], Hout[q], sc, Xend[q], s);
+        slow(Us[q], 0, Yend[q]);
+        mark(K_COARSE_VEL);
+        launch_un_vel(m, st, uN, st.un[q], cs[q], 0, Yend[q], nullptr, 0, 0, 0, sc, s);
+    }
+    if (m.eb.if2 > 0) CUDA_TRY(c, cudaMemcpyAsync(uNew, st.un[2], (size_t)m.eb.if2 * 8, cudaMemcpyDeviceToDevice, s));
+    // ---- fine phase
+    if (c->have_fine) {
+        for (int k = 0; k < M; ++k) {
+            const double *hk = k == 0 ? hN : hb(k - 1), *uk = k == 0 ? uN : ub(k - 1);
+            const PredConst pc = pred(k);
+            mark(K_FINE_S1);                                         // stage 1: thickness (U0 = u^{n,k} on F_E)
+            launch_fine_s1(m, st, hN, hNew, hk, uk, sc, pc, k, s, m.cb, true);
+            launch_un_views(m, st, 1, hN, hNew, hk, nullptr, uN, uk, sc, pc, s);
+            slow(st.uv, m.eb.f, m.eb.end);
+            mark(K_FINE_VEL);
+            launch_un_vel(m, st, uk, st.unk[0], sc.c1f, m.eb.f, m.eb.end, nullptr, 0, 0, 0, sc, s);
+            mark(K_FINE_S2);                                         // stage 2
+            launch_un_fstage(m, st, 2, hN, hNew, hk, st.unk[0], st.h2, sc, pc, k, s);
+            launch_un_views(m, st, 2, hN, hNew, hk, nullptr, uN, st.unk[0], sc, pc, s);
+            slow(st.uv, m.eb.f, m.eb.end);
+            mark(K_FINE_VEL);
+            launch_un_vel(m, st, uk, st.unk[1], sc.c2f, m.eb.f, m.eb.end, nullptr, 0, 0, 0, sc, s);
+            mark(K_FINE_S3);                                         // stage 3 + correction summands
+            launch_un_views(m, st, 3, hN, hNew, hk, hk, uN, st.unk[1], sc, pc, s);   // U2 view for the sweep
+            launch_un_fstage(m, st, 3, hN, hNew, hk, st.uv, hb(k), sc, pc, k, s);
+            launch_un_views(m, st, 3, hN, hNew, hk, hb(k), uN, st.unk[1], sc, pc, s);
+            slow(st.uv, m.eb.if2, m.eb.end);
+            mark(K_FINE_VEL);
+            launch_un_vel(m, st, uk, ub(k), sc.c3f, m.eb.if2, m.eb.end, st.accU, m.eb.if2, m.eb.f, k == 0, sc, s);
+        }
+        mark(K_CORRECT);
+        launch_correct(m, st, hN, uN, hNew, uNew, sc, s, m.cb, true);
+    }
+    mark(-1);
+    return FBLTS_OK;
+}
+
 int enqueue_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
     if (c->cfg.scheme == FBLTS_SCHEME_RK4) return enqueue_rk4_step(c, par, s, rec);
+    if (c->cfg.unsplit) return enqueue_unsplit_step(c, par, s, rec);
     const bool multi = c->cfg.nranks > 1;
     PhaseX px, px1;
     for (int ph = 0; enqueue_phase(c, par, ph, s, rec, &px, 0); ++ph) {

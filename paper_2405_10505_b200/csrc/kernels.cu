@@ -1252,4 +1252,169 @@ void launch_rk4_stage(const DevMesh &m, const DevState &st, int stage, const dou
                                                                       hout, uout, cnext, dt6, g, nbC, st.err));
 }
 
+
+// ====================================================================== unsplit FB-LTS (N1)
+// SURVEY 8(f) N1, P:L468-787 with the full Phi(U, HS) = Phi^fast(HS) + Phi^slow(U, HS) in every velocity
+// update (reading Q16).  The stage velocities are stored (they need the slow terms at the stage), so
+// every stage is: thickness sweep (stored U) -> FB-averaged thickness / views -> slow sweeps on the
+// extent -> velocity sweep.  Same canonical arithmetic as the oracle (oracle/lts.py split=False).
+
+// coarse thickness stage s on cells [0, end): out = hN + c Psi(U, H) and the FB average into hsv
+// (s = 1: h* = b1 h1 + (1-b1) hN; 2: h** = b2 h2 + (1-b2) hN; 3: h*** = b3 h3 + (1-2b3) h2 + b3 hN)
+template <int G, int STAGE>
+__global__ void __launch_bounds__(TPB) k_un_cstage(DevMesh m, const double *__restrict__ hN,
+                                                   const double *__restrict__ H, const double *__restrict__ U,
+                                                   double *__restrict__ out, double *__restrict__ hsv,
+                                                   StepConst sc, int end, DevError *err) {
+    const int i = blockIdx.x * TPB + threadIdx.x;
+    if (i >= end) return;
+    int2 r[G];
+    load_row<G>(m, i, r);
+    const int n = m.nEoC[i];
+    const double Hi = H[i];
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+        if (j < n) {
+            bool pos;
+            const int e = decode(r[j].x, pos);
+            acc = acc + psi_term(pos, Hi, H[r[j].y], U[e], m.dv[e]);
+        }
+    }
+    const double c = STAGE == 1 ? sc.c1 : (STAGE == 2 ? sc.c2 : sc.c3);
+    const double psi = -acc / m.areaCell[i];
+    const double v = hN[i] + c * psi;
+    out[i] = v;
+    const double hn = hN[i];
+    hsv[i] = STAGE == 1 ? sc.b1 * v + sc.omb1 * hn
+                        : (STAGE == 2 ? sc.b2 * v + sc.omb2 * hn : sc.b3 * v + sc.om2b3 * Hi + sc.b3 * hn);
+    if (!(v > 0.0)) report(err, STAGE == 1 ? K_COARSE_S1 : (STAGE == 2 ? K_COARSE_S2 : K_COARSE_S3), -1, i, v);
+}
+
+// velocity sweep on edges [e0, e1): out = base + c (Phi^fast(HS) + S); with acc != nullptr the edges
+// [a0, a1) instead accumulate acc[e - a0] += Phi^fast(HS) + S (correction summand, k = 0 starts from 0)
+__global__ void __launch_bounds__(TPB) k_un_vel(DevMesh m, const double *__restrict__ HS,
+                                                const double *__restrict__ S, const double *__restrict__ base,
+                                                double *__restrict__ out, double c, double g, int e0, int e1,
+                                                double *__restrict__ acc, int a0, int a1, int first) {
+    const int e = e0 + blockIdx.x * TPB + threadIdx.x;
+    if (e >= e1) return;
+    const int2 cc = m.coe[e];
+    const double phi = phi_fast(g, HS[cc.x], m.zb[cc.x], HS[cc.y], m.zb[cc.y], m.dc[e]);
+    if (acc && e >= a0 && e < a1) {
+        const double prev = first ? 0.0 : acc[e - a0];
+        acc[e - a0] = prev + (phi + S[e]);
+    } else {
+        out[e] = base[e] + c * (phi + S[e]);
+    }
+}
+
+// fine-phase views of stage s (1..3) at subcycle k: HS view on every owned cell (view1/2/3: fine
+// FB average, IF-1 predicted, IF-2/int coarse) and the stage's U view on every owned edge
+// (U0 / U1 / U2: F_E fine, IF-1_E predicted from the stored coarse velocities, others coarse)
+template <int S>
+__global__ void __launch_bounds__(TPB) k_un_views(DevMesh m, FineArrays a, const double *__restrict__ hnext,
+                                                  const double *__restrict__ uN, const double *__restrict__ ufine,
+                                                  const double *__restrict__ u1c, const double *__restrict__ u2c,
+                                                  const double *__restrict__ u3c, double *__restrict__ hsv,
+                                                  double *__restrict__ uv, StepConst sc, PredConst p, unsigned nbC) {
+    if (blockIdx.x < nbC) {
+        const int i = blockIdx.x * TPB + threadIdx.x;
+        if (i >= m.nOwnC) return;
+        double H, HS;
+        if (S == 1) view1<true>(m, sc, p, a, i, H, HS);
+        else if (S == 2) view2<true>(m, sc, p, a, i, H, HS);
+        else HS = view3<true>(m, sc, p, a, hnext, i);
+        hsv[i] = HS;
+    } else {
+        const int e = (blockIdx.x - nbC) * TPB + threadIdx.x;
+        if (e >= m.nOwnE) return;
+        const int ec = ecls(m.eb, e);
+        double v;
+        if (ec == 3) v = ufine[e];
+        else if (ec == 2) v = S == 1 ? p.a * u3c[e] + p.oma * uN[e]
+                                     : p.a * u3c[e] + p.b * (S == 2 ? u1c[e] : u2c[e]) + p.c * uN[e];
+        else v = S == 1 ? uN[e] : (S == 2 ? u1c[e] : u2c[e]);
+        uv[e] = v;
+    }
+}
+
+// fine thickness stage 2 / 3 with stored velocities: cells [begin, end)
+//   s = 2: F: hk2 = hk + dt/(2M) Psi(U1 = uk1 on F_E, H1 view)
+//   s = 3: F: hkn = hk + dt/M Psi(U2 view, H2 view); IF-1 u IF-2: accH += Psi(U2, H2)
+template <int G, int STAGE>
+__global__ void __launch_bounds__(TPB) k_un_fstage(DevMesh m, FineArrays a, const double *__restrict__ U,
+                                                   double *__restrict__ out, double *__restrict__ accH,
+                                                   StepConst sc, PredConst p, int k, int begin, int end,
+                                                   DevError *err) {
+    const int i = begin + blockIdx.x * TPB + threadIdx.x;
+    if (i >= end) return;
+    int2 r[G];
+    load_row<G>(m, i, r);
+    const int n = m.nEoC[i];
+    double Hi, HSi;
+    if (STAGE == 2) view1<true>(m, sc, p, a, i, Hi, HSi);
+    else view2<true>(m, sc, p, a, i, Hi, HSi);
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+        if (j < n) {
+            bool pos;
+            const int e = decode(r[j].x, pos);
+            double Hn, HSn;
+            if (STAGE == 2) view1<true>(m, sc, p, a, r[j].y, Hn, HSn);
+            else view2<true>(m, sc, p, a, r[j].y, Hn, HSn);
+            acc = acc + psi_term(pos, Hi, Hn, U[e], m.dv[e]);
+        }
+    }
+    const double psi = -acc / m.areaCell[i];
+    if (i >= m.cb.f) {
+        const double v = a.hk[i] + (STAGE == 2 ? sc.c2f : sc.c3f) * psi;
+        out[i] = v;
+        if (!(v > 0.0)) report(err, STAGE == 2 ? K_FINE_S2 : K_FINE_S3, k, i, v);
+    } else {
+        const double prev = k == 0 ? 0.0 : accH[i];
+        accH[i] = prev + psi;
+    }
+}
+
+void launch_un_cstage(const DevMesh &m, const DevState &st, int stage, const double *hN, const double *H,
+                      const double *U, double *out, const StepConst &sc, int end, cudaStream_t s) {
+    if (end <= 0) return;
+    FBLTS_DISPATCH_G(m.ecS, {
+        if (stage == 1) k_un_cstage<G, 1><<<nblocks(end), TPB, 0, s>>>(m, hN, H, U, out, st.hv, sc, end, st.err);
+        else if (stage == 2) k_un_cstage<G, 2><<<nblocks(end), TPB, 0, s>>>(m, hN, H, U, out, st.hv, sc, end, st.err);
+        else k_un_cstage<G, 3><<<nblocks(end), TPB, 0, s>>>(m, hN, H, U, out, st.hv, sc, end, st.err);
+    });
+}
+void launch_un_vel(const DevMesh &m, const DevState &st, const double *base, double *out, double c, int e0, int e1,
+                   double *acc, int a0, int a1, int first, const StepConst &sc, cudaStream_t s) {
+    if (e1 > e0)
+        k_un_vel<<<nblocks(e1 - e0), TPB, 0, s>>>(m, st.hv, st.Sk, base, out, c, sc.g, e0, e1, acc, a0, a1, first);
+}
+void launch_un_views(const DevMesh &m, const DevState &st, int stage, const double *hN, const double *hNew,
+                     const double *hk, const double *hnext, const double *uN, const double *ufine,
+                     const StepConst &sc, const PredConst &pc, cudaStream_t s) {
+    const FineArrays a = fine_arrays(st, hN, hNew, hk);
+    const unsigned nbC = nblocks(m.nOwnC), nbE = nblocks(m.nOwnE);
+    if (stage == 1)
+        k_un_views<1><<<nbC + nbE, TPB, 0, s>>>(m, a, hnext, uN, ufine, st.un[0], st.un[1], st.un[2], st.hv, st.uv, sc, pc, nbC);
+    else if (stage == 2)
+        k_un_views<2><<<nbC + nbE, TPB, 0, s>>>(m, a, hnext, uN, ufine, st.un[0], st.un[1], st.un[2], st.hv, st.uv, sc, pc, nbC);
+    else
+        k_un_views<3><<<nbC + nbE, TPB, 0, s>>>(m, a, hnext, uN, ufine, st.un[0], st.un[1], st.un[2], st.hv, st.uv, sc, pc, nbC);
+}
+void launch_un_fstage(const DevMesh &m, const DevState &st, int stage, const double *hN, const double *hNew,
+                      const double *hk, const double *U, double *out, const StepConst &sc, const PredConst &pc,
+                      int k, cudaStream_t s) {
+    const FineArrays a = fine_arrays(st, hN, hNew, hk);
+    const int b0 = stage == 2 ? m.cb.f : m.cb.if2, end = m.cb.end;
+    if (end <= b0) return;
+    FBLTS_DISPATCH_G(m.ecS, {
+        if (stage == 2)
+            k_un_fstage<G, 2><<<nblocks(end - b0), TPB, 0, s>>>(m, a, U, out, st.accH, sc, pc, k, b0, end, st.err);
+        else
+            k_un_fstage<G, 3><<<nblocks(end - b0), TPB, 0, s>>>(m, a, U, out, st.accH, sc, pc, k, b0, end, st.err);
+    });
+}
 }  // namespace fblts

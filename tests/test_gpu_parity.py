@@ -421,3 +421,22 @@ def test_hurricane_terms_match_oracle(Solver, scheme):
     s.close()
     eh, eu = assert_parity(hg, ug, ho, uo)
     print(f"hurricane {scheme}: eps_h={eh:.3e} eps_u={eu:.3e} bitwise={np.array_equal(hg, ho) and np.array_equal(ug, uo)}")
+
+
+@pytest.mark.parametrize("which,M", [("config1", 4), ("shelf", 2), ("shelf", 3), ("shelf", 1)])
+def test_unsplit_matches_oracle(Solver, which, M):
+    """Unsplit FB-LTS: the full Phi(U, HS) in every velocity update on
+    the paper's extents, through the C ABI, against the oracle's fblts_step(split=False), 40 steps."""
+    c = configs.config1() if which == "config1" else configs.small_shelf(nx=64, ny=48, seed=5,
+                                                                          dt=20.0 if M > 1 else 5.0)
+    lab = lts.label_regions(c.mesh, c.fine_mask)
+    ho, uo = lts.run(c.mesh, lab, c.h0, c.u0, c.dt, M, phys_of(c), 40, split=False)
+    assert np.all(np.isfinite(ho))
+    s = Solver(c.mesh, c.fine_mask, c.dt, M, g=c.g, beta=c.beta, rho0=c.rho0, slow=c.slow, tau_n=c.tau_n,
+               unsplit=True)
+    s.set_state(c.h0, c.u0)
+    s.step(40)
+    hg, ug, _ = s.state()
+    s.close()
+    eh, eu = assert_parity(hg, ug, ho, uo)
+    print(f"unsplit {which} M={M}: eps_h={eh:.3e} eps_u={eu:.3e} bitwise={np.array_equal(hg, ho) and np.array_equal(ug, uo)}")
