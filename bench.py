@@ -61,13 +61,17 @@ def cpu_sample_case():
 
 
 # ------------------------------------------------------------------ byte model
-def byte_model(counts, M, fused, maxE=6, maxE2=10):
+def byte_model(counts, M, fused, sub=0, maxE=6, maxE2=10):
     """Algorithmic bytes PER STEP of each kernel kind (the method's arrays, each element once per
     sweep; recomputable intermediates and padding not counted), summed over that kind's launches in
     one coarse step.  On a hex mesh the stage sweeps give SURVEY 8(d)'s 188 B/cell (s >= 2).
     `fused`: the deep fine velocity sweep of subcycle k-1 runs inside the deep stage-1 sweep of
     subcycle k (kind fine_vel_s1, k = 1..M-1); fine_s1 then holds the band stage 1 (every k) and the
-    deep stage 1 of k = 0, fine_vel the band velocity sweeps and the last full one."""
+    deep stage 1 of k = 0, fine_vel the band velocity sweeps and the last full one.
+    `sub` (the fused-subcycle start level, 0 = off): the cells of F\F^sub run whole subcycles in
+    kind fine_sub (per launch: the subcycle's inputs h^{n,k}, [h^{n,k-1}, h2], z_b, A and the
+    connectivity per cell, u, S, l_e, d_e per edge, once; writes h^{n,k+1}, h2 [+ its publishing
+    copy] and [u^{n,k}]); the staged deep sweeps then stop at F^sub."""
     C, E = counts["owned_cells"], counts["owned_edges"]          # this rank's share
     V = counts["nVertices"] * C // max(1, counts["nCells"])
     cc, ec = counts["cells_by_region"], counts["edges_by_region"]
@@ -80,7 +84,8 @@ def byte_model(counts, M, fused, maxE=6, maxE2=10):
     edge_s = 8 + 8 + 8 + 8                   # u_base, S, l_e, d_e
     vel_e = 8 + 8 + 8 + 8 + 8                # cellsOnEdge, u_base, S, d_e, write
     vel_c = 8 * 4                            # h3, h2, h_base, z_b
-    fs1 = lambda lo: cells(lo, 8) * (slotC + 8 + 8 + 8) + edges(lo, 8) * edge_s1
+    top = 8 if not sub else 2 + sub        # last region code of the staged fine sweeps (F^sub \ F^(sub-1))
+    fs1 = lambda lo: cells(lo, top) * (slotC + 8 + 8 + 8) + edges(lo, top) * edge_s1
     fvel = lambda lo: edges(lo, 8) * vel_e + cells(lo, 8) * vel_c
     b = {}
     b["slow_pre"] = V * (12 + 12 + 24 + 8 + 8) + C * (4 + 4 * maxE + 8 + 8) + E * (8 + 8 + 8 + 8)
@@ -89,8 +94,13 @@ def byte_model(counts, M, fused, maxE=6, maxE2=10):
     b["coarse_s2"] = cells(0, 5) * cell_s + edges(0, 5) * edge_s
     b["coarse_s3"] = cells(0, 3) * cell_s + edges(0, 3) * edge_s
     b["coarse_vel"] = edges(0, 0) * vel_e + cells(0, 1) * vel_c
-    b["fine_s2"] = M * (cells(3, 8) * (slotC + 8 + 8 + 8 + 8 + 8 - 8) + edges(3, 8) * edge_s)
-    b["fine_s3"] = M * (cells(1, 8) * (slotC + 8 + 8 + 8 + 8 + 8 - 8) + edges(1, 8) * edge_s)
+    b["fine_s2"] = M * (cells(3, top) * (slotC + 8 + 8 + 8 + 8 + 8 - 8) + edges(3, top) * edge_s)
+    b["fine_s3"] = M * (cells(1, top) * (slotC + 8 + 8 + 8 + 8 + 8 - 8) + edges(1, top) * edge_s)
+    if sub:
+        cs_, es_ = cells(top + 1, 8), edges(top + 1, 8)
+        k0 = cs_ * (slotC + 8 * 3 + 8 * 2) + es_ * edge_s                        # h, z_b, A; write h2, out
+        k1 = cs_ * (slotC + 8 * 5 + 8 * 2 + 16) + es_ * (edge_s + 8)            # + h^{n,k-1}, h2, copy; write u
+        b["fine_sub"] = k0 + (M - 1) * k1
     b["correct_if"] = cells(1, 2) * 24 + edges(1, 2) * 24
     # slow-term refresh (k = 1..M-1): views (cells IF..F write h, edges IF-1_E..F_E write u), the
     # restricted slow_pre (cells IF-1..F, edges IF-1_E..F_E, vertices ~2 per cell) and slow_edge on F_E
@@ -104,7 +114,7 @@ def byte_model(counts, M, fused, maxE=6, maxE2=10):
         b["fine_s1"] = M * band_s1 + fs1(4)
         b["fine_vel"] = (M - 1) * band_vel + fvel(1)
         # deep vel(k-1) + s1(k): cells row, h^{n,k}, h2, h^{n,k-1}, z_b, A, write h1; edges u, S, l, d, write u
-        b["fine_vel_s1"] = (M - 1) * (cells(4, 8) * (slotC + 8 * 6) + edges(4, 8) * 40)
+        b["fine_vel_s1"] = (M - 1) * (cells(4, top) * (slotC + 8 * 6) + edges(4, top) * 40)
     else:
         b["fine_s1"] = M * fs1(3)
         b["fine_vel"] = M * fvel(1)
@@ -315,7 +325,9 @@ def arm_native(args):
     n_prof = max(1, min(args.steps, 5))
     prof = s.profile(n_prof)
     fused = prof.get("fine_vel_s1", (0.0, 0))[1] > 0
-    bm = byte_model(counts, c.M, fused)                     # bytes per step per kind
+    sub = 5 if prof.get("fine_sub", (0.0, 0))[1] > 0 else 0
+    sub = int(os.environ.get("FBLTS_SUB_LEVEL", sub)) if sub else 0
+    bm = byte_model(counts, c.M, fused, sub)                # bytes per step per kind
     if args.unsplit:                                        # different sweep structure: no per-kind byte model
         bm = {k: float("nan") for k in bm}
     t_step = {k: tms / n_prof for k, (tms, n) in prof.items() if n}

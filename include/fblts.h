@@ -146,12 +146,14 @@ int fblts_set_regions(fblts_ctx *ctx, const uint8_t *fine_mask);
 /* Region codes in ORIGINAL order (see FBLTS_REGION_*); either pointer may be NULL. */
 int fblts_get_labels(fblts_ctx *ctx, int8_t *cell_region, int8_t *edge_region);
 
-/* Entity counts (out must hold 28 int64): out[0..2] = nCells, nEdges, nVertices; cells per
+/* Entity counts (out must hold 32 int64): out[0..2] = nCells, nEdges, nVertices; cells per
  * region code 0..8 at out[3..11], edges per code 0..8 at out[12..20]; out[21] = owned cells,
  * out[22] = owned edges (equal to nCells, nEdges for one rank); out[23] = kernel launches per
  * coarse step (nodes of the captured CUDA graph, 0 before the first fblts_step); out[24..27] =
  * cell tiles of the staged kernels: number of tiles, total halo cells, total local edges,
- * largest per-tile shared-memory footprint in bytes. */
+ * largest per-tile shared-memory footprint in bytes; out[28..31] = subcycle tiles of the fused
+ * fine subcycle (0 when it is off): number of tiles, total ring-1..3 cells, total local edges,
+ * shared-memory footprint in bytes. */
 int fblts_get_counts(fblts_ctx *ctx, int64_t *out);
 
 /* Halo exchange lists of this rank with `peer` (host logic, no device needed): which = 0 ring-1
@@ -213,7 +215,7 @@ int fblts_diagnostics(fblts_ctx *ctx, double out[4]);
 /* Instrumented replay for the roofline: runs n_coarse steps WITHOUT the graph, with
  * CUDA events around every launch on cfg.stream; ms[k] = total device ms of kernel
  * kind k, launches[k] = launch count, for k < FBLTS_NUM_KERNELS.  Advances the state. */
-#define FBLTS_NUM_KERNELS 11
+#define FBLTS_NUM_KERNELS 15
 int fblts_profile(fblts_ctx *ctx, int32_t n_coarse, double *ms, int64_t *launches);
 const char *fblts_kernel_name(int32_t kind);
 

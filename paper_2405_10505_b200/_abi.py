@@ -23,7 +23,7 @@ _lib = C.CDLL(LIB_PATH)
 FBLTS_OK = 0
 ERRORS = {-1: "INVALID_ARG", -2: "MESH", -3: "LABELS", -4: "STATE", -5: "CUDA", -6: "NCCL", -7: "POSITIVITY",
           -8: "ORDER"}
-NUM_KERNELS = 14
+NUM_KERNELS = 15
 
 _i32p = C.POINTER(C.c_int32)
 _f64p = C.POINTER(C.c_double)
@@ -155,7 +155,7 @@ def fblts_get_labels(ctx, nCells, nEdges):
 
 
 def fblts_get_counts(ctx):
-    out = np.zeros(28, np.int64)
+    out = np.zeros(32, np.int64)
     _check(ctx, _lib_counts(ctx, _ptr(out, C.c_int64)))
     return out
 

@@ -21,7 +21,8 @@ namespace fblts {
 
 enum KernelKind {
     K_SLOW_PRE = 0, K_SLOW_EDGE, K_COARSE_S1, K_COARSE_S2, K_COARSE_S3, K_COARSE_VEL,
-    K_FINE_S1, K_FINE_S2, K_FINE_S3, K_FINE_VEL, K_CORRECT, K_FINE_VS1, K_RK4_STAGE, K_SLOW_REFRESH, K_NUM
+    K_FINE_S1, K_FINE_S2, K_FINE_S3, K_FINE_VEL, K_CORRECT, K_FINE_VS1, K_RK4_STAGE, K_SLOW_REFRESH, K_FINE_SUB,
+    K_NUM
 };
 
 // Region boundaries of one region-major block: [begin,if2) int, [if2,if1) IF-2,
@@ -64,6 +65,29 @@ struct TileMesh {
     const uint16_t *__restrict__ row;       // [maxE][strideRow]
 };
 
+// Subcycle tiles (fused fine subcycle): the tiles of the deep fine region
+// F\F^2 with their 3-ring neighbourhood, so that one CTA advances a tile through a whole fine
+// subcycle (velocity stage 3 of subcycle k-1, thickness stages 1-3 of subcycle k) by recomputing
+// the stage values on the rings it needs: stage 1 on rings 0-2, stage 2 on rings 0-1, stage 3 on
+// the tile.  Local cells: own (i - c0), then the halo list R1 | R2 | R3 at HALO0 + position (each
+// ring sorted).  Local edges (every edge of a ring-0..2 cell): the tile's owned run [eo0, eo1)
+// (e - eo0), then FGAP, then the foreign edges sorted by (lowest ring of their two cells, index):
+// nF0 | nF1 | nF2, so each stage's edge set is a prefix.  ecl as in TileMesh (per local edge, list
+// order); rows: slot-major 16-bit slot tables of the rows own | R1 | R2 (row r -> local cell r or
+// HALO0 + r - nOwn), each tile's table padded to 8 entries.  info[t * FTINFO + k], k = c0, c1, h0, n1, n2, n3, eo0, eo1, f0, nF0, nF1, nF2,
+// l0, s0, flags (bit 0: a ring-1 cell lies outside the fused region, so stage 1 is written out).
+constexpr int FTINFO = 16;
+struct SubTileMesh {
+    int32_t nTiles;
+    int32_t hmax, emax;                     // largest R1+R2+R3 count / local-edge count of any tile
+    int32_t rmax;                           // largest slot-table size (uint16 entries, padded to 8)
+    const int32_t *__restrict__ info;
+    const int32_t *__restrict__ halo;
+    const int32_t *__restrict__ fedge;
+    const uint32_t *__restrict__ ecl;
+    const uint16_t *__restrict__ row;
+};
+
 struct DevMesh {
     int32_t nC, nE, nV;               // local entity counts (owned + halo)
     int32_t nOwnC, nOwnE;              // owned cells [0, nOwnC); edges touching owned cells [0, nOwnE)
@@ -100,6 +124,7 @@ struct DevMesh {
     Bounds eb;                         // edges touching owned cells (eb.end = nOwnE)
     Bounds cbh;                        // halo cell block [nOwnC, nC), region-major, absolute indices
     TileMesh tm;                       // tiles of the owned cells
+    SubTileMesh st;                    // subcycle tiles of F\F^2 (one rank; fused fine subcycle)
 };
 
 // Device error record (positivity / NaN), first failure wins.
@@ -142,6 +167,8 @@ struct DevState {
                                         // unsplit: stage slow tendency, HS array / view, U view
     double *un[3];                      // unsplit: stored coarse stage velocities u~1, u~2, u~3
     double *unk[2];                     // unsplit: stored fine stage velocities uk1, uk2
+    double *hT2;                        // fused subcycle: third fine level buffer (levels k-1, k, k+1 distinct)
+    double *h2alt;                      // fused subcycle: stage-2 thickness of F\F^2 before it is published
     double *stage;                      // staging for set/get_state (max(nC, nE) doubles)
     int32_t *cellOld, *edgeOld;         // new -> old permutation (device)
     double *diag;                       // reduction scratch
@@ -167,6 +194,19 @@ struct StageArgs {
     const double *h2 = nullptr;   // STAGE 4
     double *unew = nullptr;       // STAGE 4
 };
+// Fused fine subcycle k on the subcycle tiles (kernels.cu k_fine_sub): with vel (k >= 1) first
+//   u^{n,k}_e = u^{n,k-1}_e + dt/M (Phi^fast_e(h***) + S_e),  h*** = b3 h^{n,k} + (1-2b3) h2 + b3 h^{n,k-1}
+// on the edges of rings 0-2 (written on the owned run), else u^{n,k} = ubase; then the three
+// thickness stages of subeqn fine_fbrk32 with the stage velocities recomputed per edge.
+struct SubArgs {
+    const double *hk, *hm, *h2, *ubase, *S;   // h^{n,k}, h^{n,k-1}, stage-2 thickness of k-1, u^{n,k-1} (or u^{n,0})
+    double *unew, *h1out, *h2out, *out;       // u^{n,k} (owned runs), stage 1 (border tiles), stage 2, h^{n,k+1}
+    double g, b1, omb1, b2, omb2, b3, om2b3, c1f, c2f, c3f;
+    int32_t k;
+};
+int sub_smem_bytes_host(int hmax, int emax, int rmax);
+void launch_fine_sub(const DevMesh &m, bool vel, int nsm, const SubArgs &a, DevError *err, cudaStream_t s);
+
 void launch_stage_tiled(const DevMesh &m, int stage, int tile0, int tile1, int hmax, int emax, int nsm,
                         const StageArgs &a, DevError *err, cudaStream_t s);
 int stage_tiled_smem_bytes_host(int stage, int hmax, int emax);   // bytes for tiles with <= hmax / emax

@@ -24,7 +24,7 @@ namespace {
 
 const char *kKernelNames[K_NUM] = {"slow_pre",  "slow_edge", "coarse_s1", "coarse_s2", "coarse_s3", "coarse_vel",
                                    "fine_s1",   "fine_s2",   "fine_s3",   "fine_vel",  "correct_if", "fine_vel_s1",
-                                   "rk4_stage", "slow_refresh"};
+                                   "rk4_stage", "slow_refresh", "fine_sub"};
 
 enum Phase { P_CREATED = 0, P_MESH, P_REGIONS, P_BOUND, P_STATE };
 
@@ -104,6 +104,15 @@ struct fblts_ctx {
     bool tiled = true;
     bool split = false;        // FBLTS_SPLIT=1: separate launches for the thin interface blocks
     bool fuse_vel = true;      // deep fine velocity stage fused into the next stage 1 (FBLTS_FUSE=0: off)
+    // subcycle tiles of F\F^5 (fused fine subcycle; one rank, split FB-LTS).  Opt-in (FBLTS_SUB=1):
+    // bitwise equal to the per-stage sweeps but measured slower on B200
+    bool fuse_sub = false;
+    int sub_level = 5;         // subcycle tiles cover F\F^sub_level (>= 2)
+    std::vector<int32_t> s_info, s_halo, s_fedge;
+    std::vector<uint32_t> s_ecl;
+    std::vector<uint16_t> s_row;
+    int s_nT = 0, s_hmax = 0, s_emax = 0, s_rmax = 0;
+    size_t s_nHalo = 0, s_nFedge = 0, s_nEcl = 0, s_nRow = 0;
     int nsm = 148;         // FBLTS_TILED=0 selects the unstaged kernels (development comparisons)
 };
 namespace {
@@ -271,6 +280,9 @@ int fblts_create(fblts_ctx **out, const fblts_config *cfg) {
     if (const char *ev = std::getenv("FBLTS_TILED")) c->tiled = std::atoi(ev) != 0;
     if (const char *ev = std::getenv("FBLTS_SPLIT")) c->split = std::atoi(ev) != 0;
     if (const char *ev = std::getenv("FBLTS_FUSE")) c->fuse_vel = std::atoi(ev) != 0;
+    if (const char *ev = std::getenv("FBLTS_SUB")) c->fuse_sub = std::atoi(ev) != 0;
+    if (const char *ev = std::getenv("FBLTS_SUB_LEVEL")) c->sub_level = std::min(5, std::max(2, std::atoi(ev)));
+    if (cfg->nranks != 1 || cfg->scheme != FBLTS_SCHEME_FBLTS || cfg->slow_refresh || cfg->unsplit) c->fuse_sub = false;
     // canonical constants (computed once in double, SURVEY c.1)
     StepConst &s = c->sc;
     const double dt = cfg->dt;
@@ -550,6 +562,143 @@ int build_tiles(fblts_ctx *c) {
     return FBLTS_OK;
 }
 
+// Subcycle tiles (fblts_internal.h SubTileMesh): the tiles of build_tiles that lie in F\F^2 of the
+// (single) owned block, each with its rings R1-R3, the edges of its rings 0-2 and their slot tables.
+// A cell of F\F^2 is at least 5 hops from every coarse cell (r = 2), so its 3-ring neighbourhood is
+// fine (a fine cell's value is its fine data in every view): the tile needs no region views, and
+// the band kernels (cells of F^1 and coarser, at most 3 hops into F) never read its cells.
+int build_subtiles(fblts_ctx *c) {
+    c->s_nT = 0;
+    c->s_info.assign(FTINFO, 0);
+    c->s_halo.clear();
+    c->s_fedge.clear();
+    c->s_ecl.clear();
+    c->s_row.clear();
+    c->s_hmax = c->s_emax = c->s_rmax = 0;
+    const Local &L = c->lo;
+    if (!c->fuse_sub || L.cbI.end > L.cbI.begin || c->t_start.size() < 2) {
+        c->fuse_sub = false;
+        return FBLTS_OK;
+    }
+    // the bulk F\F^5 by default: the thin 2-hop bands F^3\F^2 .. F^5\F^4 cut into 256-cell tiles are
+    // long strips whose 3-ring halos would triple the tile (FBLTS_SUB_LEVEL = 2..5 moves the start)
+    const int G = c->ecS, maxE = c->hm.maxE, lo = L.cb.fl[c->sub_level], hi = L.cb.end;
+    std::vector<int8_t> ring(L.nC, -1);
+    std::vector<int32_t> lidx(L.nC, -1);
+    std::vector<int32_t> R[4], el, fl[3];
+    auto nbr = [&](int i, int j) { return c->d_ec[((size_t)i * G + j) * 2 + 1]; };
+    auto edg = [&](int i, int j) {
+        const int es = c->d_ec[((size_t)i * G + j) * 2];
+        return es >= 0 ? es : ~es;
+    };
+    const int nT = (int)c->t_start.size() - 1;
+    for (int t = 0; t < nT; ++t) {
+        const int c0 = c->t_start[t], c1 = c->t_start[t + 1];
+        if (c0 < lo || c0 >= hi) continue;
+        R[0].clear();
+        for (int i = c0; i < c1; ++i) R[0].push_back(i), ring[i] = 0;
+        for (int k = 1; k <= 3; ++k) {
+            R[k].clear();
+            for (int i : R[k - 1])
+                for (int j = 0; j < c->d_nEoC[i]; ++j) {
+                    const int nb = nbr(i, j);
+                    if (nb < 0 || nb >= L.nOwnC) return fail(c, FBLTS_ERR_LABELS, "subtiles: tile %d reaches a halo cell", t);
+                    if (ring[nb] < 0) ring[nb] = (int8_t)k, R[k].push_back(nb);
+                }
+            std::sort(R[k].begin(), R[k].end());
+        }
+        for (int k = 1; k <= 3; ++k)
+            for (int x : R[k])
+                if (x < L.cb.f)
+                    return fail(c, FBLTS_ERR_LABELS, "subtiles: tile %d: ring-%d cell %d is not fine", t, k, x);
+        const int nOwn = c1 - c0, n1 = (int)R[1].size(), n2 = (int)R[2].size(), n3 = (int)R[3].size();
+        int q = 0;
+        for (int i = c0; i < c1; ++i) lidx[i] = i - c0;
+        for (int k = 1; k <= 3; ++k)
+            for (int x : R[k]) lidx[x] = HALO0 + q++;
+        bool border = false;
+        for (int x : R[1]) border = border || x < lo;
+        // local edges: every edge of a ring-0..2 cell; owned run of the staged tile, foreign by ring
+        el.clear();
+        for (int k = 0; k <= 2; ++k)
+            for (int i : R[k])
+                for (int j = 0; j < c->d_nEoC[i]; ++j) el.push_back(edg(i, j));
+        std::sort(el.begin(), el.end());
+        el.erase(std::unique(el.begin(), el.end()), el.end());
+        const int32_t *trec = &c->t_info[(size_t)t * TINFO];
+        const int eo0 = trec[2], eo1 = trec[3], nOE = eo1 - eo0;
+        for (auto &f : fl) f.clear();
+        for (int e : el) {
+            const int r0 = ring[c->d_coe[2 * e]], r1 = ring[c->d_coe[2 * e + 1]];
+            if (r0 < 0 || r1 < 0) return fail(c, FBLTS_ERR_LABELS, "subtiles: edge %d leaves the 3-ring set", e);
+            const int mr = std::min(r0, r1);
+            if (e >= eo0 && e < eo1) {
+                if (mr != 0) return fail(c, FBLTS_ERR_LABELS, "subtiles: owned edge %d not on the tile", e);
+                continue;
+            }
+            fl[mr].push_back(e);
+        }
+        const int nF = (int)(fl[0].size() + fl[1].size() + fl[2].size());
+        if (nOE + FGAP + nF >= 0x7FFF || HALO0 + n1 + n2 + n3 > 0xFFFF)
+            return fail(c, FBLTS_ERR_MESH, "subtiles: tile %d has %d edges / %d halo cells (too many)", t, nOE + nF,
+                        n1 + n2 + n3);
+        int32_t *rec = &c->s_info[(size_t)c->s_nT * FTINFO];
+        rec[0] = c0, rec[1] = c1, rec[2] = (int32_t)c->s_halo.size(), rec[3] = n1, rec[4] = n2, rec[5] = n3;
+        rec[6] = eo0, rec[7] = eo1, rec[8] = (int32_t)c->s_fedge.size();
+        rec[9] = (int32_t)fl[0].size(), rec[10] = (int32_t)fl[1].size(), rec[11] = (int32_t)fl[2].size();
+        rec[12] = (int32_t)c->s_ecl.size(), rec[13] = (int32_t)c->s_row.size(), rec[14] = border ? 1 : 0;
+        for (int k = 1; k <= 3; ++k) c->s_halo.insert(c->s_halo.end(), R[k].begin(), R[k].end());
+        // local edge index (q-space: owned run, FGAP, foreign list)
+        std::vector<std::pair<int, int>> fpos;     // (edge, q) for the foreign edges
+        int p = 0;
+        for (auto &f : fl)
+            for (int e : f) {
+                c->s_fedge.push_back(e);
+                fpos.push_back({e, nOE + FGAP + p++});
+            }
+        std::sort(fpos.begin(), fpos.end());
+        auto ledge = [&](int e) {
+            if (e >= eo0 && e < eo1) return e - eo0;
+            return std::lower_bound(fpos.begin(), fpos.end(), std::make_pair(e, -1))->second;
+        };
+        auto pair = [&](int e) {
+            return (uint32_t)lidx[c->d_coe[2 * e + 1]] << 16 | (uint32_t)lidx[c->d_coe[2 * e]];
+        };
+        for (int e = eo0; e < eo1; ++e) c->s_ecl.push_back(pair(e));
+        for (auto &f : fl)
+            for (int e : f) c->s_ecl.push_back(pair(e));
+        const int nR2 = nOwn + n1 + n2;
+        const size_t rb = c->s_row.size();
+        c->s_row.resize(rb + (size_t)maxE * nR2, TILE_SENT);
+        int r = 0;
+        for (int k = 0; k <= 2; ++k)
+            for (int i : R[k]) {
+                for (int j = 0; j < c->d_nEoC[i]; ++j) {
+                    const int es = c->d_ec[((size_t)i * G + j) * 2];
+                    c->s_row[rb + (size_t)j * nR2 + r] = (uint16_t)((es < 0 ? 0x8000u : 0u) | ledge(es >= 0 ? es : ~es));
+                }
+                ++r;
+            }
+        c->s_row.resize((c->s_row.size() + 7) & ~(size_t)7, TILE_SENT);     // 16-byte aligned tables
+        c->s_rmax = std::max(c->s_rmax, (int)(c->s_row.size() - rb));
+        c->s_hmax = std::max(c->s_hmax, n1 + n2 + n3);
+        c->s_emax = std::max(c->s_emax, nOE + FGAP + nF);
+        for (int k = 0; k <= 3; ++k)
+            for (int x : R[k]) ring[x] = -1, lidx[x] = -1;
+        ++c->s_nT;
+        c->s_info.resize((size_t)(c->s_nT + 1) * FTINFO, 0);
+    }
+    c->s_nHalo = c->s_halo.size(), c->s_nFedge = c->s_fedge.size(), c->s_nEcl = c->s_ecl.size();
+    c->s_nRow = c->s_row.size();
+    if (c->s_halo.empty()) c->s_halo.push_back(0);
+    if (c->s_fedge.empty()) c->s_fedge.push_back(0);
+    if (c->s_ecl.empty()) c->s_ecl.push_back(0);
+    if (c->s_row.empty()) c->s_row.push_back(0);
+    if (c->s_nT == 0 || sub_smem_bytes_host(c->s_hmax, c->s_emax, c->s_rmax) > TILE_SMEM_MAX) c->fuse_sub = false;
+    return FBLTS_OK;
+}
+
+
 // first tile of the tile run starting at owned cell `cell` (a region block boundary)
 int tile_at(const fblts_ctx *c, int cell) {
     return (int)(std::lower_bound(c->t_start.begin(), c->t_start.end(), cell) - c->t_start.begin());
@@ -805,7 +954,9 @@ int build_local(fblts_ctx *c, const std::vector<int32_t> &coc) {
         c->d_xidx.insert(c->d_xidx.end(), L.x[x].recvIdx.begin(), L.x[x].recvIdx.end());
     }
     if (c->d_xidx.empty()) c->d_xidx.push_back(0);
-    return build_tiles(c);
+    const int rc = build_tiles(c);
+    if (rc) return rc;
+    return build_subtiles(c);
 }
 
 }  // namespace
@@ -884,6 +1035,10 @@ int fblts_get_counts(fblts_ctx *c, int64_t *out) {
     out[25] = (int64_t)c->t_nHalo;
     out[26] = (int64_t)c->t_nEcl;
     out[27] = stage_tiled_smem_bytes_host(3, c->t_hmax, c->t_emax);
+    out[28] = c->fuse_sub ? c->s_nT : 0;
+    out[29] = c->fuse_sub ? (int64_t)c->s_nHalo : 0;
+    out[30] = c->fuse_sub ? (int64_t)c->s_nFedge : 0;
+    out[31] = c->fuse_sub ? sub_smem_bytes_host(c->s_hmax, c->s_emax, c->s_rmax) : 0;
     return FBLTS_OK;
 }
 
@@ -998,6 +1153,25 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
     put(tFedge, std::max<size_t>(1, c->t_nFedge));
     put(tEcl, std::max<size_t>(1, c->t_nEcl));
     put(tRow, (size_t)c->hm.maxE * c->t_sRow);
+    const bool fs = c->fuse_sub;
+    put(s.hT2, fs ? (size_t)L.nC : 1);
+    put(s.h2alt, fs ? (size_t)L.nC : 1);
+    SubTileMesh &sm = c->dm.st;
+    int32_t *sInfo, *sHalo, *sFedge;
+    uint32_t *sEcl;
+    uint16_t *sRow;
+    put(sInfo, fs ? c->s_info.size() : 1);
+    put(sHalo, fs ? std::max<size_t>(1, c->s_nHalo) : 1);
+    put(sFedge, fs ? std::max<size_t>(1, c->s_nFedge) : 1);
+    put(sEcl, fs ? std::max<size_t>(1, c->s_nEcl) : 1);
+    put(sRow, fs ? std::max<size_t>(1, c->s_nRow) : 1);
+    if (base) {
+        sm.nTiles = fs ? c->s_nT : 0;
+        sm.hmax = c->s_hmax;
+        sm.emax = c->s_emax;
+        sm.rmax = c->s_rmax;
+        sm.info = sInfo, sm.halo = sHalo, sm.fedge = sFedge, sm.ecl = sEcl, sm.row = sRow;
+    }
     if (base) {
         tm.nTiles = (int32_t)c->t_start.size() - 1;
         tm.strideRow = c->t_sRow;
@@ -1086,6 +1260,14 @@ int fblts_bind_workspace(fblts_ctx *c, void *ptr, size_t bytes) {
     CUDA_TRY(c, up(tm.fedge, c->t_fedge.data(), c->t_fedge.size() * 4));
     CUDA_TRY(c, up(tm.ecl, c->t_ecl.data(), c->t_ecl.size() * 4));
     CUDA_TRY(c, up(tm.row, c->t_row.data(), c->t_row.size() * 2));
+    if (c->fuse_sub) {
+        const SubTileMesh &sm = d.st;
+        CUDA_TRY(c, up(sm.info, c->s_info.data(), c->s_info.size() * 4));
+        CUDA_TRY(c, up(sm.halo, c->s_halo.data(), c->s_halo.size() * 4));
+        CUDA_TRY(c, up(sm.fedge, c->s_fedge.data(), c->s_fedge.size() * 4));
+        CUDA_TRY(c, up(sm.ecl, c->s_ecl.data(), c->s_ecl.size() * 4));
+        CUDA_TRY(c, up(sm.row, c->s_row.data(), c->s_row.size() * 2));
+    }
     if (stage_tiled_smem_bytes_host(4, c->t_hmax, c->t_emax) > TILE_SMEM_MAX) c->split = true;    // size launches per block
     if (stage_tiled_smem_bytes_host(4, c->t_hmax, c->t_emax) > TILE_SMEM_MAX && !c->split) c->tiled = false;
     CUDA_TRY(c, cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->cfg.device));
@@ -1099,6 +1281,10 @@ int fblts_bind_workspace(fblts_ctx *c, void *ptr, size_t bytes) {
     std::vector<int32_t>().swap(c->t_fedge);
     std::vector<uint32_t>().swap(c->t_ecl);
     std::vector<uint16_t>().swap(c->t_row);
+    std::vector<int32_t>().swap(c->s_halo);
+    std::vector<int32_t>().swap(c->s_fedge);
+    std::vector<uint32_t>().swap(c->s_ecl);
+    std::vector<uint16_t>().swap(c->s_row);
     c->phase = P_BOUND;
     return FBLTS_OK;
 }
@@ -1250,7 +1436,12 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
         if (rec) rec->mark(k, s);
     };
     const int M = sc.M;
-    auto hb = [&](int k) { return ((M - 1 - k) % 2 == 0) ? hNew : st.hT; };
+    const bool T = c->tiled;
+    // fused subcycle on F\F^2: the fine levels k-1, k, k+1 live in three distinct buffers (a tile
+    // reads level k-1 on its rings while its neighbours write level k+1); level M lands in hNew
+    const bool SUB = T && c->fuse_sub && m.st.nTiles > 0 && c->deep_runs_ok;
+    double *hrot[3] = {hNew, st.hT, st.hT2};
+    auto hb = [&](int k) { return SUB ? hrot[(M - 1 - k) % 3] : (((M - 1 - k) % 2 == 0) ? hNew : st.hT); };
     auto ub = [&](int k) { return ((M - 1 - k) % 2 == 0) ? uNew : st.uT; };
     auto pred = [&](int k) {
         PredConst pc;
@@ -1262,7 +1453,8 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
         pc.c = 1.0 - (double)(k + 1) / (double)M;
         return pc;
     };
-    const bool T = c->tiled;
+    const int subBegin = B.fl[c->sub_level];
+    const int deepEnd = SUB ? subBegin : B.end;    // the staged deep kernels stop where the subcycle tiles start
     *px = PhaseX{-1, nullptr, -1, nullptr};
     const int nfine = c->have_fine ? 3 * M : 0;
     if (ph > 3 + nfine) return false;
@@ -1305,7 +1497,7 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
         if (stg == 0) {
             // k >= 1 with the fusion: the band velocity sweep runs alone and the deep velocity sweep
             // of subcycle k-1 is folded into the deep stage-1 sweep of subcycle k (STAGE 4)
-            const bool fused = k > 0 && T && c->fuse_vel && c->deep_runs_ok;
+            const bool fused = k > 0 && T && (c->fuse_vel || SUB) && c->deep_runs_ok;
             if (part == 0) {
                 if (k == 0) {
                     mark(K_COARSE_VEL);
@@ -1325,9 +1517,22 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
                              sc.c3f, sc.b3, sc.om2b3, sc.c1f, sc.g, K_FINE_VS1, k};
                 va.h2 = st.h2;
                 va.unew = ub(k - 1);
-                stage_tiled(c, 4, B, B.fl[1], B.end, va, s);
+                stage_tiled(c, 4, B, B.fl[1], deepEnd, va, s);
             } else if (T) {
-                stage_tiled(c, 1, B, B.fl[1], B.end, StageArgs{hk, hk, uk, st.S, st.h1, 0, 0, 0, sc.c1f, sc.g, K_FINE_S1, k}, s);
+                stage_tiled(c, 1, B, B.fl[1], deepEnd, StageArgs{hk, hk, uk, st.S, st.h1, 0, 0, 0, sc.c1f, sc.g, K_FINE_S1, k}, s);
+            }
+            if (SUB && part == 0) {
+                // the whole subcycle k on F\F^2 (after the kernels above, which read level k-1 and
+                // stage 2 of k-1 there; before the stage-2/3 sweeps, which read its stage 1 / 2)
+                mark(K_FINE_SUB);
+                SubArgs sa{hk, k == 0 ? hN : (k - 1 == 0 ? hN : hb(k - 2)), st.h2, k == 0 ? uN : (k - 1 == 0 ? uN : ub(k - 2)),
+                           st.Sf, k == 0 ? nullptr : ub(k - 1), st.h1, k == 0 ? st.h2 : st.h2alt, hb(k),
+                           sc.g, sc.b1, sc.omb1, sc.b2, sc.omb2, sc.b3, sc.om2b3, sc.c1f, sc.c2f, sc.c3f, k};
+                launch_fine_sub(m, k > 0, c->nsm, sa, st.err, s);
+                if (k > 0)        // publish stage 2 (the tiles read stage 2 of k-1 on their rings)
+                    cudaMemcpyAsync(st.h2 + subBegin, st.h2alt + subBegin, (size_t)(B.end - subBegin) * 8,
+                                    cudaMemcpyDeviceToDevice, s);
+                any = true;
             }
             *px = PhaseX{X_C1, st.h1, -1, nullptr};
         } else if (stg == 1) {
@@ -1348,14 +1553,14 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
             cell_mark(K_FINE_S2);
             launch_fine_s2(m, st, hN, hNew, hk, uk, sc, pred(k), k, s, B, !T);
             if (T)
-                stage_tiled(c, 2, B, B.fl[1], B.end,
+                stage_tiled(c, 2, B, B.fl[1], deepEnd,
                             StageArgs{hk, st.h1, uk, st.Sf, st.h2, sc.c1f, sc.b1, sc.omb1, sc.c2f, sc.g, K_FINE_S2, k}, s);
             *px = PhaseX{X_C1, st.h2, -1, nullptr};
         } else {
             cell_mark(K_FINE_S3);
             launch_fine_s3(m, st, hN, uN, hNew, hk, uk, hb(k), sc, pred(k), k, s, B, !T);
             if (T)
-                stage_tiled(c, 3, B, B.fl[1], B.end,
+                stage_tiled(c, 3, B, B.fl[1], deepEnd,
                             StageArgs{hk, st.h2, uk, st.Sf, hb(k), sc.c2f, sc.b2, sc.omb2, sc.c3f, sc.g, K_FINE_S3, k}, s);
             *px = PhaseX{X_C1, hb(k), -1, nullptr};
         }

@@ -1026,6 +1026,12 @@ int stage_tiled_smem_bytes_host(int stage, int hmax, int emax) {
     return 8 * (((NBUF + 1) & ~1) + NBUF * (nca * CS2 + nea * ES2 + ES2 / 2 + 2));
 }
 
+#ifndef FBLTS_SUB_NTHR
+#define FBLTS_SUB_NTHR 512
+#endif
+template <int G, bool VEL>
+__global__ void __launch_bounds__(FBLTS_SUB_NTHR, 1) k_fine_sub(DevMesh m, int CS, int ES, int BUF, SubArgs a, DevError *err);
+
 int stage_tiled_configure(const DevMesh &m) {
     cudaError_t e = cudaSuccess;
     auto set = [&](const void *f) {      // process-wide attributes: the limit, not one context's need
@@ -1037,6 +1043,8 @@ int stage_tiled_configure(const DevMesh &m) {
         set((const void *)k_stage_tiled<G, 2>);
         set((const void *)k_stage_tiled<G, 3>);
         set((const void *)k_stage_tiled<G, 4>);
+        set((const void *)k_fine_sub<G, false>);
+        set((const void *)k_fine_sub<G, true>);
     });
     return (int)e;
 }
@@ -1059,6 +1067,287 @@ void launch_stage_tiled(const DevMesh &m, int stage, int tile0, int tile1, int h
         else if (stage == 2) k_stage_tiled<G, 2><<<grid, NTHR, smem, s>>>(m, tile0, tile1, CS, ES, a, err);
         else if (stage == 3) k_stage_tiled<G, 3><<<grid, NTHR, smem, s>>>(m, tile0, tile1, CS, ES, a, err);
         else k_stage_tiled<G, 4><<<grid, NTHR, smem, s>>>(m, tile0, tile1, CS, ES, a, err);
+    });
+}
+
+// ====================================================================== fused fine subcycle
+// A subcycle tile (fblts_internal.h SubTileMesh, a tile of F\F^5) goes through a whole fine
+// subcycle of subeqn fine_fbrk32 inside one CTA: [velocity stage 3 of subcycle k-1 on
+// the edges of rings 0-2 (VEL)], stage 1 on rings 0-2, stage 2 on rings 0-1, stage 3 on the tile,
+// every stage value kept in shared memory; the rings are recomputed redundantly by the neighbouring
+// tiles (same operands, same order: the same bits).  Per edge and stage the flux term
+// T_e = l_e ((0.5 (H_c0 + H_c1)) u_bar_e) is computed once, then summed per cell in slot order, which
+// is the staged kernels' (and the oracle's) arithmetic.  Every cell of a ring <= 3 is fine, so no
+// region views are needed.
+// Persistent CTAs (one per SM, SNT threads) walk the tiles with two shared buffers: while tile i is
+// computed, tile i+1's contiguous ranges arrive by 1-D bulk copies (mbarrier) and its ring cells and
+// foreign edges by cp.async gathers whose indices were fetched into registers before the compute.
+constexpr int SNT = FBLTS_SUB_NTHR;
+constexpr int SHPT = 1, SFPT = 3;          // ring-cell / foreign-edge indices prefetched per thread
+
+static void sub_strides(int hmax, int emax, int rmax, int &CS, int &ES, int &RS, int &BUF) {
+    CS = (HALO0 + hmax + 1 + 1) & ~1;
+    ES = (emax + FGAP + 8 + 3) & ~3;
+    RS = ((rmax + 7) / 8) * 2;             // doubles holding rmax uint16 (16-byte multiple)
+    BUF = 5 * CS + 5 * ES + ES / 2 + RS;
+}
+int sub_smem_bytes_host(int hmax, int emax, int rmax) {
+    int CS, ES, RS, BUF;
+    sub_strides(hmax, emax, rmax, CS, ES, RS, BUF);
+    return 8 * (2 + 2 * BUF);
+}
+
+struct SubRec {
+    int c0, c1, h0, n1, n2, n3, eo0, eo1, f0, nF0, nF1, nF2, l0, s0, flags;
+    __device__ __forceinline__ int nH() const { return n1 + n2 + n3; }
+    __device__ __forceinline__ int nF() const { return nF0 + nF1 + nF2; }
+};
+__device__ __forceinline__ SubRec load_subrec(const SubTileMesh &t, int tile) {
+    const int *p = t.info + (size_t)tile * FTINFO;
+    return SubRec{p[0], p[1], p[2], p[3], p[4], p[5], p[6], p[7], p[8], p[9], p[10], p[11], p[12], p[13], p[14]};
+}
+struct SubBuf {                              // views of one buffer for tile r (local index 0 = first own cell / edge)
+    double *hk, *hA, *hB, *zb, *A, *u, *S, *l, *d, *T;
+    uint32_t *ecl;
+    uint16_t *row;
+    __device__ __forceinline__ SubBuf(double *B, int CS, int ES, const SubRec &r) {
+        const int oc = r.c0 & 1, oe = r.eo0 & 1;
+        hk = B + oc, hA = B + CS + oc, hB = B + 2 * CS + oc, zb = B + 3 * CS + oc, A = B + 4 * CS + oc;
+        double *E = B + 5 * CS;
+        u = E + oe, S = E + ES + oe, l = E + 2 * ES + oe, d = E + 3 * ES + oe, T = E + 4 * ES + oe;
+        ecl = reinterpret_cast<uint32_t *>(E + 5 * ES) + (r.l0 & 3);
+        row = reinterpret_cast<uint16_t *>(E + 5 * ES + ES / 2);
+    }
+};
+
+template <bool VEL>
+__device__ __forceinline__ void sub_issue_bulk(const DevMesh &m, const SubArgs &a, const SubRec &r, double *B, int CS,
+                                               int ES, uint64_t *bar) {
+    const int nLE = r.eo1 - r.eo0 + r.nF();
+    const int ca = r.c0 & ~1, cb = (r.c1 + 1) & ~1, ea = r.eo0 & ~1, eb = (r.eo1 + 1) & ~1;
+    const int la = r.l0 & ~3, lb = (r.l0 + nLE + 3) & ~3;
+    const int nR2 = r.c1 - r.c0 + r.n1 + r.n2;
+    const unsigned cbytes = 8u * (cb - ca), ebytes = 8u * (eb - ea), lbytes = 4u * (lb - la);
+    const unsigned rbytes = 16u * ((m.maxE * nR2 + 7) / 8);   // rows are padded to 8 entries per tile
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    mbar_expect_tx(bar, (VEL ? 5u : 3u) * cbytes + (ebytes ? 4u * ebytes : 0u) + lbytes + rbytes);
+    bulk_g2s(B, a.hk + ca, cbytes, bar);
+    if (VEL) {
+        bulk_g2s(B + CS, a.hm + ca, cbytes, bar);
+        bulk_g2s(B + 2 * CS, a.h2 + ca, cbytes, bar);
+    }
+    bulk_g2s(B + 3 * CS, m.zb + ca, cbytes, bar);
+    bulk_g2s(B + 4 * CS, m.areaCell + ca, cbytes, bar);
+    double *E = B + 5 * CS;
+    if (ebytes) {
+        bulk_g2s(E, a.ubase + ea, ebytes, bar);
+        bulk_g2s(E + ES, a.S + ea, ebytes, bar);
+        bulk_g2s(E + 2 * ES, m.dv + ea, ebytes, bar);
+        bulk_g2s(E + 3 * ES, m.dc + ea, ebytes, bar);
+    }
+    bulk_g2s(E + 5 * ES, m.st.ecl + la, lbytes, bar);
+    bulk_g2s(E + 5 * ES + ES / 2, m.st.row + r.s0, rbytes, bar);
+}
+
+__device__ __forceinline__ void sub_load_idx(const SubTileMesh &t, const SubRec &r, int tid, int (&hx)[SHPT],
+                                             int (&fx)[SFPT]) {
+#pragma unroll
+    for (int k = 0; k < SHPT; ++k) {
+        const int q = k * SNT + tid;
+        hx[k] = q < r.nH() ? t.halo[r.h0 + q] : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < SFPT; ++k) {
+        const int q = k * SNT + tid;
+        fx[k] = q < r.nF() ? t.fedge[r.f0 + q] : 0;
+    }
+}
+
+template <bool VEL>
+__device__ __forceinline__ void sub_issue_gather(const DevMesh &m, const SubArgs &a, const SubRec &r, const SubBuf &b,
+                                                 int tid, const int (&hx)[SHPT], const int (&fx)[SFPT]) {
+    const int nH = r.nH(), nF = r.nF(), n12 = r.n1 + r.n2, n01 = r.nF0 + r.nF1, nOE = r.eo1 - r.eo0;
+    // ring cells: h^{n,k} on R1-R3; z_b on R1-R3 (VEL) or R1-R2; A on R1-R2; h^{n,k-1}, h2 on R1-R3 (VEL)
+    auto cell = [&](int q, int x) {
+        cp_async8(b.hk + HALO0 + q, a.hk + x);
+        if (VEL) {
+            cp_async8(b.hA + HALO0 + q, a.hm + x);
+            cp_async8(b.hB + HALO0 + q, a.h2 + x);
+        }
+        if (VEL || q < n12) cp_async8(b.zb + HALO0 + q, m.zb + x);
+        if (q < n12) cp_async8(b.A + HALO0 + q, m.areaCell + x);
+    };
+    // foreign edges: u, l on all; S, d where a velocity is formed (all with VEL, rings 0-1 without)
+    auto edge = [&](int p, int e) {
+        const int q = nOE + FGAP + p;
+        cp_async8(b.u + q, a.ubase + e);
+        cp_async8(b.l + q, m.dv + e);
+        if (VEL || p < n01) {
+            cp_async8(b.S + q, a.S + e);
+            cp_async8(b.d + q, m.dc + e);
+        }
+    };
+#pragma unroll
+    for (int k = 0; k < SHPT; ++k)
+        if (k * SNT + tid < nH) cell(k * SNT + tid, hx[k]);
+    for (int q = SHPT * SNT + tid; q < nH; q += SNT) cell(q, m.st.halo[r.h0 + q]);
+#pragma unroll
+    for (int k = 0; k < SFPT; ++k)
+        if (k * SNT + tid < nF) edge(k * SNT + tid, fx[k]);
+    for (int p = SFPT * SNT + tid; p < nF; p += SNT) edge(p, m.st.fedge[r.f0 + p]);
+}
+
+template <int G, bool VEL>
+__global__ void __launch_bounds__(SNT, 1) k_fine_sub(DevMesh m, int CS, int ES, int BUF, SubArgs a, DevError *err) {
+    extern __shared__ __align__(16) double smem[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);   // 2 mbarriers
+    double *buf0 = smem + 2;
+    const SubTileMesh &t = m.st;
+    const int tid = threadIdx.x, G0 = gridDim.x, nT = t.nTiles;
+    int tile = blockIdx.x;
+    if (tile >= nT) return;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    // the ring-cell / foreign-edge indices run one tile ahead of the copies: tile i+1's gathers are
+    // issued as soon as tile i is staged (indices already in registers) and tile i+2's indices load
+    // during tile i's compute
+    int hx[SHPT], fx[SFPT];
+    {
+        const SubRec r0 = load_subrec(t, tile);
+        if (tid == 0) sub_issue_bulk<VEL>(m, a, r0, buf0, CS, ES, &bar[0]);
+        sub_load_idx(t, r0, tid, hx, fx);
+        sub_issue_gather<VEL>(m, a, r0, SubBuf(buf0, CS, ES, r0), tid, hx, fx);
+        cp_async_commit();
+        if (tile + G0 < nT) sub_load_idx(t, load_subrec(t, tile + G0), tid, hx, fx);
+    }
+    unsigned phase = 0u;
+    int buf = 0;
+    for (; tile < nT; tile += G0, buf ^= 1) {
+        const SubRec r = load_subrec(t, tile);
+        const bool more = tile + G0 < nT;
+        SubRec nx{};
+        if (more) nx = load_subrec(t, tile + G0);
+        mbar_wait(&bar[buf], (phase >> buf) & 1u);
+        phase ^= 1u << buf;
+        cp_async_wait_pending<0>();
+        __syncthreads();                                  // tile r staged; the other buffer is free
+        double *Bn = buf0 + (buf ^ 1) * BUF;
+        if (more) {
+            if (tid == 0) sub_issue_bulk<VEL>(m, a, nx, Bn, CS, ES, &bar[buf ^ 1]);
+            sub_issue_gather<VEL>(m, a, nx, SubBuf(Bn, CS, ES, nx), tid, hx, fx);
+            if (tile + 2 * G0 < nT) sub_load_idx(t, load_subrec(t, tile + 2 * G0), tid, hx, fx);
+        }
+        cp_async_commit();
+        const SubBuf b(buf0 + buf * BUF, CS, ES, r);
+        const int nOwn = r.c1 - r.c0, nOE = r.eo1 - r.eo0;
+        const int nLE0 = nOE + r.nF0, nLE1 = nLE0 + r.nF1, nLE2 = nLE1 + r.nF2;
+        const int nR1 = nOwn + r.n1, nR2 = nR1 + r.n2;
+        // ---- edges of rings 0-2: u^{n,k} (VEL: velocity stage 3 of subcycle k-1) and the stage-1 flux
+        for (int p = tid; p < nLE2; p += SNT) {
+            const uint32_t pr = b.ecl[p];
+            const int q = p < nOE ? p : p + FGAP;
+            const int x0 = pr & 0xFFFF, x1 = pr >> 16;
+            const double H0 = b.hk[x0], H1 = b.hk[x1];
+            double ue = b.u[q];
+            if (VEL) {
+                const double HS0 = a.b3 * H0 + a.om2b3 * b.hB[x0] + a.b3 * b.hA[x0];
+                const double HS1 = a.b3 * H1 + a.om2b3 * b.hB[x1] + a.b3 * b.hA[x1];
+                const double phi = phi_fast(a.g, HS0, b.zb[x0], HS1, b.zb[x1], b.d[q]);
+                ue = ue + a.c3f * (phi + b.S[q]);
+                if (p < nOE) a.unew[r.eo0 + p] = ue;
+                b.u[q] = ue;
+            }
+            const double Fe = (0.5 * (H0 + H1)) * ue;
+            b.T[q] = b.l[q] * Fe;
+        }
+        __syncthreads();
+        // cell-phase helper: -(sum of the signed flux terms of row rr in slot order) / A
+        auto psi_row = [&](int rr, int x) {
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+                if (j < m.maxE) {
+                    const uint16_t sl = b.row[j * nR2 + rr];
+                    if (sl != TILE_SENT) {
+                        const double tt = b.T[sl & 0x7FFF];
+                        acc = acc + ((sl >> 15) ? -tt : tt);
+                    }
+                }
+            }
+            return -acc / b.A[x];
+        };
+        // ---- stage 1 on rows 0..nR2 (rings 0-2) -> hA
+        for (int rr = tid; rr < nR2; rr += SNT) {
+            const int x = rr < nOwn ? rr : HALO0 + rr - nOwn;
+            const double v = b.hk[x] + a.c1f * psi_row(rr, x);
+            b.hA[x] = v;
+            if (rr < nOwn) {
+                if (r.flags & 1) a.h1out[r.c0 + rr] = v;
+                if (!(v > 0.0)) report(err, K_FINE_S1, a.k, r.c0 + rr, v);
+            }
+        }
+        __syncthreads();
+        // ---- stage-2 flux on the edges of rings 0-1: u_bar = u^{n,k} + dt/(3M) (Phi^fast(h*) + S)
+        for (int p = tid; p < nLE1; p += SNT) {
+            const uint32_t pr = b.ecl[p];
+            const int q = p < nOE ? p : p + FGAP;
+            const int x0 = pr & 0xFFFF, x1 = pr >> 16;
+            const double H0 = b.hA[x0], H1 = b.hA[x1];
+            const double HS0 = a.b1 * H0 + a.omb1 * b.hk[x0];
+            const double HS1 = a.b1 * H1 + a.omb1 * b.hk[x1];
+            const double phi = phi_fast(a.g, HS0, b.zb[x0], HS1, b.zb[x1], b.d[q]);
+            const double ue = b.u[q] + a.c1f * (phi + b.S[q]);
+            const double Fe = (0.5 * (H0 + H1)) * ue;
+            b.T[q] = b.l[q] * Fe;
+        }
+        __syncthreads();
+        // ---- stage 2 on rows 0..nR1 (rings 0-1) -> hB
+        for (int rr = tid; rr < nR1; rr += SNT) {
+            const int x = rr < nOwn ? rr : HALO0 + rr - nOwn;
+            const double v = b.hk[x] + a.c2f * psi_row(rr, x);
+            b.hB[x] = v;
+            if (rr < nOwn) {
+                a.h2out[r.c0 + rr] = v;
+                if (!(v > 0.0)) report(err, K_FINE_S2, a.k, r.c0 + rr, v);
+            }
+        }
+        __syncthreads();
+        // ---- stage-3 flux on the tile's edges: u_bar = u^{n,k} + dt/(2M) (Phi^fast(h**) + S)
+        for (int p = tid; p < nLE0; p += SNT) {
+            const uint32_t pr = b.ecl[p];
+            const int q = p < nOE ? p : p + FGAP;
+            const int x0 = pr & 0xFFFF, x1 = pr >> 16;
+            const double H0 = b.hB[x0], H1 = b.hB[x1];
+            const double HS0 = a.b2 * H0 + a.omb2 * b.hk[x0];
+            const double HS1 = a.b2 * H1 + a.omb2 * b.hk[x1];
+            const double phi = phi_fast(a.g, HS0, b.zb[x0], HS1, b.zb[x1], b.d[q]);
+            const double ue = b.u[q] + a.c2f * (phi + b.S[q]);
+            const double Fe = (0.5 * (H0 + H1)) * ue;
+            b.T[q] = b.l[q] * Fe;
+        }
+        __syncthreads();
+        // ---- stage 3 on the tile -> h^{n,k+1}
+        for (int rr = tid; rr < nOwn; rr += SNT) {
+            const double v = b.hk[rr] + a.c3f * psi_row(rr, rr);
+            a.out[r.c0 + rr] = v;
+            if (!(v > 0.0)) report(err, K_FINE_S3, a.k, r.c0 + rr, v);
+        }
+    }
+}
+
+void launch_fine_sub(const DevMesh &m, bool vel, int nsm, const SubArgs &a, DevError *err, cudaStream_t s) {
+    if (m.st.nTiles <= 0) return;
+    int CS, ES, RS, BUF;
+    sub_strides(m.st.hmax, m.st.emax, m.st.rmax, CS, ES, RS, BUF);
+    const int smem = sub_smem_bytes_host(m.st.hmax, m.st.emax, m.st.rmax);
+    const int grid = std::max(1, std::min(m.st.nTiles, nsm));
+    FBLTS_DISPATCH_G(m.ecS, {
+        if (vel) k_fine_sub<G, true><<<grid, SNT, smem, s>>>(m, CS, ES, BUF, a, err);
+        else k_fine_sub<G, false><<<grid, SNT, smem, s>>>(m, CS, ES, BUF, a, err);
     });
 }
 

@@ -58,7 +58,8 @@ class Solver:
                 "cells_by_region": c[3:12].tolist(), "edges_by_region": c[12:21].tolist(),
                 "owned_cells": int(c[21]), "owned_edges": int(c[22]), "kernels_per_step": int(c[23]),
                 "tiles": int(c[24]), "tile_halo_cells": int(c[25]), "tile_edges": int(c[26]),
-                "tile_smem_bytes": int(c[27])}
+                "tile_smem_bytes": int(c[27]), "sub_tiles": int(c[28]), "sub_halo_cells": int(c[29]),
+                "sub_foreign_edges": int(c[30]), "sub_smem_bytes": int(c[31])}
 
     # --- state and stepping
     def set_state(self, h, u, t=0.0):

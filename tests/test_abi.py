@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(abi):
 
 def test_kernel_names(abi):
     names = [abi.fblts_kernel_name(k) for k in range(abi.NUM_KERNELS)]
-    assert names[0] == "slow_pre" and names[-1] == "slow_refresh" and len(set(names)) == abi.NUM_KERNELS
+    assert names[0] == "slow_pre" and names[-1] == "fine_sub" and len(set(names)) == abi.NUM_KERNELS
 
 
 @pytest.mark.parametrize("which", ["cfg1", "shelf", "shelf_big"])

@@ -440,3 +440,30 @@ def test_unsplit_matches_oracle(Solver, which, M):
     s.close()
     eh, eu = assert_parity(hg, ug, ho, uo)
     print(f"unsplit {which} M={M}: eps_h={eh:.3e} eps_u={eu:.3e} bitwise={np.array_equal(hg, ho) and np.array_equal(ug, uo)}")
+
+
+@pytest.mark.parametrize("M", [1, 2, 4])
+def test_fused_subcycle_matches_oracle(Solver, monkeypatch, M):
+    """The fused fine subcycle (one CTA advances a tile of F\\F^5 -- or of F\\F^2 with
+    FBLTS_SUB_LEVEL=2 -- through velocity stage 3 of subcycle k-1 and thickness stages 1-3 of k,
+    recomputing the stage values on its rings; opt-in, FBLTS_SUB=1) evaluates the same formulas as the
+    per-stage sweeps: bitwise equal to them (the default) and to the oracle, on a 256 x 256 block of
+    the config-5 recipe."""
+    c = configs.config5(nx=256, ny=256)
+    c.dt = c.dt * M / c.M                  # the same fine step dt/M for every M (stable)
+    n = 3
+    ho, uo, _ = run_oracle(c, n, M=M)
+    res = []
+    for env in ({"FBLTS_SUB": "1"}, {"FBLTS_SUB": "1", "FBLTS_SUB_LEVEL": "2"}, {}):
+        for k in ("FBLTS_SUB", "FBLTS_SUB_LEVEL"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        s, hg, ug, _ = run_gpu(Solver, c, n, M=M)
+        cnt = s.counts()
+        assert (cnt["sub_tiles"] > 0) == ("FBLTS_SUB" in env), cnt
+        s.close()
+        res.append((hg, ug))
+    for hg, ug in res:
+        assert_parity(hg, ug, ho, uo)
+        assert np.array_equal(hg, ho) and np.array_equal(ug, uo)
