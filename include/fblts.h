@@ -124,6 +124,10 @@ typedef struct {
     int32_t unsplit;     /* 1: unsplit FB-LTS: the full Phi(U, HS) =
                             Phi^fast + Phi^slow in every velocity update, stage velocities stored;
                             one rank, FB-LTS scheme, no slow refresh.  0: split mode (the paper's runs) */
+    int32_t pv_energy;   /* 1: energy-conserving PV flux in the slow tendency (the variant
+                            of reading Q2): q_hat_e F_perp_e is replaced by
+                            sum_j W_{e,j} F_{e_j} (q_hat_e + q_hat_{e_j}) / 2, which does no work
+                            (sum_e l_e d_e F_e PV_e = 0); one rank, no slow refresh.  0: centred q_hat */
 } fblts_config;
 
 #define FBLTS_SCHEME_FBLTS 0
@@ -186,8 +190,11 @@ int fblts_set_forcing(fblts_ctx *ctx, const double *tau_n);
  * (S at t^n).  Errors: INVALID_ARG (non-finite wind or coefficients), ORDER (before bind), CUDA. */
 int fblts_set_hurricane(fblts_ctx *ctx, const double *uw_n, const double *uw_t, double cd, double cw);
 
-/* Initial state, HOST arrays in original order: h [nCells] (m), u [nEdges] (m/s), t (s).
- * Errors: STATE (h <= 0 or non-finite at index i), ORDER. */
+/* Initial state, HOST arrays in original order: h [nCells] (m), u [nEdges] (m/s), t (s); copied
+ * (synchronous; pinned host memory makes the copies DMA-speed).  The arrays are checked on the
+ * device after the copy.  Errors: STATE (h <= 0 or non-finite, u non-finite; the message names the
+ * smallest offending index; the context then holds no valid state until the next successful
+ * set_state), ORDER, CUDA. */
 int fblts_set_state(fblts_ctx *ctx, const double *h, const double *u, double t);
 
 /* Enqueue n_coarse coarse steps on cfg.stream (asynchronous, CUDA-graph replay). */

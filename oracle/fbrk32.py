@@ -24,6 +24,9 @@ class Phys:
     (eq. hurricane_fast_terms, P:L1222-1230), evaluated with g_fast = g (1 - sal);
     cd: bottom-drag coefficient C_D; cw: wind coefficient C_W; uw_n, uw_t: per-edge normal and
     tangential components of the wind velocity u_W (None: no drag / wind terms).
+    pv: the PV flux term of the slow tendency -- "centered": q_hat_e F_perp_e with
+    q_hat_e = (q_v0 + q_v1) / 2 (reading Q2, the paper's symbol); "energy": the
+    energy-conserving TRiSK form sum_j W_{e,j} F_{e_j} (q_hat_e + q_hat_{e_j}) / 2.
     """
     g: float = 9.81
     beta: tuple = BETA_PAPER
@@ -35,6 +38,7 @@ class Phys:
     cw: float = 0.0
     uw_n: np.ndarray | None = None
     uw_t: np.ndarray | None = None
+    pv: str = "centered"
 
     def g_fast(self):
         """g (1 - beta_SAL): the gravity of the fast term -g grad(xi - beta xi)."""

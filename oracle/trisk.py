@@ -122,6 +122,25 @@ def perp_flux(mesh, F_all, edges):
     return acc
 
 
+def pv_flux_energy(mesh, F_all, q_hat, edges):
+    """Energy-conserving PV flux term sum_j W_{e,j} F_{eoe_j} (q_hat_e + q_hat_{eoe_j}) / 2: the
+    symmetric pairwise PV average inside the F_perp sum (the variant of reading Q2).
+    With l_e d_e W_{e,e'} antisymmetric (pin P7) the term does no work on the flow:
+    sum_e l_e d_e F_e PV_e = 0.  Evaluated per slot as (W * F) * (0.5 * (q_e + q_e')), summed
+    sequentially in slot order from +0.0."""
+    edges = np.asarray(edges)
+    acc = np.zeros(edges.size)
+    nE2 = mesh.nEdgesOnEdge[edges]
+    for j in range(mesh.maxEdges2):
+        act = j < nE2
+        if not np.any(act):
+            break
+        e = edges[act]
+        ej = mesh.edgesOnEdge[e, j]
+        acc[act] = acc[act] + mesh.weightsOnEdge[e, j] * F_all[ej] * (0.5 * (q_hat[e] + q_hat[ej]))
+    return acc
+
+
 def kinetic_energy(mesh, U):
     """K_i = (1/A_i) sum_{e in E_i} (l_e d_e / 4) u_e^2 on every cell.
 
@@ -169,8 +188,9 @@ def slow_momentum(mesh, U, H, tau_n, rho0, phys=None):
      as  q_hat_e F_perp_e - (K[c1] - K[c0]) / d_e   (sign reading Q5:
     F_perp along +t_e, so the PV term enters with +), plus the wind-stress-like
     forcing G_e = (tau . n_e) / (rho0 h_e) (reading Q19; config 2 and 5).
-    q_hat_e = 0.5 (q[v0] + q[v1]) (reading Q2).
-    Evaluated as  (q_hat * F_perp - (K1 - K0) / d_e) + G_e.
+    q_hat_e = 0.5 (q[v0] + q[v1]) (reading Q2); phys.pv == "energy" replaces q_hat_e F_perp_e by
+    the energy-conserving pv_flux_energy.
+    Evaluated as  (PV_e - (K1 - K0) / d_e) + G_e,  PV_e = q_hat * F_perp (centred).
     """
     e = np.arange(mesh.nEdges)
     F = edge_flux(mesh, U, H, e)
@@ -178,13 +198,16 @@ def slow_momentum(mesh, U, H, tau_n, rho0, phys=None):
     v0 = mesh.verticesOnEdge[:, 0]
     v1 = mesh.verticesOnEdge[:, 1]
     q_hat = 0.5 * (q[v0] + q[v1])
-    Fperp = perp_flux(mesh, F, e)
+    if phys is not None and phys.pv == "energy":
+        PV = pv_flux_energy(mesh, F, q_hat, e)
+    else:
+        PV = q_hat * perp_flux(mesh, F, e)
     K = kinetic_energy(mesh, U)
     c0 = mesh.cellsOnEdge[:, 0]
     c1 = mesh.cellsOnEdge[:, 1]
     h_e = 0.5 * (H[c0] + H[c1])
     G = tau_n / (rho0 * h_e)
-    S = q_hat * Fperp - (K[c1] - K[c0]) / mesh.dcEdge + G
+    S = PV - (K[c1] - K[c0]) / mesh.dcEdge + G
     if phys is not None and phys.hurricane():
         D, W = hurricane_terms(mesh, U, h_e, phys)
         S = S - D + W

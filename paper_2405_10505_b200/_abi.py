@@ -45,7 +45,7 @@ class fblts_config(C.Structure):
                 ("M", C.c_int32), ("r", C.c_int32), ("slow", C.c_int32), ("device", C.c_int32),
                 ("stream", C.c_void_p), ("rank", C.c_int32), ("nranks", C.c_int32), ("nccl_id", C.c_void_p),
                 ("scheme", C.c_int32), ("slow_refresh", C.c_int32), ("sal_beta", C.c_double),
-                ("unsplit", C.c_int32)]
+                ("unsplit", C.c_int32), ("pv_energy", C.c_int32)]
 
 SCHEMES = {"fblts": 0, "rk4": 1}
 
@@ -111,14 +111,15 @@ def _arr(a, dtype):
 
 # ------------------------------------------------------------------ entry points
 def fblts_create(dt, M, g=9.81, beta=(0.531, 0.531, 0.313), rho0=1000.0, r=2, slow=True, device=0,
-                 stream=None, rank=0, nranks=1, nccl_id=None, scheme="fblts", slow_refresh=False, sal=0.0, unsplit=False):
+                 stream=None, rank=0, nranks=1, nccl_id=None, scheme="fblts", slow_refresh=False, sal=0.0, unsplit=False,
+                 pv="centered"):
     """nccl_id: 128 bytes from fblts_nccl_unique_id() on rank 0 (None: single rank or loopback group)."""
     idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id is not None else None
     cfg = fblts_config(dt=float(dt), g=float(g), beta=(C.c_double * 3)(*beta), rho0=float(rho0), M=int(M),
                        r=int(r), slow=1 if slow else 0, device=int(device), stream=stream, rank=int(rank),
                        nranks=int(nranks), nccl_id=C.cast(idbuf, C.c_void_p) if idbuf is not None else None,
                        scheme=SCHEMES[scheme], slow_refresh=1 if slow_refresh else 0, sal_beta=float(sal),
-                       unsplit=1 if unsplit else 0)
+                       unsplit=1 if unsplit else 0, pv_energy={"centered": 0, "energy": 1}[pv])
     ctx = _vp()
     rc = _lib_create(C.byref(ctx), C.byref(cfg))
     if rc != FBLTS_OK:

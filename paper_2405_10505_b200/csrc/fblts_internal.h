@@ -145,6 +145,7 @@ struct StepConst {
     double c1f, c2f, c3f;     // dt/(3M), dt/(2M), dt/M
     int32_t M;
     int32_t hur;              // hurricane drag / wind terms in the slow tendency (fblts_set_hurricane)
+    int32_t pve;              // energy-conserving PV flux (fblts_config.pv_energy)
     double cd, cw;            // C_D, C_W
 };
 
@@ -159,6 +160,7 @@ struct DevState {
     double *hN, *hNew, *h1, *h2, *hT;   // cells
     double *uN, *uNew, *uT, *S, *F;     // edges
     double *q;                          // vertices
+    double *qe;                         // q_hat per edge (energy-conserving PV flux only)
     double *K;                          // cells
     double *accH, *accU;                // accH indexed by owned cell (IF cells used), accU by e - eb.if2 (IF edges)
     double *rkU[2], *rkAccU;            // RK4 scheme: stage velocities (ping-pong) and the velocity sum
@@ -175,6 +177,7 @@ struct DevState {
     double *sendbuf, *recvbuf;          // halo exchange buffers
     int32_t *xidx;                      // halo exchange index lists (all exchanges, send then recv)
     DevError *err;
+    int32_t *vbad;                      // set_state check: first bad index of h, of u (INT_MAX-like if none)
 };
 
 // Staged stage sweep over the whole tiles [tile0, tile1) (kernels.cu): one thread per cell,
@@ -269,6 +272,8 @@ void launch_un_fstage(const DevMesh &m, const DevState &st, int stage, const dou
                       int k, cudaStream_t s);
 void launch_permute_in(const int32_t *old_of_new, const double *src, double *dst, int n, cudaStream_t s);
 void launch_permute_out(const int32_t *old_of_new, const double *src, double *dst, int n, cudaStream_t s);
+// *bad = min(*bad, first index i < n with v[i] not finite, or not > 0 when positive)
+void launch_validate(const double *v, int n, int positive, int *bad, cudaStream_t s);
 // diagnostics: writes out[4] (device) = mass, Gamma, min h, max nu
 // halo exchange: buf[k] = a[idx[k]] (pack), a[idx[k]] = buf[k] (unpack)
 void launch_pack(const int32_t *idx, const double *a, double *buf, int n, cudaStream_t s);

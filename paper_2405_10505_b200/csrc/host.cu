@@ -268,6 +268,7 @@ int fblts_create(fblts_ctx **out, const fblts_config *cfg) {
     if (cfg->slow_refresh && (cfg->nranks != 1 || cfg->scheme != FBLTS_SCHEME_FBLTS)) return FBLTS_ERR_INVALID_ARG;
     if (cfg->unsplit && (cfg->nranks != 1 || cfg->scheme != FBLTS_SCHEME_FBLTS || cfg->slow_refresh))
         return FBLTS_ERR_INVALID_ARG;
+    if (cfg->pv_energy && (cfg->nranks != 1 || cfg->slow_refresh)) return FBLTS_ERR_INVALID_ARG;
     // No CUDA call here: mesh upload, labelling and renumbering are host work, so a context
     // can be created (and its labels inspected) on a machine without a GPU.
     fblts_ctx *c = new fblts_ctx();
@@ -289,6 +290,7 @@ int fblts_create(fblts_ctx **out, const fblts_config *cfg) {
     const double M = (double)cfg->M;
     s.g = cfg->g * (1.0 - cfg->sal_beta);      // fast term -g grad(xi - beta xi)
     s.rho0 = cfg->rho0;
+    s.pve = cfg->pv_energy ? 1 : 0;
     s.b1 = cfg->beta[0];
     s.b2 = cfg->beta[1];
     s.b3 = cfg->beta[2];
@@ -1122,6 +1124,7 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
     put(s.S, L.nE);
     put(s.F, nE1);
     put(s.q, L.nV);
+    put(s.qe, c->cfg.pv_energy ? (size_t)L.nE : 1);
     put(s.accH, std::max(1, L.nOwnC));
     put(s.accU, std::max(1, L.eb.f - L.eb.if2));
     const size_t nrk = c->cfg.scheme == FBLTS_SCHEME_RK4 ? nE1 : 1;
@@ -1141,6 +1144,7 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
     put(s.edgeOld, L.nE);
     put(s.diag, 296 * 6 + 8 + 6 * 64);
     put(s.err, 1);
+    put(s.vbad, 2);
     put(s.sendbuf, c->xmax);
     put(s.recvbuf, c->xmax);
     put(s.xidx, c->d_xidx.size());
@@ -1340,20 +1344,28 @@ int fblts_set_hurricane(fblts_ctx *c, const double *uw_n, const double *uw_t, do
 int fblts_set_state(fblts_ctx *c, const double *h, const double *u, double t) {
     if (!c || !h || !u) return FBLTS_ERR_INVALID_ARG;
     if (c->phase < P_BOUND) return fail(c, FBLTS_ERR_ORDER, "set_state: bind the workspace first");
-    for (int i = 0; i < c->hm.nC; ++i)
-        if (!(std::isfinite(h[i]) && h[i] > 0.0)) return fail(c, FBLTS_ERR_STATE, "set_state: h[%d]=%g", i, h[i]);
-    for (int e = 0; e < c->hm.nE; ++e)
-        if (!std::isfinite(u[e])) return fail(c, FBLTS_ERR_STATE, "set_state: u[%d] not finite", e);
     cudaStream_t s = c->stream;
     const Local &L = c->lo;
     c->parity = 0;
+    // the input check runs on the device, on the copied arrays (first offending index reported)
+    int32_t bad[2] = {0, 0};
+    CUDA_TRY(c, cudaMemsetAsync(c->ds.vbad, 0x7F, 2 * sizeof(int32_t), s));
     CUDA_TRY(c, cudaMemcpyAsync(c->ds.stage, h, (size_t)c->hm.nC * 8, cudaMemcpyHostToDevice, s));
+    launch_validate(c->ds.stage, c->hm.nC, 1, c->ds.vbad, s);
     launch_permute_in(c->ds.cellOld, c->ds.stage, c->hbuf[0], L.nC, s);
     CUDA_TRY(c, cudaMemcpyAsync(c->ds.stage, u, (size_t)c->hm.nE * 8, cudaMemcpyHostToDevice, s));
+    launch_validate(c->ds.stage, c->hm.nE, 0, c->ds.vbad + 1, s);
     launch_permute_in(c->ds.edgeOld, c->ds.stage, c->ubuf[0], L.nE, s);
     CUDA_TRY(c, cudaGetLastError());
     CUDA_TRY(c, cudaMemsetAsync(c->ds.err, 0, sizeof(DevError), s));
+    CUDA_TRY(c, cudaMemcpyAsync(bad, c->ds.vbad, sizeof bad, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(c, cudaStreamSynchronize(s));
+    constexpr int32_t none = 0x7F7F7F7F;
+    if (bad[0] != none || bad[1] != none) {
+        c->phase = P_BOUND;                  // the device state was overwritten: no valid state now
+        if (bad[0] != none) return fail(c, FBLTS_ERR_STATE, "set_state: h[%d]=%g", bad[0], h[bad[0]]);
+        return fail(c, FBLTS_ERR_STATE, "set_state: u[%d] not finite", bad[1]);
+    }
     c->t = t;
     c->phase = P_STATE;
     return FBLTS_OK;

@@ -160,10 +160,14 @@ __global__ void __launch_bounds__(TPB) k_slow_pre(DevMesh m, const double *__res
 #ifndef FBLTS_SLOW_MINB
 #define FBLTS_SLOW_MINB 6
 #endif
-template <int MAXE2, bool HUR>
+// PVE (energy-conserving PV flux): the term q_hat_e F_perp_e becomes
+// sum_j (W_j F_eoe_j) (0.5 (q_hat_e + q_hat_eoe_j)) with q_hat per edge from k_qhat (oracle
+// trisk.pv_flux_energy); it does no work on the flow (sum_e l_e d_e F_e PV_e = 0).
+template <int MAXE2, bool HUR, bool PVE>
 __global__ void __launch_bounds__(TPB, FBLTS_SLOW_MINB) k_slow_edge(DevMesh m, const double *__restrict__ h,
                                                    const double *__restrict__ q, const double *__restrict__ K,
                                                    const double *__restrict__ F, const double *__restrict__ u,
+                                                   const double *__restrict__ qe,
                                                    double *__restrict__ S, double rho0, double cd, double cw,
                                                    int e0, int e1) {
     const int e = e0 + blockIdx.x * TPB + threadIdx.x;
@@ -173,9 +177,10 @@ __global__ void __launch_bounds__(TPB, FBLTS_SLOW_MINB) k_slow_edge(DevMesh m, c
     // with the hurricane terms also v_e = sum_j W_j u_eoe_j (tangential reconstruction)
     constexpr int CH = FBLTS_SLOW_CHUNK < MAXE2 ? FBLTS_SLOW_CHUNK : MAXE2;
     double fp = 0.0, vt = 0.0;
+    const double qs = PVE ? qe[e] : 0.0;
 #pragma unroll
     for (int j0 = 0; j0 < MAXE2; j0 += CH) {
-        double w[CH], f[CH], ut[HUR ? CH : 1];
+        double w[CH], f[CH], ut[HUR ? CH : 1], qj[PVE ? CH : 1];
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
             if (j0 + j < n && j0 + j < MAXE2) {
@@ -183,21 +188,29 @@ __global__ void __launch_bounds__(TPB, FBLTS_SLOW_MINB) k_slow_edge(DevMesh m, c
                 w[j] = m.W[(j0 + j) * m.strideE + e];
                 f[j] = F[ee];
                 if (HUR) ut[HUR ? j : 0] = u[ee];
+                if (PVE) qj[PVE ? j : 0] = qe[ee];
             }
         }
 #pragma unroll
         for (int j = 0; j < CH; ++j)
             if (j0 + j < n && j0 + j < MAXE2) {
-                fp = fp + w[j] * f[j];
+                if (PVE) fp = fp + w[j] * f[j] * (0.5 * (qs + qj[PVE ? j : 0]));
+                else fp = fp + w[j] * f[j];
                 if (HUR) vt = vt + w[j] * ut[HUR ? j : 0];
             }
     }
-    const int2 v = m.voe[e];
     const int2 c = m.coe[e];
-    const double qh = 0.5 * (q[v.x] + q[v.y]);
+    double pv;
+    if (PVE) {
+        pv = fp;
+    } else {
+        const int2 v = m.voe[e];
+        const double qh = 0.5 * (q[v.x] + q[v.y]);
+        pv = qh * fp;
+    }
     const double he = 0.5 * (h[c.x] + h[c.y]);
     const double G = m.tau[e] / (rho0 * he);
-    double s = qh * fp - (K[c.y] - K[c.x]) / m.dc[e] + G;
+    double s = pv - (K[c.y] - K[c.x]) / m.dc[e] + G;
     if (HUR) {   // bottom drag and wind (eq. hurricane_model)
         const double ue = u[e];
         const double speed = sqrt(ue * ue + vt * vt);
@@ -883,6 +896,14 @@ __global__ void k_permute_in(const int32_t *__restrict__ old, const double *__re
     const int i = blockIdx.x * TPB + threadIdx.x;
     if (i < n) dst[i] = src[old[i]];
 }
+// set_state input check on the device: bad[0] = smallest index whose value is not finite (or, with
+// positive, not > 0) -- the first offending entry, as a sequential host scan would report it
+__global__ void k_validate(const double *__restrict__ v, int n, int positive, int *bad) {
+    const int i = blockIdx.x * TPB + threadIdx.x;
+    if (i >= n) return;
+    const double x = v[i];
+    if (!(isfinite(x) && (!positive || x > 0.0))) atomicMin(bad, i);
+}
 __global__ void k_permute_out(const int32_t *__restrict__ old, const double *__restrict__ src,
                               double *__restrict__ dst, int n) {
     const int i = blockIdx.x * TPB + threadIdx.x;
@@ -1395,16 +1416,30 @@ void launch_slow_pre_range(const DevMesh &m, const DevState &st, const double *h
 void launch_slow_pre(const DevMesh &m, const DevState &st, const double *h, const double *u, cudaStream_t s) {
     launch_slow_pre_range(m, st, h, u, 0, 0, 0, s);
 }
+// q_hat_e = 0.5 (q_v0 + q_v1) on every local edge (energy-conserving PV flux only)
+__global__ void __launch_bounds__(TPB) k_qhat(DevMesh m, const double *__restrict__ q, double *__restrict__ qe) {
+    const int e = blockIdx.x * TPB + threadIdx.x;
+    if (e >= m.nE) return;
+    const int2 v = m.voe[e];
+    qe[e] = 0.5 * (q[v.x] + q[v.y]);
+}
+
 void launch_slow_edge_range(const DevMesh &m, const DevState &st, const double *h, const double *u, double *out,
                             int e0, int e1, const StepConst &sc, cudaStream_t s) {
     if (e1 <= e0) return;
     const unsigned nb = nblocks(e1 - e0);
+    if (sc.pve) k_qhat<<<nblocks(m.nE), TPB, 0, s>>>(m, st.q, st.qe);
+#define FBLTS_SLOW_EDGE3(ME2, HU, PV)                                                                              \
+    k_slow_edge<ME2, HU, PV><<<nb, TPB, 0, s>>>(m, h, st.q, st.K, st.F, u, st.qe, out, sc.rho0, sc.cd, sc.cw, e0, e1)
 #define FBLTS_SLOW_EDGE(ME2)                                                                                     \
     do {                                                                                                         \
-        if (sc.hur)                                                                                              \
-            k_slow_edge<ME2, true><<<nb, TPB, 0, s>>>(m, h, st.q, st.K, st.F, u, out, sc.rho0, sc.cd, sc.cw, e0, e1);  \
-        else                                                                                                     \
-            k_slow_edge<ME2, false><<<nb, TPB, 0, s>>>(m, h, st.q, st.K, st.F, u, out, sc.rho0, sc.cd, sc.cw, e0, e1); \
+        if (sc.pve) {                                                                                            \
+            if (sc.hur) FBLTS_SLOW_EDGE3(ME2, true, true);                                                       \
+            else FBLTS_SLOW_EDGE3(ME2, false, true);                                                             \
+        } else {                                                                                                 \
+            if (sc.hur) FBLTS_SLOW_EDGE3(ME2, true, false);                                                      \
+            else FBLTS_SLOW_EDGE3(ME2, false, false);                                                            \
+        }                                                                                                        \
     } while (0)
     if (m.maxE2 <= 10)
         FBLTS_SLOW_EDGE(10);
@@ -1413,6 +1448,7 @@ void launch_slow_edge_range(const DevMesh &m, const DevState &st, const double *
     else
         FBLTS_SLOW_EDGE(30);
 #undef FBLTS_SLOW_EDGE
+#undef FBLTS_SLOW_EDGE3
 }
 void launch_slow_edge(const DevMesh &m, const DevState &st, const double *h, const double *u, const StepConst &sc,
                       cudaStream_t s) {
@@ -1517,6 +1553,9 @@ void launch_correct(const DevMesh &m, const DevState &st, const double *hN, cons
 }
 void launch_permute_in(const int32_t *old, const double *src, double *dst, int n, cudaStream_t s) {
     if (n > 0) k_permute_in<<<nblocks(n), TPB, 0, s>>>(old, src, dst, n);
+}
+void launch_validate(const double *v, int n, int positive, int *bad, cudaStream_t s) {
+    if (n > 0) k_validate<<<nblocks(n), TPB, 0, s>>>(v, n, positive, bad);
 }
 void launch_permute_out(const int32_t *old, const double *src, double *dst, int n, cudaStream_t s) {
     if (n > 0) k_permute_out<<<nblocks(n), TPB, 0, s>>>(old, src, dst, n);

@@ -21,7 +21,7 @@ from . import _abi as abi
 class Solver:
     def __init__(self, mesh, fine_mask, dt, M, *, g=9.81, beta=(0.531, 0.531, 0.313), rho0=1000.0, r=2,
                  slow=True, tau_n=None, device=None, stream=None, rank=0, nranks=1, nccl_id=None, scheme="fblts",
-                 slow_refresh=False, hurricane=None, unsplit=False):
+                 slow_refresh=False, hurricane=None, unsplit=False, pv="centered"):
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2405_10505_b200.Solver needs a CUDA device (no CPU fallback)")
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
@@ -30,7 +30,7 @@ class Solver:
         self.ctx = abi.fblts_create(dt, M, g=g, beta=beta, rho0=rho0, r=r, slow=slow, device=self.device.index,
                                     stream=self.stream.cuda_stream, rank=rank, nranks=nranks, nccl_id=nccl_id,
                                     scheme=scheme, slow_refresh=slow_refresh,
-                                    sal=(hurricane or {}).get("sal", 0.0), unsplit=unsplit)
+                                    sal=(hurricane or {}).get("sal", 0.0), unsplit=unsplit, pv=pv)
         self.rank, self.nranks = rank, nranks
         try:
             abi.fblts_upload_mesh(self.ctx, mesh)

@@ -205,9 +205,20 @@ def test_set_state_rejects_bad_h(Solver):
     s = Solver(c.mesh, c.fine_mask, c.dt, c.M)
     h = c.h0.copy()
     h[5] = -1.0
+    h[9] = np.nan
     with pytest.raises(abi.FbltsError) as ei:
         s.set_state(h, c.u0)
-    assert ei.value.code == -4 and "h[5]" in str(ei.value)
+    assert ei.value.code == -4 and "h[5]" in str(ei.value)         # the first offending index
+    with pytest.raises(abi.FbltsError) as ei:                      # no valid state after a rejected one
+        s.step(1)
+    u = c.u0.copy()
+    u[7] = np.inf
+    with pytest.raises(abi.FbltsError) as ei:
+        s.set_state(c.h0, u)
+    assert ei.value.code == -4 and "u[7]" in str(ei.value)
+    s.set_state(c.h0, c.u0)                                        # a good state is accepted again
+    s.step(1)
+    assert np.all(np.isfinite(s.state()[0]))
 
 
 def test_profile_counts_launches(Solver):
@@ -467,3 +478,35 @@ def test_fused_subcycle_matches_oracle(Solver, monkeypatch, M):
     for hg, ug in res:
         assert_parity(hg, ug, ho, uo)
         assert np.array_equal(hg, ho) and np.array_equal(ug, uo)
+
+
+@pytest.mark.parametrize("case", ["config1", "shelf_ragged", "rk4", "unsplit"])
+def test_energy_pv_matches_oracle(Solver, case):
+    """Energy-conserving PV flux (oracle trisk.pv_flux_energy): FB-LTS, classical RK4
+    and unsplit FB-LTS with the variant, element by element against the oracle (expected bitwise)."""
+    import dataclasses
+    c = configs.config1() if case == "config1" else configs.small_shelf(nx=70, ny=38, seed=11, dt=25.0)
+    M = 3 if case == "shelf_ragged" else c.M
+    phys = dataclasses.replace(phys_of(c), pv="energy")
+    lab = lts.label_regions(c.mesh, c.fine_mask)
+    n = 30
+    if case == "rk4":
+        dt = 5.0
+        ho, uo = c.h0.copy(), c.u0.copy()
+        for _ in range(n):
+            ho, uo = fbrk32.rk4_step(c.mesh, ho, uo, dt, phys)
+        s = Solver(c.mesh, c.fine_mask, dt, 1, g=c.g, beta=c.beta, rho0=c.rho0, tau_n=c.tau_n, scheme="rk4",
+                   pv="energy")
+    else:
+        unsplit = case == "unsplit"
+        ho, uo = lts.run(c.mesh, lab, c.h0, c.u0, c.dt, M, phys, n, split=not unsplit)
+        s = Solver(c.mesh, c.fine_mask, c.dt, M, g=c.g, beta=c.beta, rho0=c.rho0, tau_n=c.tau_n,
+                   unsplit=unsplit, pv="energy")
+    s.set_state(c.h0, c.u0)
+    s.step(n)
+    hg, ug, _ = s.state()
+    assert_parity(hg, ug, ho, uo)
+    assert np.array_equal(hg, ho) and np.array_equal(ug, uo)
+    hc, uc, _ = run_oracle(c, n, M=M) if case != "rk4" else (None, None, None)
+    if uc is not None:
+        assert not np.array_equal(uc, ug)              # the variant is active
