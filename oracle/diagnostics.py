@@ -23,6 +23,18 @@ def total_abs_vorticity(mesh, u):
     return math.fsum(vertex_abs_vorticity_integrals(mesh, u).tolist())
 
 
+def total_pv_volume(mesh, h, u):
+    """Volume integral of PV, sum_v A_v h_v q_v (Remark rmk:volume_conservation_pv, eq.
+    vol_integral_pv): h_v the kite-weighted dual-cell thickness, q_v = eta_v / h_v.
+    Equal to Gamma = sum_v A_v eta_v up to rounding (the identity the remark uses), so FB-LTS
+    conserves it wherever Theorem 2 holds.  Raises if some h_v <= 0 (q undefined)."""
+    hv = trisk.vertex_thickness(mesh, h)
+    if np.any(~(hv > 0.0)):
+        raise ValueError("total_pv_volume: dual-cell thickness h_v <= 0")
+    q = trisk.potential_vorticity(mesh, u, h)
+    return math.fsum((mesh.areaTriangle * hv * q).tolist())
+
+
 def courant_numbers(mesh, lab, h, u, dt, M, g):
     """nu_e = (|u_e| + sqrt(g h_e)) dt_e / d_e with dt_e = dt/M on F_E, else dt  (eq. cfl)."""
     c0, c1 = mesh.cellsOnEdge[:, 0], mesh.cellsOnEdge[:, 1]

@@ -127,6 +127,11 @@ struct DevMesh {
     SubTileMesh st;                    // subcycle tiles of F\F^2 (one rank; fused fine subcycle)
 };
 
+// blocks of the diagnostics reduction (fixed: the partial sums are merged in block order, so the
+// result is a deterministic function of the state)
+constexpr int DIAG_RB = 592;                  // blocks per role (cells, vertices, edges)
+constexpr int DIAG_BLOCKS = 3 * DIAG_RB;
+
 // Device error record (positivity / NaN), first failure wins.
 struct DevError {
     int32_t flag;    // 0 = ok, 1 = positivity

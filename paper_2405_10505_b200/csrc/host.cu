@@ -1142,7 +1142,7 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
     put(s.stage, std::max(m.nC, m.nE));
     put(s.cellOld, L.nC);
     put(s.edgeOld, L.nE);
-    put(s.diag, 296 * 6 + 8 + 6 * 64);
+    put(s.diag, DIAG_BLOCKS * 6 + 8 + 6 * 64);
     put(s.err, 1);
     put(s.vbad, 2);
     put(s.sendbuf, c->xmax);
@@ -1195,7 +1195,7 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
         d.nB = L.nB, d.cb = L.cb, d.cbI = L.cbI, d.eb = L.eb, d.cbh = L.cbh;
         c->hbuf[0] = hA, c->hbuf[1] = hB, c->ubuf[0] = uA, c->ubuf[1] = uB;
         s.hN = hA, s.hNew = hB, s.uN = uA, s.uNew = uB;
-        c->diag_out = s.diag + 296 * 6;
+        c->diag_out = s.diag + DIAG_BLOCKS * 6;
     }
     return p.total;
 }

@@ -942,37 +942,51 @@ __device__ __forceinline__ DD dd_merge(DD a, DD b) {
     return r;
 }
 
-constexpr int DIAG_BLOCKS = 296;
 
+// Diagnostics, pass 1: three roles by block range -- blocks [0, DIAG_RB) sum A_i h_i and min h over
+// the owned cells, [DIAG_RB, 2 DIAG_RB) the absolute circulation of the owned vertices, the rest the
+// Courant maximum over the owned edges; each block writes its 6 partials (identities for the
+// quantities it does not touch).  Pass 2 merges them in a fixed order, so the result is a
+// deterministic function of the state.
 __global__ void __launch_bounds__(TPB) k_diag_partial(DevMesh m, const double *__restrict__ h,
                                                       const double *__restrict__ u, StepConst sc,
                                                       double *__restrict__ part) {
-    const int tid = blockIdx.x * TPB + threadIdx.x;
-    const int T = gridDim.x * TPB;
+    const int role = blockIdx.x / DIAG_RB;
+    const int tid = (blockIdx.x - role * DIAG_RB) * TPB + threadIdx.x;
+    const int T = DIAG_RB * TPB;
     DD mass{0.0, 0.0}, gam{0.0, 0.0};
     double hmin = (double)INFINITY, numax = 0.0;
-    for (int i = tid; i < m.nOwnC; i += T) {
-        dd_add(mass, m.areaCell[i] * h[i]);
-        hmin = fmin(hmin, h[i]);
-    }
-    for (int v = tid; v < m.nV; v += T) {
-        if (!m.vOwn[v]) continue;
-        double circ = 0.0;
-        for (int k = 0; k < 3; ++k) {
-            bool pos;
-            const int e = decode(m.eov[k * m.strideV + v], pos);
-            const double t = m.dc[e] * u[e];
-            circ = circ + (pos ? t : -t);
+    if (role == 0) {
+#pragma unroll 4
+        for (int i = tid; i < m.nOwnC; i += T) {
+            const double hi = h[i];
+            dd_add(mass, m.areaCell[i] * hi);
+            hmin = fmin(hmin, hi);
         }
-        dd_add(gam, circ + m.areaTri[v] * m.fV[v]);
-    }
-    for (int e = tid; e < m.eb.end; e += T) {
-        if (!m.eOwn[e]) continue;
-        const int2 c = m.coe[e];
-        const double he = 0.5 * (h[c.x] + h[c.y]);
-        const double dte = e >= m.eb.f ? sc.c3f : sc.c3;
-        const double nu = (fabs(u[e]) + sqrt(sc.g * he)) * dte / m.dc[e];
-        numax = fmax(numax, nu);
+    } else if (role == 1) {
+#pragma unroll 2
+        for (int v = tid; v < m.nV; v += T) {
+            if (!m.vOwn[v]) continue;
+            double circ = 0.0;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                bool pos;
+                const int e = decode(m.eov[k * m.strideV + v], pos);
+                const double t = m.dc[e] * u[e];
+                circ = circ + (pos ? t : -t);
+            }
+            dd_add(gam, circ + m.areaTri[v] * m.fV[v]);
+        }
+    } else {
+#pragma unroll 4
+        for (int e = tid; e < m.eb.end; e += T) {
+            if (!m.eOwn[e]) continue;
+            const int2 c = m.coe[e];
+            const double he = 0.5 * (h[c.x] + h[c.y]);
+            const double dte = e >= m.eb.f ? sc.c3f : sc.c3;
+            const double nu = (fabs(u[e]) + sqrt(sc.g * he)) * dte / m.dc[e];
+            numax = fmax(numax, nu);
+        }
     }
     __shared__ double sh[6][TPB];
     sh[0][threadIdx.x] = mass.hi;
@@ -1001,22 +1015,41 @@ __global__ void __launch_bounds__(TPB) k_diag_partial(DevMesh m, const double *_
     if (threadIdx.x < 6) part[blockIdx.x * 6 + threadIdx.x] = sh[threadIdx.x][0];
 }
 
-__global__ void k_diag_final(const double *__restrict__ part, int nb, double *__restrict__ out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// Pass 2 (one block): thread t merges the partials of blocks t, t + TPB, ... in order, then a fixed
+// tree over the threads.
+__global__ void __launch_bounds__(TPB) k_diag_final(const double *__restrict__ part, int nb, double *__restrict__ out) {
     DD mass{0.0, 0.0}, gam{0.0, 0.0};
     double hmin = (double)INFINITY, numax = 0.0;
-    for (int b = 0; b < nb; ++b) {
+    for (int b = threadIdx.x; b < nb; b += TPB) {
         mass = dd_merge(mass, DD{part[b * 6 + 0], part[b * 6 + 1]});
         gam = dd_merge(gam, DD{part[b * 6 + 2], part[b * 6 + 3]});
         hmin = fmin(hmin, part[b * 6 + 4]);
         numax = fmax(numax, part[b * 6 + 5]);
     }
-    out[0] = mass.hi;          // raw double-double parts: ranks are combined on the host in rank order
-    out[1] = mass.lo;
-    out[2] = gam.hi;
-    out[3] = gam.lo;
-    out[4] = hmin;
-    out[5] = numax;
+    __shared__ double sh[6][TPB];
+    sh[0][threadIdx.x] = mass.hi;
+    sh[1][threadIdx.x] = mass.lo;
+    sh[2][threadIdx.x] = gam.hi;
+    sh[3][threadIdx.x] = gam.lo;
+    sh[4][threadIdx.x] = hmin;
+    sh[5][threadIdx.x] = numax;
+    __syncthreads();
+    for (int w = TPB / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            const int o = threadIdx.x + w;
+            DD r = dd_merge(DD{sh[0][threadIdx.x], sh[1][threadIdx.x]}, DD{sh[0][o], sh[1][o]});
+            sh[0][threadIdx.x] = r.hi;
+            sh[1][threadIdx.x] = r.lo;
+            DD r2 = dd_merge(DD{sh[2][threadIdx.x], sh[3][threadIdx.x]}, DD{sh[2][o], sh[3][o]});
+            sh[2][threadIdx.x] = r2.hi;
+            sh[3][threadIdx.x] = r2.lo;
+            sh[4][threadIdx.x] = fmin(sh[4][threadIdx.x], sh[4][o]);
+            sh[5][threadIdx.x] = fmax(sh[5][threadIdx.x], sh[5][o]);
+        }
+        __syncthreads();
+    }
+    // raw double-double parts: ranks are combined on the host in rank order
+    if (threadIdx.x < 6) out[threadIdx.x] = sh[threadIdx.x][0];
 }
 
 // ---------------------------------------------------------------- launchers
@@ -1569,7 +1602,7 @@ void launch_unpack(const int32_t *idx, const double *buf, double *a, int n, cuda
 void launch_diagnostics(const DevMesh &m, const DevState &st, const double *h, const double *u, const StepConst &sc,
                         double *out_dev, cudaStream_t s) {
     k_diag_partial<<<DIAG_BLOCKS, TPB, 0, s>>>(m, h, u, sc, st.diag);
-    k_diag_final<<<1, 32, 0, s>>>(st.diag, DIAG_BLOCKS, out_dev);
+    k_diag_final<<<1, TPB, 0, s>>>(st.diag, DIAG_BLOCKS, out_dev);
 }
 
 void launch_rk4_stage(const DevMesh &m, const DevState &st, int stage, const double *hN, const double *uN,

@@ -6,6 +6,7 @@ do no work: sum_e l_e d_e F_e PV_e = 0 for ANY state -- the TRiSK energy-conserv
 identity tells the two apart; uniform PV makes them agree; conservation (Theorems 1-2) and the
 M = 1 reduction hold for the variant as for the default."""
 import dataclasses
+import math
 
 import numpy as np
 import pytest
@@ -105,3 +106,27 @@ def test_conservation_and_M1_with_energy_pv(M):
         for _ in range(10):
             hh, uu = fbrk32.fbrk32_step(c.mesh, hh, uu, c.dt, phys)
         assert np.array_equal(hh, h) and np.array_equal(uu, u)
+
+
+def test_pv_volume_integral():
+    """Remark rmk:volume_conservation_pv: sum_v A_v h_v q_v = sum_v A_v eta_v = Gamma
+    (to rounding) for any state; with uniform q = 1 (eta_v = h_v) it is sum_v A_v h_v; and it is
+    conserved by FB-LTS steps as Gamma is (Theorem 2)."""
+    c = configs.small_shelf(nx=32, ny=28, dt=20.0)
+    rng = np.random.default_rng(5)
+    h = c.h0 * (1.0 + 0.1 * rng.random(c.mesh.nCells))
+    u = rng.standard_normal(c.mesh.nEdges)
+    pv, gam = dg.total_pv_volume(c.mesh, h, u), dg.total_abs_vorticity(c.mesh, u)
+    scale = math.fsum(np.abs(dg.vertex_abs_vorticity_integrals(c.mesh, u)).tolist())
+    assert abs(pv - gam) <= 1e-14 * scale
+    m = build_periodic_hex_mesh(8, 6, 2000.0)          # uniform q = 1: f_v = h_v, u = 0
+    hh = 50.0 + 10.0 * rng.random(m.nCells)
+    m.fVertex = trisk.vertex_thickness(m, hh)
+    want = math.fsum((m.areaTriangle * trisk.vertex_thickness(m, hh)).tolist())
+    assert abs(dg.total_pv_volume(m, hh, np.zeros(m.nEdges)) - want) <= 1e-14 * want
+    lab = lts.label_regions(c.mesh, c.fine_mask)
+    h1, u1 = lts.run(c.mesh, lab, c.h0, c.u0, c.dt, c.M, fbrk32.Phys(tau_n=c.tau_n), 10)
+    p0, p1 = dg.total_pv_volume(c.mesh, c.h0, c.u0), dg.total_pv_volume(c.mesh, h1, u1)
+    assert abs(p1 - p0) <= 1e-13 * max(abs(p0), scale * 1e-3)
+    with pytest.raises(ValueError):
+        dg.total_pv_volume(m, -hh, np.zeros(m.nEdges))
