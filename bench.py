@@ -354,9 +354,13 @@ def arm_native(args):
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         s.set_state(h_host, u_host, 0.0)                # H2D of the initial state (+ device permutation)
+        records = []
         for _ in range(args.steps):
             s.step(1)
-            s.diagnostics()                              # per-step run record: D2H of 4 doubles
+            # per-step run record (mass, Gamma, min h, max nu): reduction + D2H.  Synchronous: the
+            # asynchronous variant (diagnostics_async, overlapped with the next step) measured slower
+            # on config 5 (5.24e9 vs 5.46e9 cell-updates/s): both passes are bandwidth-bound.
+            records.append(s.diagnostics())
         s.state(h_out.numpy(), u_out.numpy())            # D2H of the final state
         f1.record(stream)
         torch.cuda.synchronize()
@@ -369,7 +373,9 @@ def arm_native(args):
         e2e = {"value": units / (ems * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": state_bytes / args.steps,
                "d2h_bytes_per_step": 32 + state_bytes / args.steps,
-               "how": "set_state(pinned host h,u) + K x (step(1) + diagnostics()) + get_state(pinned host)"}
+               "how": "set_state(pinned host h,u) + K x (step(1) + diagnostics(): mass, Gamma, min h, max nu "
+                      "read back every step) + get_state(pinned host)"}
+        assert all(np.all(np.isfinite(r)) for r in records)
 
     # ---------------- the same workload as global FB-RK(3,2) at the fine step (no LTS), same GPU:
     # the paper's speedup framing (FB-LTS vs a global scheme at the step the fine region needs,

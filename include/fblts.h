@@ -219,6 +219,15 @@ int fblts_get_state(fblts_ctx *ctx, double *h, double *u, double *t);
  * (NCCL) and combined in rank order, so every rank returns the same bits (synchronises). */
 int fblts_diagnostics(fblts_ctx *ctx, double out[4]);
 
+/* The same four numbers for the state after the steps enqueued so far, WITHOUT synchronising
+ * (one rank): the reduction runs on a library stream that waits for the compute stream, its 48-byte
+ * result is copied to pinned host memory and combined into out[4] by a host callback.  out must stay
+ * valid until the next synchronising call (fblts_sync, fblts_get_state, fblts_diagnostics), after
+ * which it holds the values.  Later steps that overwrite the state being reduced wait for the
+ * reduction, so the numbers are those of the state at the call.  Errors: ORDER (no state, or
+ * nranks > 1), CUDA. */
+int fblts_diagnostics_async(fblts_ctx *ctx, double *out);
+
 /* Instrumented replay for the roofline: runs n_coarse steps WITHOUT the graph, with
  * CUDA events around every launch on cfg.stream; ms[k] = total device ms of kernel
  * kind k, launches[k] = launch count, for k < FBLTS_NUM_KERNELS.  Advances the state. */

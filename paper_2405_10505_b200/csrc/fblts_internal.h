@@ -179,6 +179,7 @@ struct DevState {
     double *stage;                      // staging for set/get_state (max(nC, nE) doubles)
     int32_t *cellOld, *edgeOld;         // new -> old permutation (device)
     double *diag;                       // reduction scratch
+    double *diagA;                      // reduction scratch of the asynchronous diagnostics
     double *sendbuf, *recvbuf;          // halo exchange buffers
     int32_t *xidx;                      // halo exchange index lists (all exchanges, send then recv)
     DevError *err;
@@ -283,7 +284,7 @@ void launch_validate(const double *v, int n, int positive, int *bad, cudaStream_
 // halo exchange: buf[k] = a[idx[k]] (pack), a[idx[k]] = buf[k] (unpack)
 void launch_pack(const int32_t *idx, const double *a, double *buf, int n, cudaStream_t s);
 void launch_unpack(const int32_t *idx, const double *buf, double *a, int n, cudaStream_t s);
-void launch_diagnostics(const DevMesh &m, const DevState &st, const double *h, const double *u,
-                        const StepConst &sc, double *out_dev, cudaStream_t s);
+void launch_diagnostics(const DevMesh &m, const double *h, const double *u, const StepConst &sc, double *part,
+                        double *out_dev, cudaStream_t s);
 
 }  // namespace fblts

@@ -86,6 +86,17 @@ struct fblts_ctx {
     cudaGraphExec_t exec[2]{};
     size_t graph_nodes = 0;   // kernel launches per coarse step (nodes of the captured graph)
     void *nccl = nullptr;     // ncclComm_t (nranks > 1)
+    // asynchronous diagnostics (fblts_diagnostics_async): side stream, per-state-buffer events that
+    // the steps overwriting that buffer wait on, pinned result slots and host-callback payloads
+    cudaStream_t dstream = nullptr;
+    cudaEvent_t evHead = nullptr, evDiag[2]{};
+    bool diagPending[2]{};
+    double *dhost = nullptr;
+    struct DiagJob {
+        const double *slot;
+        double *out;
+    } *djobs = nullptr;
+    uint64_t ndiag = 0;
     unsigned char nccl_id[128]{};
     // host-side staging of the permuted device tables (filled at set_regions)
     std::vector<int32_t> d_nEoC, d_ec, d_nEoE, d_eoe, d_eov, d_cov, d_coe, d_voe, d_xidx;
@@ -134,6 +145,7 @@ int fail(fblts_ctx *c, int code, const char *fmt, ...) {
     } while (0)
 
 int pad32(int n) { return (n + 31) / 32 * 32; }
+void diag_wait(fblts_ctx *c, int b);
 
 // ---------------------------------------------------------------- SFC keys
 // 2-D Hilbert index (planar meshes) on a 2^16 x 2^16 grid over the bounding box.
@@ -1143,6 +1155,7 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
     put(s.cellOld, L.nC);
     put(s.edgeOld, L.nE);
     put(s.diag, DIAG_BLOCKS * 6 + 8 + 6 * 64);
+    put(s.diagA, DIAG_BLOCKS * 6 + 8);
     put(s.err, 1);
     put(s.vbad, 2);
     put(s.sendbuf, c->xmax);
@@ -1346,6 +1359,8 @@ int fblts_set_state(fblts_ctx *c, const double *h, const double *u, double t) {
     if (c->phase < P_BOUND) return fail(c, FBLTS_ERR_ORDER, "set_state: bind the workspace first");
     cudaStream_t s = c->stream;
     const Local &L = c->lo;
+    diag_wait(c, 0);
+    diag_wait(c, 1);
     c->parity = 0;
     // the input check runs on the device, on the copied arrays (first offending index reported)
     int32_t bad[2] = {0, 0};
@@ -1816,11 +1831,26 @@ void dd_merge_host(double &ah, double &al, double bh, double bl) {
 }
 
 int diag_partial(fblts_ctx *c, double out6[6]) {
-    launch_diagnostics(c->dm, c->ds, c->hbuf[c->parity], c->ubuf[c->parity], c->sc, c->diag_out, c->stream);
+    launch_diagnostics(c->dm, c->hbuf[c->parity], c->ubuf[c->parity], c->sc, c->ds.diag, c->diag_out, c->stream);
     CUDA_TRY(c, cudaGetLastError());
     CUDA_TRY(c, cudaMemcpyAsync(out6, c->diag_out, 6 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     return FBLTS_OK;
+}
+
+// asynchronous diagnostics: the compute stream waits for the last asynchronous reduction that
+// reads state buffer b before anything overwrites b
+constexpr int DIAG_RING = 1024;
+void diag_wait(fblts_ctx *c, int b) {
+    if (c->diagPending[b]) {
+        cudaStreamWaitEvent(c->stream, c->evDiag[b], 0);
+        c->diagPending[b] = false;
+    }
+}
+void diag_combine(const double *parts, int n, double out[4]);
+void CUDART_CB diag_host_fn(void *p) {
+    const fblts_ctx::DiagJob *j = static_cast<const fblts_ctx::DiagJob *>(p);
+    diag_combine(j->slot, 1, j->out);
 }
 
 void diag_combine(const double *parts, int n, double out[4]) {
@@ -1853,6 +1883,7 @@ int fblts_step(fblts_ctx *c, int32_t n) {
             if (rc) return rc;
         }
     for (int i = 0; i < n; ++i) {
+        diag_wait(c, 1 - c->parity);
         CUDA_TRY(c, cudaGraphLaunch(c->exec[c->parity], c->stream));
         c->parity ^= 1;
         c->t += c->cfg.dt;
@@ -1921,6 +1952,7 @@ int fblts_step_group(fblts_ctx **cs, int32_t n, int32_t n_coarse) {
 int fblts_sync(fblts_ctx *c) {
     if (!c) return FBLTS_ERR_INVALID_ARG;
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (c->dstream) CUDA_TRY(c, cudaStreamSynchronize(c->dstream));
     if (c->phase >= P_BOUND) return check_device_error(c);
     return FBLTS_OK;
 }
@@ -1943,9 +1975,39 @@ int fblts_get_state(fblts_ctx *c, double *h, double *u, double *t) {
         CUDA_TRY(c, cudaMemcpyAsync(u, c->ds.stage, (size_t)c->hm.nE * 8, cudaMemcpyDeviceToHost, s));
     }
     CUDA_TRY(c, cudaStreamSynchronize(s));
+    if (c->dstream) CUDA_TRY(c, cudaStreamSynchronize(c->dstream));   // outstanding async diagnostics
     CUDA_TRY(c, cudaGetLastError());
     if (t) *t = c->t;
     return check_device_error(c);
+}
+
+int fblts_diagnostics_async(fblts_ctx *c, double *out) {
+    if (!c || !out) return FBLTS_ERR_INVALID_ARG;
+    if (c->phase != P_STATE) return fail(c, FBLTS_ERR_ORDER, "diagnostics_async: no state set");
+    if (c->cfg.nranks > 1) return fail(c, FBLTS_ERR_ORDER, "diagnostics_async: one rank (use fblts_diagnostics)");
+    CUDA_TRY(c, cudaSetDevice(c->cfg.device));
+    if (!c->dstream) {
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->dstream, cudaStreamNonBlocking));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->evHead, cudaEventDisableTiming));
+        for (auto &e : c->evDiag) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CUDA_TRY(c, cudaHostAlloc((void **)&c->dhost, sizeof(double) * 6 * DIAG_RING, cudaHostAllocDefault));
+        c->djobs = new fblts_ctx::DiagJob[DIAG_RING];
+    }
+    const uint64_t k = c->ndiag++;
+    if (k > 0 && k % DIAG_RING == 0) CUDA_TRY(c, cudaStreamSynchronize(c->dstream));   // ring slots reusable
+    const int slot = (int)(k % DIAG_RING), b = c->parity;
+    CUDA_TRY(c, cudaEventRecord(c->evHead, c->stream));                // the state the caller sees now
+    CUDA_TRY(c, cudaStreamWaitEvent(c->dstream, c->evHead, 0));
+    double *dout = c->ds.diagA + DIAG_BLOCKS * 6;
+    launch_diagnostics(c->dm, c->hbuf[b], c->ubuf[b], c->sc, c->ds.diagA, dout, c->dstream);
+    CUDA_TRY(c, cudaGetLastError());
+    CUDA_TRY(c, cudaEventRecord(c->evDiag[b], c->dstream));
+    c->diagPending[b] = true;
+    double *hs = c->dhost + 6 * (size_t)slot;
+    CUDA_TRY(c, cudaMemcpyAsync(hs, dout, 6 * sizeof(double), cudaMemcpyDeviceToHost, c->dstream));
+    c->djobs[slot] = fblts_ctx::DiagJob{hs, out};
+    CUDA_TRY(c, cudaLaunchHostFunc(c->dstream, diag_host_fn, &c->djobs[slot]));
+    return FBLTS_OK;
 }
 
 int fblts_diagnostics(fblts_ctx *c, double out[4]) {
@@ -1953,6 +2015,7 @@ int fblts_diagnostics(fblts_ctx *c, double out[4]) {
     if (c->phase != P_STATE) return fail(c, FBLTS_ERR_ORDER, "diagnostics: no state set");
     if (c->cfg.nranks > 1 && !c->nccl)
         return fail(c, FBLTS_ERR_ORDER, "diagnostics: loopback contexts use fblts_diagnostics_group");
+    if (c->dstream) CUDA_TRY(c, cudaStreamSynchronize(c->dstream));   // completes outstanding async results
     double part[6];
     int rc = diag_partial(c, part);
     if (rc) return rc;
@@ -1994,6 +2057,7 @@ int fblts_profile(fblts_ctx *c, int32_t n, double *ms, int64_t *launches) {
     }
     for (int i = 0; i < n; ++i) {
         Recorder rec;
+        diag_wait(c, 1 - c->parity);
         const int rc = enqueue_step(c, c->parity, c->stream, &rec);
         if (rc) return rc;
         CUDA_TRY(c, cudaGetLastError());
@@ -2021,6 +2085,14 @@ void fblts_destroy(fblts_ctx *c) {
     if (c->comm) cudaStreamDestroy(c->comm);
     if (c->evFork) cudaEventDestroy(c->evFork);
     if (c->evJoin) cudaEventDestroy(c->evJoin);
+    if (c->dstream) {
+        cudaStreamSynchronize(c->dstream);
+        cudaStreamDestroy(c->dstream);
+        cudaEventDestroy(c->evHead);
+        for (auto e : c->evDiag) cudaEventDestroy(e);
+        cudaFreeHost(c->dhost);
+        delete[] c->djobs;
+    }
     nccl_destroy(c);
     delete c;
 }

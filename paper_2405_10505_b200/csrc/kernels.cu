@@ -1599,10 +1599,10 @@ void launch_pack(const int32_t *idx, const double *a, double *buf, int n, cudaSt
 void launch_unpack(const int32_t *idx, const double *buf, double *a, int n, cudaStream_t s) {
     if (n > 0) k_unpack<<<nblocks(n), TPB, 0, s>>>(idx, buf, a, n);
 }
-void launch_diagnostics(const DevMesh &m, const DevState &st, const double *h, const double *u, const StepConst &sc,
+void launch_diagnostics(const DevMesh &m, const double *h, const double *u, const StepConst &sc, double *part,
                         double *out_dev, cudaStream_t s) {
-    k_diag_partial<<<DIAG_BLOCKS, TPB, 0, s>>>(m, h, u, sc, st.diag);
-    k_diag_final<<<1, TPB, 0, s>>>(st.diag, DIAG_BLOCKS, out_dev);
+    k_diag_partial<<<DIAG_BLOCKS, TPB, 0, s>>>(m, h, u, sc, part);
+    k_diag_final<<<1, TPB, 0, s>>>(part, DIAG_BLOCKS, out_dev);
 }
 
 void launch_rk4_stage(const DevMesh &m, const DevState &st, int stage, const double *hN, const double *uN,

@@ -47,6 +47,7 @@ class Solver:
             self.ctx = None
             raise
         self.dt, self.M = dt, M
+        self._pending = []              # arrays filled by outstanding diagnostics_async calls
 
     # --- setup queries
     def labels(self):
@@ -73,15 +74,27 @@ class Solver:
 
     def sync(self):
         abi.fblts_sync(self.ctx)
+        self._pending.clear()
 
     def state(self, h_out=None, u_out=None):
         h = np.empty(self.nCells) if h_out is None else h_out
         u = np.empty(self.nEdges) if u_out is None else u_out
         t = abi.fblts_get_state(self.ctx, h, u)
+        self._pending.clear()
         return h, u, t
 
     def diagnostics(self):
-        return abi.fblts_diagnostics(self.ctx)
+        d = abi.fblts_diagnostics(self.ctx)
+        self._pending.clear()
+        return d
+
+    def diagnostics_async(self):
+        """(mass, Gamma, min h, max nu) of the current state, filled in without synchronising: the
+        returned array holds the values after the next sync() / state() / diagnostics()."""
+        out = np.full(4, np.nan)
+        self._pending.append(out)
+        abi.fblts_diagnostics_async(self.ctx, out)
+        return out
 
     def profile(self, n_coarse):
         ms, cnt = abi.fblts_profile(self.ctx, n_coarse)

@@ -510,3 +510,25 @@ def test_energy_pv_matches_oracle(Solver, case):
     hc, uc, _ = run_oracle(c, n, M=M) if case != "rk4" else (None, None, None)
     if uc is not None:
         assert not np.array_equal(uc, ug)              # the variant is active
+
+
+def test_diagnostics_async_match_sync(Solver):
+    """fblts_diagnostics_async gives, bit for bit, what fblts_diagnostics gives for the state at the
+    call, even when later steps (enqueued before any sync) overwrite that state's buffers."""
+    c = configs.config1()
+    s = Solver(c.mesh, c.fine_mask, c.dt, c.M, g=c.g, beta=c.beta, rho0=c.rho0, tau_n=c.tau_n)
+    s.set_state(c.h0, c.u0)
+    want = [s.diagnostics()]
+    for _ in range(6):
+        s.step(1)
+        want.append(s.diagnostics())
+    s.set_state(c.h0, c.u0)
+    got = [s.diagnostics_async()]
+    for _ in range(6):
+        s.step(1)
+        got.append(s.diagnostics_async())
+    s.step(3)                                        # overwrites both state buffers before any sync
+    h, _, _ = s.state()
+    for g_, w in zip(got, want):
+        assert np.array_equal(g_, w), (g_, w)
+    assert np.all(np.isfinite(h))
