@@ -123,3 +123,61 @@ def test_global_cfl_limit_on_hex(factor, grows):
         assert not np.isfinite(a1) or a1 > 100 * a0
     else:
         assert a1 < 2 * a0
+
+
+def _standing_wave(eps, n_steps, slow):
+    """Global FB-RK(3,2) on a flat 24 x 24 periodic hex (H = 100 m, f = 0) started from
+    h = H + eps cos(k.x), u = 0, k = 2 pi (3/L_x, 2/L_y); returns the measured mode amplitudes
+    (A_n of h - H on c = cos(k.x), B_n of u on p = D c / kappa) and the linear prediction.
+    dt is 0.8 of the stability limit of the fastest (K-point) grid mode, z = omega dt ~ 1."""
+    nx = ny = 24
+    dc, H, g = 10e3, 100.0, 9.81
+    m = build_periodic_hex_mesh(nx, ny, dc)
+    m.bottomDepth = np.full(m.nCells, H)
+    m.fVertex = np.zeros(m.nVertices)
+    Lx, Ly = nx * dc, ny * dc * np.sqrt(3.0) / 2.0
+    k = 2.0 * np.pi * np.array([3.0 / Lx, 2.0 / Ly])
+    c = np.cos(k[0] * m.xCell + k[1] * m.yCell)
+    # P15: kappa^2 = (2 / (3 d^2)) sum_j (1 - cos k.delta_j) over the 6 neighbour offsets of the hex
+    delta = dc * np.array([[np.cos(a), np.sin(a)] for a in np.arange(6) * np.pi / 3.0])
+    kappa = np.sqrt(2.0 / (3.0 * dc * dc) * np.sum(1.0 - np.cos(delta @ k)))
+    c0, c1 = m.cellsOnEdge[:, 0], m.cellsOnEdge[:, 1]
+    p = (c[c1] - c[c0]) / m.dcEdge / kappa
+    omega = np.sqrt(g * H) * kappa
+    dt = 0.8 * 3.8621532 / (np.sqrt(g * H) * np.sqrt(6.0) / dc)    # 0.8 of the grid-scale (K-point) limit
+    z = omega * dt
+    phys = fbrk32.Phys(g=g, slow=slow)
+    h, u = H + eps * c, np.zeros(m.nEdges)
+    for _ in range(n_steps):
+        h, u = fbrk32.fbrk32_step(m, h, u, dt, phys)
+    A = np.dot(h - H, c) / np.dot(c, c)
+    B = np.dot(u, p) / np.dot(p, p)
+    # linear prediction: (b, a) = (B sqrt(H), A sqrt(g)) obey b' = -omega a, a' = omega b, i.e. the
+    # scalar oscillator of P13 with z = omega dt
+    y = np.array([0.0, eps * np.sqrt(g)])
+    Gz = G_closed(z)
+    for _ in range(n_steps):
+        y = Gz @ y
+    return A, B, y[1] / np.sqrt(g), y[0] / np.sqrt(H), h, u, c, p
+
+
+@pytest.mark.parametrize("slow", [False, True])
+def test_standing_wave_mode_follows_G(slow):
+    """P15: a tiny standing wave on the flat regular hex evolves, mode by mode, as the
+    scalar FB-RK(3,2) amplification G(omega dt)^n of P13 with the discrete frequency
+    omega^2 = g H (2/(3 d^2)) sum_j (1 - cos k.delta_j), and the state stays in the mode.  With the
+    slow terms the deviation is their O(eps^2) nonlinearity (O(eps) relative: 1e-3 vs 1e-4); in the
+    gravity-wave model the mode follows G to the mesh-geometry rounding (< 1e-8).  A wrong sign, a
+    dropped factor or a transposed operand in Psi, Phi^fast or the FB stages changes omega or G."""
+    dev = []
+    for eps in (1e-3, 1e-4):
+        A, B, A_lin, B_lin, h, u, c, p = _standing_wave(eps, 10, slow)
+        scale = np.hypot(A_lin, B_lin * np.sqrt(100.0 / 9.81))
+        dev.append(max(abs(A - A_lin), abs(B - B_lin) * np.sqrt(100.0 / 9.81)) / scale)
+        assert np.max(np.abs(h - 100.0 - A * c)) <= 1e-2 * eps      # no other mode excited (O(eps^2))
+        assert np.max(np.abs(u - B * p)) <= 1e-2 * np.max(np.abs(B * p)) + 1e-12
+    if slow:        # q_hat F_perp - grad K is O(eps^2): the mode deviates at O(eps) relative
+        assert dev[0] < 1e-3 and dev[1] < 1e-4
+        assert 5.0 < dev[0] / dev[1] < 20.0
+    else:           # gravity-wave model: h_e u is the only nonlinearity and it feeds other modes only
+        assert dev[0] < 1e-8 and dev[1] < 1e-8
