@@ -1,5 +1,7 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || exit 1
-timeout 600 python -m pytest tests -m gpu -q -x -k "diagnostics or conservation or set_state or dist" > gpurun_out/t6.log 2>&1; tail -2 gpurun_out/t6.log
-timeout 300 python scripts/e2e_parts.py 4096
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_stage_tiled -s 6 -c 1 -o gpurun_out/tiled_s3 -f python scripts/quick_perf.py hex2048 1 > gpurun_out/ncu_tiled.log 2>&1
-tail -2 gpurun_out/ncu_tiled.log
+timeout 900 python -m pytest tests -m gpu -q -x -k "not config5_full" > gpurun_out/t10.log 2>&1; tail -2 gpurun_out/t10.log
+for V in 0 1; do echo "== FBLTS_SLOWPRE_CELL=$V"; FBLTS_SLOWPRE_CELL=$V timeout 300 python scripts/quick_perf.py hex2048 10 2>&1 | grep -E "ms/coarse|slow_pre|slow_edge"; done
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1
+grep '^{' gpurun_out/bench.log | tail -1 | python -c "
+import json,sys
+d=json.loads(sys.stdin.read()); print('ms/step', d['ms_per_step'], 'value', d['value'], 'e2e', d['e2e']['value'], d['roofline']['kernel'], d['roofline']['frac'], d['roofline']['step_frac']); print({k:(round(v['ms_per_step'],3), round(v['GBps'])) for k,v in d['kernels'].items()})"
