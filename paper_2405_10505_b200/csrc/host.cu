@@ -1716,7 +1716,11 @@ int enqueue_unsplit_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
             return;
         }
         mark(K_SLOW_PRE);
-        launch_slow_pre_range(m, st, st.hv, U, 0, 0, 0, s);
+        // S on F_E needs q, K, F only on its stencil (vertices of F_E edges, cells from IF-1, edges
+        // from IF-1_E; the slow-term refresh's range); wider extents and the energy-conserving PV
+        // flux (q_hat on the edges of the cells of F_E edges: one more vertex ring) take the whole mesh
+        if (e0 >= m.eb.f && !sc.pve) launch_slow_pre_range(m, st, st.hv, U, c->vminF, m.cb.if1, m.eb.if1, s);
+        else launch_slow_pre_range(m, st, st.hv, U, 0, 0, 0, s);
         mark(K_SLOW_EDGE);
         launch_slow_edge_range(m, st, st.hv, U, st.Sk, e0, e1, sc, s);
     };
