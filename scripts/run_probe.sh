@@ -1,2 +1,6 @@
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || exit 1
-timeout 900 python -m pytest tests -m gpu -q -x -k "unsplit or energy or refresh" > gpurun_out/t12.log 2>&1; tail -2 gpurun_out/t12.log
+for V in "" "-DFBLTS_PROBE=1" "-DFBLTS_PROBE=2"; do
+  FBLTS_NVCC_EXTRA="$V" python -m paper_2405_10505_b200.build --force > /dev/null 2>&1 || { echo "build failed: $V"; continue; }
+  echo "=== [$V]"
+  timeout 300 python scripts/quick_perf.py hex2048 10 2>&1 | grep -E "ms/coarse|fine_s2|fine_s3|vel_s1|FbltsError"
+done
+python -m paper_2405_10505_b200.build --force > /dev/null 2>&1
