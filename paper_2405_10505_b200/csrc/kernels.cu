@@ -438,7 +438,8 @@ __device__ __forceinline__ void load_indices(const TileMesh &t, const TileRec &r
 }
 
 // development probes (never in the default build): FBLTS_PROBE=1 skips the compute of every tile
-// (copies only), FBLTS_PROBE=2 skips the copies (compute on whatever the buffers hold, no reports)
+// (copies only), 2 skips the copies (compute on whatever the buffers hold, no reports), 3 skips the
+// compute and the gathers (bulk copies only), 4 skips the compute and the bulk copies (gathers only)
 #ifndef FBLTS_PROBE
 #define FBLTS_PROBE 0
 #endif
@@ -469,9 +470,9 @@ __global__ void __launch_bounds__(NTHR, FBLTS_TILE_MINB) k_stage_tiled(DevMesh m
         if (tk < tile1) {
             const TileRec rk = load_rec(t, tk);
             double *Bk = buf0 + k * BUF;
-            if (FBLTS_PROBE != 2 && tid == 0) issue_bulk<STAGE>(m, a, rk, Bk, CS2, ES2, &bar[k]);
+            if (FBLTS_PROBE != 2 && FBLTS_PROBE != 4 && tid == 0) issue_bulk<STAGE>(m, a, rk, Bk, CS2, ES2, &bar[k]);
             load_indices(t, rk, tid, hx, fx);
-            if (FBLTS_PROBE != 2) issue_indexed<STAGE>(m, a, rk, TileBuf<STAGE>(Bk, CS2, ES2, rk), tid, hx, fx);
+            if (FBLTS_PROBE != 2 && FBLTS_PROBE != 3) issue_indexed<STAGE>(m, a, rk, TileBuf<STAGE>(Bk, CS2, ES2, rk), tid, hx, fx);
         }
         cp_async_commit();
     }
@@ -483,18 +484,18 @@ __global__ void __launch_bounds__(NTHR, FBLTS_TILE_MINB) k_stage_tiled(DevMesh m
         const bool more = tn < tile1;
         TileRec nx{};
         if (more) nx = load_rec(t, tn);
-        if (FBLTS_PROBE != 2) mbar_wait(&bar[buf], (phase >> buf) & 1u);
+        if (FBLTS_PROBE != 2 && FBLTS_PROBE != 4) mbar_wait(&bar[buf], (phase >> buf) & 1u);
         phase ^= 1u << buf;
         cp_async_wait_pending<NBUF - 2>();
         __syncthreads();                                   // tile `cur` staged; the previous buffer free
         const int bn = buf == 0 ? NBUF - 1 : buf - 1;
         double *Bn = buf0 + bn * BUF;
         if (more) {
-            if (FBLTS_PROBE != 2 && tid == 0) issue_bulk<STAGE>(m, a, nx, Bn, CS2, ES2, &bar[bn]);
+            if (FBLTS_PROBE != 2 && FBLTS_PROBE != 4 && tid == 0) issue_bulk<STAGE>(m, a, nx, Bn, CS2, ES2, &bar[bn]);
             load_indices(t, nx, tid, hx, fx);              // consumed after this tile's compute
         }
         const TileBuf<STAGE> bc(buf0 + buf * BUF, CS2, ES2, cur);
-#if FBLTS_PROBE != 1
+#if FBLTS_PROBE == 0 || FBLTS_PROBE == 2
         // ---- compute tile `cur`
         const int nOwn = cur.c1 - cur.c0;
         const int i = cur.c0 + tid;
@@ -556,7 +557,7 @@ __global__ void __launch_bounds__(NTHR, FBLTS_TILE_MINB) k_stage_tiled(DevMesh m
             if (FBLTS_PROBE == 0 && !(v > 0.0)) report(err, a.kind, a.k, i, v);
         }
 #endif
-        if (FBLTS_PROBE != 2 && more) issue_indexed<STAGE>(m, a, nx, TileBuf<STAGE>(Bn, CS2, ES2, nx), tid, hx, fx);
+        if (FBLTS_PROBE != 2 && FBLTS_PROBE != 3 && more) issue_indexed<STAGE>(m, a, nx, TileBuf<STAGE>(Bn, CS2, ES2, nx), tid, hx, fx);
         cp_async_commit();
     }
 }
