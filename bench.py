@@ -68,7 +68,7 @@ def byte_model(counts, M, fused, sub=0, maxE=6, maxE2=10):
     `fused`: the deep fine velocity sweep of subcycle k-1 runs inside the deep stage-1 sweep of
     subcycle k (kind fine_vel_s1, k = 1..M-1); fine_s1 then holds the band stage 1 (every k) and the
     deep stage 1 of k = 0, fine_vel the band velocity sweeps and the last full one.
-    `sub` (the fused-subcycle start level, 0 = off): the cells of F\F^sub run whole subcycles in
+    `sub` (the fused-subcycle start level, 0 = off): the cells of F minus F^sub run whole subcycles in
     kind fine_sub (per launch: the subcycle's inputs h^{n,k}, [h^{n,k-1}, h2], z_b, A and the
     connectivity per cell, u, S, l_e, d_e per edge, once; writes h^{n,k+1}, h2 [+ its publishing
     copy] and [u^{n,k}]); the staged deep sweeps then stop at F^sub."""
