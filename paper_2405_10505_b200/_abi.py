@@ -79,6 +79,7 @@ _lib_sync = _sig("fblts_sync", C.c_int, _vp)
 _lib_get_state = _sig("fblts_get_state", C.c_int, _vp, _f64p, _f64p, C.POINTER(C.c_double))
 _lib_diag = _sig("fblts_diagnostics", C.c_int, _vp, _f64p)
 _lib_diag_async = _sig("fblts_diagnostics_async", C.c_int, _vp, _f64p)
+_lib_diag_mass = _sig("fblts_diagnostics_mass", C.c_int, _vp, _f64p)
 _lib_profile = _sig("fblts_profile", C.c_int, _vp, C.c_int32, _f64p, C.POINTER(C.c_int64))
 _lib_kname = _sig("fblts_kernel_name", C.c_char_p, C.c_int32)
 _lib_last_error = _sig("fblts_last_error", C.c_char_p, _vp)
@@ -92,7 +93,8 @@ _lib_diag_group = _sig("fblts_diagnostics_group", C.c_int, C.POINTER(_vp), C.c_i
 EXPORTED = ["fblts_create", "fblts_upload_mesh", "fblts_set_regions", "fblts_get_labels", "fblts_get_counts",
             "fblts_get_halo", "fblts_nccl_unique_id", "fblts_workspace_size", "fblts_bind_workspace",
             "fblts_set_forcing", "fblts_set_hurricane", "fblts_set_state", "fblts_step", "fblts_step_group", "fblts_diagnostics_group",
-            "fblts_sync", "fblts_get_state", "fblts_diagnostics", "fblts_diagnostics_async", "fblts_profile",
+            "fblts_sync", "fblts_get_state", "fblts_diagnostics", "fblts_diagnostics_async", "fblts_diagnostics_mass",
+            "fblts_profile",
             "fblts_kernel_name",
             "fblts_last_error", "fblts_destroy"]
 
@@ -260,6 +262,12 @@ def fblts_get_state(ctx, h_out, u_out):
 def fblts_diagnostics(ctx):
     out = np.zeros(4)
     _check(ctx, _lib_diag(ctx, _ptr(out, C.c_double)))
+    return out
+
+
+def fblts_diagnostics_mass(ctx):
+    out = np.zeros(2)
+    _check(ctx, _lib_diag_mass(ctx, _ptr(out, C.c_double)))
     return out
 
 

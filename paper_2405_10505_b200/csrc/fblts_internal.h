@@ -284,7 +284,8 @@ void launch_validate(const double *v, int n, int positive, int *bad, cudaStream_
 // halo exchange: buf[k] = a[idx[k]] (pack), a[idx[k]] = buf[k] (unpack)
 void launch_pack(const int32_t *idx, const double *a, double *buf, int n, cudaStream_t s);
 void launch_unpack(const int32_t *idx, const double *buf, double *a, int n, cudaStream_t s);
+// cells_only: the mass and min h partials alone (Gamma and max nu come back as 0)
 void launch_diagnostics(const DevMesh &m, const double *h, const double *u, const StepConst &sc, double *part,
-                        double *out_dev, cudaStream_t s);
+                        double *out_dev, cudaStream_t s, bool cells_only = false);
 
 }  // namespace fblts

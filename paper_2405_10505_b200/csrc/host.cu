@@ -1834,8 +1834,9 @@ void dd_merge_host(double &ah, double &al, double bh, double bl) {
     ah = hi;
 }
 
-int diag_partial(fblts_ctx *c, double out6[6]) {
-    launch_diagnostics(c->dm, c->hbuf[c->parity], c->ubuf[c->parity], c->sc, c->ds.diag, c->diag_out, c->stream);
+int diag_partial(fblts_ctx *c, double out6[6], bool cells_only = false) {
+    launch_diagnostics(c->dm, c->hbuf[c->parity], c->ubuf[c->parity], c->sc, c->ds.diag, c->diag_out, c->stream,
+                       cells_only);
     CUDA_TRY(c, cudaGetLastError());
     CUDA_TRY(c, cudaMemcpyAsync(out6, c->diag_out, 6 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -2031,6 +2032,29 @@ int fblts_diagnostics(fblts_ctx *c, double out[4]) {
         if (rc) return rc;
         diag_combine(all.data(), c->cfg.nranks, out);
     }
+    return check_device_error(c);
+}
+
+// Mass and min h only (the cell part of fblts_diagnostics): a cheap per-step monitor.
+int fblts_diagnostics_mass(fblts_ctx *c, double out[2]) {
+    if (!c || !out) return FBLTS_ERR_INVALID_ARG;
+    if (c->phase != P_STATE) return fail(c, FBLTS_ERR_ORDER, "diagnostics_mass: no state set");
+    if (c->cfg.nranks > 1 && !c->nccl)
+        return fail(c, FBLTS_ERR_ORDER, "diagnostics_mass: loopback contexts use fblts_diagnostics_group");
+    if (c->dstream) CUDA_TRY(c, cudaStreamSynchronize(c->dstream));
+    double part[6], four[4];
+    int rc = diag_partial(c, part, true);
+    if (rc) return rc;
+    if (c->cfg.nranks == 1) {
+        diag_combine(part, 1, four);
+    } else {
+        std::vector<double> all(6 * (size_t)c->cfg.nranks);
+        rc = allgather_nccl(c, part, all.data());
+        if (rc) return rc;
+        diag_combine(all.data(), c->cfg.nranks, four);
+    }
+    out[0] = four[0];
+    out[1] = four[2];
     return check_device_error(c);
 }
 

@@ -1608,9 +1608,10 @@ void launch_unpack(const int32_t *idx, const double *buf, double *a, int n, cuda
     if (n > 0) k_unpack<<<nblocks(n), TPB, 0, s>>>(idx, buf, a, n);
 }
 void launch_diagnostics(const DevMesh &m, const double *h, const double *u, const StepConst &sc, double *part,
-                        double *out_dev, cudaStream_t s) {
-    k_diag_partial<<<DIAG_BLOCKS, TPB, 0, s>>>(m, h, u, sc, part);
-    k_diag_final<<<1, TPB, 0, s>>>(part, DIAG_BLOCKS, out_dev);
+                        double *out_dev, cudaStream_t s, bool cells_only) {
+    const int nb = cells_only ? DIAG_RB : DIAG_BLOCKS;     // role 0 (mass, min h) is blocks [0, DIAG_RB)
+    k_diag_partial<<<nb, TPB, 0, s>>>(m, h, u, sc, part);
+    k_diag_final<<<1, TPB, 0, s>>>(part, nb, out_dev);
 }
 
 void launch_rk4_stage(const DevMesh &m, const DevState &st, int stage, const double *hN, const double *uN,

@@ -88,6 +88,10 @@ class Solver:
         self._pending.clear()
         return d
 
+    def diagnostics_mass(self):
+        """(total mass, min h) of the current state: the cell part of diagnostics(), same bits."""
+        return abi.fblts_diagnostics_mass(self.ctx)
+
     def diagnostics_async(self):
         """(mass, Gamma, min h, max nu) of the current state, filled in without synchronising: the
         returned array holds the values after the next sync() / state() / diagnostics()."""

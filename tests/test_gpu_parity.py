@@ -532,3 +532,17 @@ def test_diagnostics_async_match_sync(Solver):
     for g_, w in zip(got, want):
         assert np.array_equal(g_, w), (g_, w)
     assert np.all(np.isfinite(h))
+
+
+def test_diagnostics_mass_is_cell_part(Solver):
+    """fblts_diagnostics_mass = (mass, min h) of fblts_diagnostics, bit for bit, and the oracle's."""
+    c = configs.config1()
+    s = Solver(c.mesh, c.fine_mask, c.dt, c.M, g=c.g, beta=c.beta, rho0=c.rho0, tau_n=c.tau_n)
+    s.set_state(c.h0, c.u0)
+    for _ in range(4):
+        s.step(1)
+        d, dm = s.diagnostics(), s.diagnostics_mass()
+        assert dm[0] == d[0] and dm[1] == d[2]
+    h, _, _ = s.state()
+    m0 = dg.total_mass(c.mesh, h)
+    assert abs(dm[0] - m0) <= 1e-15 * m0 and dm[1] == np.min(h)
