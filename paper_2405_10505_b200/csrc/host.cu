@@ -606,9 +606,23 @@ int build_subtiles(fblts_ctx *c) {
         return es >= 0 ? es : ~es;
     };
     const int nT = (int)c->t_start.size() - 1;
-    for (int t = 0; t < nT; ++t) {
-        const int c0 = c->t_start[t], c1 = c->t_start[t + 1];
-        if (c0 < lo || c0 >= hi) continue;
+    // each staged tile of the range becomes nsplit subcycle tiles; nsplit doubles (up to 4) while the
+    // double-buffered footprint exceeds the shared memory (irregular tiles, e.g. on SCVT spheres)
+    for (int nsplit = 1;; nsplit *= 2) {
+    c->s_nT = 0;
+    c->s_info.assign(FTINFO, 0);
+    c->s_halo.clear();
+    c->s_fedge.clear();
+    c->s_ecl.clear();
+    c->s_row.clear();
+    c->s_hmax = c->s_emax = c->s_rmax = 0;
+    for (int tt = 0; tt < nT * nsplit; ++tt) {
+        const int t = tt / nsplit, part = tt % nsplit;
+        const int T0 = c->t_start[t], T1 = c->t_start[t + 1];
+        if (T0 < lo || T0 >= hi) continue;
+        const int c0 = T0 + (int)((int64_t)(T1 - T0) * part / nsplit);
+        const int c1 = T0 + (int)((int64_t)(T1 - T0) * (part + 1) / nsplit);
+        if (c1 <= c0) continue;
         R[0].clear();
         for (int i = c0; i < c1; ++i) R[0].push_back(i), ring[i] = 0;
         for (int k = 1; k <= 3; ++k) {
@@ -640,7 +654,19 @@ int build_subtiles(fblts_ctx *c) {
         std::sort(el.begin(), el.end());
         el.erase(std::unique(el.begin(), el.end()), el.end());
         const int32_t *trec = &c->t_info[(size_t)t * TINFO];
-        const int eo0 = trec[2], eo1 = trec[3], nOE = eo1 - eo0;
+        int eo0 = trec[2], eo1 = trec[3];
+        if (nsplit > 1) {           // the part's owned edges: the sub-run whose owner lies in [c0, c1)
+            int a = eo0, b, cnt = 0;
+            while (a < eo1 && c->e_owner[a] < c0) ++a;
+            for (b = a; b < eo1 && c->e_owner[b] < c1; ++b) {}
+            for (int e = trec[2]; e < trec[3]; ++e) cnt += c->e_owner[e] >= c0 && c->e_owner[e] < c1;
+            if (cnt != b - a) {     // owners not monotone along the run: no split
+                c->fuse_sub = false;
+                return FBLTS_OK;
+            }
+            eo0 = a, eo1 = b;
+        }
+        const int nOE = eo1 - eo0;
         for (auto &f : fl) f.clear();
         for (int e : el) {
             const int r0 = ring[c->d_coe[2 * e]], r1 = ring[c->d_coe[2 * e + 1]];
@@ -701,6 +727,8 @@ int build_subtiles(fblts_ctx *c) {
             for (int x : R[k]) ring[x] = -1, lidx[x] = -1;
         ++c->s_nT;
         c->s_info.resize((size_t)(c->s_nT + 1) * FTINFO, 0);
+    }
+    if (sub_smem_bytes_host(c->s_hmax, c->s_emax, c->s_rmax) <= TILE_SMEM_MAX || nsplit >= 4) break;
     }
     c->s_nHalo = c->s_halo.size(), c->s_nFedge = c->s_fedge.size(), c->s_nEcl = c->s_ecl.size();
     c->s_nRow = c->s_row.size();

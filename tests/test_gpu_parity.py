@@ -546,3 +546,19 @@ def test_diagnostics_mass_is_cell_part(Solver):
     h, _, _ = s.state()
     m0 = dg.total_mass(c.mesh, h)
     assert abs(dm[0] - m0) <= 1e-15 * m0 and dm[1] == np.min(h)
+
+
+def test_fused_subcycle_on_scvt_sphere(Solver, monkeypatch):
+    """The opt-in fused subcycle on the variable-resolution SCVT sphere (config-4 recipe at
+    dx_scale 4: pentagons to octagons, row stride G = 8, M = 8): bitwise equal to the oracle."""
+    c = configs.config4(dx_scale=4)
+    n = 5
+    ho, uo, _ = run_oracle(c, n)
+    monkeypatch.setenv("FBLTS_SUB", "1")
+    s, hg, ug, _ = run_gpu(Solver, c, n)
+    cnt = s.counts()
+    s.close()
+    if cnt["sub_tiles"] == 0:
+        pytest.skip(f"no subcycle tiles on this mesh ({cnt['cells_by_region']})")
+    assert_parity(hg, ug, ho, uo)
+    assert np.array_equal(hg, ho) and np.array_equal(ug, uo)
