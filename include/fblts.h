@@ -219,12 +219,14 @@ int fblts_get_state(fblts_ctx *ctx, double *h, double *u, double *t);
  * (NCCL) and combined in rank order, so every rank returns the same bits (synchronises). */
 int fblts_diagnostics(fblts_ctx *ctx, double out[4]);
 
-/* out[2] = { total mass, min h } of the current state: the cell part of fblts_diagnostics (same
- * reduction, same bits), a cheap per-step monitor (one pass over h and areaCell).  Synchronises;
+/* out[2] = { total mass sum A_i h_i (Theorem 1), min h (positivity) } of the current
+ * state: the cell part of fblts_diagnostics (same reduction, same bits), a cheap per-step monitor
+ * (one pass over h and areaCell).  Synchronises;
  * several ranks: NCCL all-gather, combined in rank order.  Errors: ORDER, CUDA, NCCL, POSITIVITY. */
 int fblts_diagnostics_mass(fblts_ctx *ctx, double out[2]);
 
-/* The same four numbers for the state after the steps enqueued so far, WITHOUT synchronising
+/* The same four numbers as fblts_diagnostics (Thms 1-2, eq. cfl) for the state after the steps
+ * enqueued so far, WITHOUT synchronising
  * (one rank): the reduction runs on a library stream that waits for the compute stream, its 48-byte
  * result is copied to pinned host memory and combined into out[4] by a host callback.  out must stay
  * valid until the next synchronising call (fblts_sync, fblts_get_state, fblts_diagnostics), after
