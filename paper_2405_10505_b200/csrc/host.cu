@@ -67,6 +67,12 @@ struct fblts_ctx {
     cudaStream_t cap = nullptr;
     cudaStream_t comm = nullptr;            // halo-exchange stream (nranks > 1)
     cudaEvent_t evFork = nullptr, evJoin = nullptr;
+    // one rank, captured steps: the band (interface) thickness sweeps of fine stages 2 and 3 run on
+    // `side`, concurrently with the staged deep sweep of the same stage (disjoint outputs, both read
+    // only the previous stage); FBLTS_BAND_SIDE=0 serialises them (development comparisons)
+    cudaStream_t side = nullptr;
+    cudaEvent_t evSideF = nullptr, evSideJ = nullptr;
+    bool band_side = true;
     std::string err;
     int phase = P_CREATED;
     HostMesh hm;
@@ -294,6 +300,7 @@ int fblts_create(fblts_ctx **out, const fblts_config *cfg) {
     if (const char *ev = std::getenv("FBLTS_SPLIT")) c->split = std::atoi(ev) != 0;
     if (const char *ev = std::getenv("FBLTS_FUSE")) c->fuse_vel = std::atoi(ev) != 0;
     if (const char *ev = std::getenv("FBLTS_SUB")) c->fuse_sub = std::atoi(ev) != 0;
+    if (const char *ev = std::getenv("FBLTS_BAND_SIDE")) c->band_side = std::atoi(ev) != 0;
     if (const char *ev = std::getenv("FBLTS_SUB_LEVEL")) c->sub_level = std::min(5, std::max(2, std::atoi(ev)));
     if (cfg->nranks != 1 || cfg->scheme != FBLTS_SCHEME_FBLTS || cfg->slow_refresh || cfg->unsplit) c->fuse_sub = false;
     // canonical constants (computed once in double, SURVEY c.1)
@@ -1259,6 +1266,11 @@ int fblts_bind_workspace(fblts_ctx *c, void *ptr, size_t bytes) {
     if ((uintptr_t)ptr % 256) return fail(c, FBLTS_ERR_INVALID_ARG, "bind_workspace: pointer not 256-B aligned");
     CUDA_TRY(c, cudaSetDevice(c->cfg.device));
     if (!c->cap) CUDA_TRY(c, cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
+    if (c->cfg.nranks == 1 && !c->side) {
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->evSideF, cudaEventDisableTiming));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->evSideJ, cudaEventDisableTiming));
+    }
     if (c->cfg.nranks > 1 && !c->comm) {
         CUDA_TRY(c, cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking));
         CUDA_TRY(c, cudaEventCreateWithFlags(&c->evFork, cudaEventDisableTiming));
@@ -1508,6 +1520,22 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
         pc.c = 1.0 - (double)(k + 1) / (double)M;
         return pc;
     };
+    // band sweep of fine stage 2 / 3 on the side stream (captured steps of one rank, staged path)
+    // (measured: config 2 0.263 -> 0.224 ms per step, hex2048 2.440 -> 2.432, config 5 9.49 -> 9.54:
+    // beside a long persistent deep sweep the band kernel only steals its SMs, so meshes of 8 M
+    // owned cells and more keep one stream)
+    const bool bandPar = !rec && T && c->side && c->band_side && c->cfg.nranks == 1 && m.nOwnC < (8 << 20);
+    auto band_fork = [&]() -> cudaStream_t {
+        if (!bandPar) return s;
+        cudaEventRecord(c->evSideF, s);
+        cudaStreamWaitEvent(c->side, c->evSideF, 0);
+        return c->side;
+    };
+    auto band_join = [&](cudaStream_t sb) {
+        if (sb == s) return;
+        cudaEventRecord(c->evSideJ, sb);
+        cudaStreamWaitEvent(s, c->evSideJ, 0);
+    };
     const int subBegin = B.fl[c->sub_level];
     const int deepEnd = SUB ? subBegin : B.end;    // the staged deep kernels stop where the subcycle tiles start
     *px = PhaseX{-1, nullptr, -1, nullptr};
@@ -1553,19 +1581,23 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
             // k >= 1 with the fusion: the band velocity sweep runs alone and the deep velocity sweep
             // of subcycle k-1 is folded into the deep stage-1 sweep of subcycle k (STAGE 4)
             const bool fused = k > 0 && T && (c->fuse_vel || SUB) && c->deep_runs_ok;
+            // stage 0 keeps the band sweeps on the compute stream: beside the persistent deep sweep the
+            // coarse / band velocity sweeps measured slower on hex2048 (2.51 vs 2.43 ms per step)
+            const bool par0 = false;
+            const cudaStream_t sv = par0 ? band_fork() : s;
             if (part == 0) {
                 if (k == 0) {
                     mark(K_COARSE_VEL);
-                    launch_coarse_vel(m, st, hN, uN, hNew, uNew, sc, s);
+                    launch_coarse_vel(m, st, hN, uN, hNew, uNew, sc, sv);
                 } else {
                     mark(K_FINE_VEL);
                     launch_fine_vel(m, st, hN, hNew, k - 1 == 0 ? hN : hb(k - 2), hb(k - 1),
-                                    k - 1 == 0 ? uN : ub(k - 2), ub(k - 1), sc, pred(k - 1), k - 1, s, !fused);
+                                    k - 1 == 0 ? uN : ub(k - 2), ub(k - 1), sc, pred(k - 1), k - 1, sv, !fused);
                 }
                 any = true;
             }
             cell_mark(K_FINE_S1);
-            launch_fine_s1(m, st, hN, hNew, hk, uk, sc, pred(k), k, s, B, !T);
+            if (!par0 || k == 0) launch_fine_s1(m, st, hN, hNew, hk, uk, sc, pred(k), k, sv, B, !T);
             if (fused) {
                 cell_mark(K_FINE_VS1);
                 StageArgs va{k - 1 == 0 ? hN : hb(k - 2), hk, k - 1 == 0 ? uN : ub(k - 2), st.Sf, st.h1,
@@ -1575,6 +1607,10 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
                 stage_tiled(c, 4, B, B.fl[1], deepEnd, va, s);
             } else if (T) {
                 stage_tiled(c, 1, B, B.fl[1], deepEnd, StageArgs{hk, hk, uk, st.S, st.h1, 0, 0, 0, sc.c1f, sc.g, K_FINE_S1, k}, s);
+            }
+            if (par0) {
+                band_join(sv);
+                if (k > 0) launch_fine_s1(m, st, hN, hNew, hk, uk, sc, pred(k), k, s, B, !T);
             }
             if (SUB && part == 0) {
                 // the whole subcycle k on F\F^2 (after the kernels above, which read level k-1 and
@@ -1606,17 +1642,21 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
                 any = true;
             }
             cell_mark(K_FINE_S2);
-            launch_fine_s2(m, st, hN, hNew, hk, uk, sc, pred(k), k, s, B, !T);
+            cudaStream_t sb = band_fork();
+            launch_fine_s2(m, st, hN, hNew, hk, uk, sc, pred(k), k, sb, B, !T);
             if (T)
                 stage_tiled(c, 2, B, B.fl[1], deepEnd,
                             StageArgs{hk, st.h1, uk, st.Sf, st.h2, sc.c1f, sc.b1, sc.omb1, sc.c2f, sc.g, K_FINE_S2, k}, s);
+            band_join(sb);
             *px = PhaseX{X_C1, st.h2, -1, nullptr};
         } else {
             cell_mark(K_FINE_S3);
-            launch_fine_s3(m, st, hN, uN, hNew, hk, uk, hb(k), sc, pred(k), k, s, B, !T);
+            cudaStream_t sb = band_fork();
+            launch_fine_s3(m, st, hN, uN, hNew, hk, uk, hb(k), sc, pred(k), k, sb, B, !T);
             if (T)
                 stage_tiled(c, 3, B, B.fl[1], deepEnd,
                             StageArgs{hk, st.h2, uk, st.Sf, hb(k), sc.c2f, sc.b2, sc.omb2, sc.c3f, sc.g, K_FINE_S3, k}, s);
+            band_join(sb);
             *px = PhaseX{X_C1, hb(k), -1, nullptr};
         }
     } else {                                     // ph == 3 + nfine: last velocity sweep, correction
@@ -2141,6 +2181,11 @@ void fblts_destroy(fblts_ctx *c) {
     if (c->comm) cudaStreamDestroy(c->comm);
     if (c->evFork) cudaEventDestroy(c->evFork);
     if (c->evJoin) cudaEventDestroy(c->evJoin);
+    if (c->side) {
+        cudaStreamDestroy(c->side);
+        cudaEventDestroy(c->evSideF);
+        cudaEventDestroy(c->evSideJ);
+    }
     if (c->dstream) {
         cudaStreamSynchronize(c->dstream);
         cudaStreamDestroy(c->dstream);

@@ -340,8 +340,8 @@ def test_unfused_and_unstaged_paths_agree(Solver, monkeypatch):
     c = configs.small_shelf(nx=64, ny=48, seed=9, dt=25.0)
     ho, uo, _ = run_oracle(c, 20)
     res = []
-    for env in ({}, {"FBLTS_FUSE": "0"}, {"FBLTS_TILED": "0"}, {"FBLTS_SPLIT": "1"}):
-        for k in ("FBLTS_FUSE", "FBLTS_TILED", "FBLTS_SPLIT"):
+    for env in ({}, {"FBLTS_FUSE": "0"}, {"FBLTS_TILED": "0"}, {"FBLTS_SPLIT": "1"}, {"FBLTS_BAND_SIDE": "0"}):
+        for k in ("FBLTS_FUSE", "FBLTS_TILED", "FBLTS_SPLIT", "FBLTS_BAND_SIDE"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
