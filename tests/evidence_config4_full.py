@@ -5,7 +5,7 @@ config's 100 coarse steps on the GPU, and time the step.  Writes a JSON summary 
 default gpurun_out/config4_full.json).  Development/evidence script: calls inputs/, oracle/ and
 the library through its Python binding.
 
-usage: python scripts/config4_full.py [out.json]
+usage: python tests/evidence_config4_full.py [out.json]
 """
 import json
 import os
