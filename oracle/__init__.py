@@ -1,7 +1,8 @@
 """Plain fp64 CPU oracle for FB-LTS (arXiv 2405.10505) -- TEST INFRASTRUCTURE ONLY.
 
-Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
-``--impl reference`` legs may import this package.  The product path
+Only ``tests/``, ``__graft_entry__.smoke()``, ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs and ``scripts/cfl_scan.py`` (which writes the stored time steps of
+``configs/dt.json`` from oracle calls only) may import this package.  The product path
 (``paper_2405_10505_b200``) never imports it, and this package never imports the
 product path: they share no code (only the seeded input generators in
 ``inputs/``, which hold none of the method's arithmetic).
