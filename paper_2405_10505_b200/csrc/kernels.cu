@@ -437,6 +437,15 @@ __device__ __forceinline__ void load_indices(const TileMesh &t, const TileRec &r
     }
 }
 
+// FBLTS_CHECK=1 (debug builds): device-side bounds checks of every shared-memory index the staged
+// kernel derives from its tile tables; a violation traps (the launch fails with a CUDA error)
+#ifndef FBLTS_CHECK
+#define FBLTS_CHECK 0
+#endif
+#define FBLTS_REQUIRE(cond)                  \
+    do {                                     \
+        if (FBLTS_CHECK && !(cond)) __trap(); \
+    } while (0)
 // development probes (never in the default build): FBLTS_PROBE=1 skips the compute of every tile
 // (copies only), 2 skips the copies (compute on whatever the buffers hold, no reports), 3 skips the
 // compute and the gathers (bulk copies only), 4 skips the compute and the bulk copies (gathers only)
@@ -508,6 +517,7 @@ __global__ void __launch_bounds__(NTHR, FBLTS_TILE_MINB) k_stage_tiled(DevMesh m
             A = m.areaCell[i];
         }
         const int nOE = cur.eo1 - cur.eo0, nLE = nOE + cur.f1 - cur.f0;
+        FBLTS_REQUIRE(nOwn <= TILE && HALO0 + (cur.h1 - cur.h0) + 1 <= CS2 && nLE + FGAP + 1 <= ES2 && nOE >= 0);
 #ifndef FBLTS_EDGE_UNROLL
 #define FBLTS_EDGE_UNROLL 1
 #endif
@@ -521,6 +531,8 @@ __global__ void __launch_bounds__(NTHR, FBLTS_TILE_MINB) k_stage_tiled(DevMesh m
                     const uint32_t pr = bc.ecl[p];
                     const int q = p < nOE ? p : p + FGAP;
                     const int l0 = pr & 0xFFFF, l1 = pr >> 16;
+                    FBLTS_REQUIRE((l0 < nOwn || (l0 >= HALO0 && l0 < HALO0 + cur.h1 - cur.h0)) &&
+                                  (l1 < nOwn || (l1 >= HALO0 && l1 < HALO0 + cur.h1 - cur.h0)));
                     const double H0 = bc.hp[l0], H1 = bc.hp[l1];
                     double ue = bc.u[q];
                     if (STAGE == 2 || STAGE == 3) {
@@ -547,6 +559,7 @@ __global__ void __launch_bounds__(NTHR, FBLTS_TILE_MINB) k_stage_tiled(DevMesh m
 #pragma unroll
             for (int j = 0; j < G; ++j) {
                 if (r[j] != TILE_SENT) {
+                    FBLTS_REQUIRE((r[j] & 0x7FFF) < nOE || ((r[j] & 0x7FFF) >= nOE + FGAP && (r[j] & 0x7FFF) < nLE + FGAP));
                     const double tt = bc.u[r[j] & 0x7FFF];
                     acc = acc + ((r[j] >> 15) ? -tt : tt);
                 }
