@@ -108,3 +108,31 @@ def test_rk4_scheme_is_single_rank(abi):
     with pytest.raises(abi.FbltsError) as ei:
         abi.fblts_create(10.0, 1, scheme="rk4", nranks=2, rank=0)
     assert ei.value.code == -1
+
+
+def test_subcycle_tiles_host_logic(abi, monkeypatch):
+    """Host side of the opt-in fused subcycle (FBLTS_SUB=1), no device: on a 128 x 128 block of the
+    config-5 recipe the subcycle tiles cover exactly the cells of F \\ F^5 (region code 8), their
+    ring lists and edge lists are non-empty, and the footprint fits the 227 KB of shared memory;
+    without the flag there are none."""
+    from inputs import configs
+    c = configs.config5(nx=128, ny=128)
+    for flag in ("1", None):
+        if flag:
+            monkeypatch.setenv("FBLTS_SUB", flag)
+        else:
+            monkeypatch.delenv("FBLTS_SUB", raising=False)
+        ctx = abi.fblts_create(c.dt, c.M)
+        try:
+            abi.fblts_upload_mesh(ctx, c.mesh)
+            abi.fblts_set_regions(ctx, c.fine_mask)
+            o = abi.fblts_get_counts(ctx)
+        finally:
+            abi.fblts_destroy(ctx)
+        n_tiles, n_ring, n_fedge, smem = (int(x) for x in o[28:32])
+        if flag:
+            deep = int(o[3 + 8])
+            assert deep > 0 and n_tiles >= deep // 256 and n_ring > 0 and n_fedge > 0
+            assert 0 < smem <= 227 * 1024
+        else:
+            assert n_tiles == 0 and smem == 0
