@@ -19,3 +19,27 @@ def test_reference_arm_json_line():
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
     assert line["config"]["workload"] == "config5"
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_native_arm_json_line_config1():
+    """The native arm on config 1 (one GPU, a few steps): the contract's keys, a roofline object for
+    the dominant kernel, the oracle cpu_baseline, the e2e number through the public API and the
+    launch count; run in a subprocess like the driver does."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    out = subprocess.run([sys.executable, "bench.py", "--config", "config1", "--steps", "3", "--warmup", "3"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=900, check=True).stdout
+    line = json.loads([ln for ln in out.splitlines() if ln.startswith("{")][-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert k in line, k
+    assert line["value"] > 0 and line["n_gpus"] == 1 and line["dtype"] == "f64" and line["gpu_launches"] > 0
+    r = line["roofline"]
+    assert r["bound"] == "hbm" and r["peak"] > 0 and r["achieved"] > 0 and r["unit"] == "GB/s"
+    assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
+    assert line["cpu_baseline"]["kind"] == "oracle"
