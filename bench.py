@@ -273,7 +273,9 @@ def arm_native(args):
     import torch.distributed as dist
 
     from paper_2405_10505_b200 import Solver
+    from paper_2405_10505_b200 import _abi
 
+    build_info = _abi.require_default_build()        # never time a probe / bounds-checked build
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
@@ -446,7 +448,7 @@ def arm_native(args):
                          "working set may be L2-resident (no flush)",
                    "parallelism": "1 GPU" if world == 1 else
                    f"{world} GPUs, dual-set SFC partition of one mesh, NCCL halo exchange per stage",
-                   "setup_s": round(t_setup, 1)},
+                   "setup_s": round(t_setup, 1), "build": build_info},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "bytes_per_launch": bm[dom] / launches_dom,
                      "launch_ms": dom_ms, "share_of_step": t_step[dom] / prof_total, "peak_source": peak_src,

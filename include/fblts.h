@@ -114,7 +114,8 @@ typedef struct {
     int32_t scheme;      /* FBLTS_SCHEME_FBLTS (0): FB-LTS, split mode (global FB-RK(3,2) when there are
                             no fine cells or M = 1); FBLTS_SCHEME_RK4 (1): classical four-stage RK4 on
                             the unsplit system, global (M and the fine mask ignored), one
-                            rank -- the paper's reference scheme, for speedup comparisons */
+                            rank -- the paper's reference scheme, for speedup comparisons;
+                            FBLTS_SCHEME_RK32 (2): RK(3,2) on the unsplit system, global, one rank */
     int32_t slow_refresh;/* 1: the paper's proposed variant: the slow tendency is
                             re-evaluated at every fine level t^{n,k} and used on the fine edges
                             (DESIGN.md 3 for the reading); FB-LTS scheme, one rank.  0: frozen S */
@@ -132,6 +133,8 @@ typedef struct {
 
 #define FBLTS_SCHEME_FBLTS 0
 #define FBLTS_SCHEME_RK4   1
+#define FBLTS_SCHEME_RK32  2   /* RK(3,2) of Wicker & Skamarock on the unsplit system, global,
+                                  one rank: the scheme FB-RK(3,2) extends (Table-1 analogue baseline) */
 
 /* Create a context.  *out receives the handle (NULL on failure).
  * Errors: INVALID_ARG (M < 1, dt <= 0, r < 1, bad rank/nranks), CUDA, NCCL. */
@@ -241,6 +244,11 @@ int fblts_diagnostics_async(fblts_ctx *ctx, double *out);
 #define FBLTS_NUM_KERNELS 15
 int fblts_profile(fblts_ctx *ctx, int32_t n_coarse, double *ms, int64_t *launches);
 const char *fblts_kernel_name(int32_t kind);
+
+/* Compile-time configuration of this library build, e.g. "probe=0 check=0 tile=256 ...": probe != 0
+ * is a development build that skips work (never a measurement), check != 0 adds device-side bounds
+ * traps.  Static string, no context needed. */
+const char *fblts_build_info(void);
 
 const char *fblts_last_error(const fblts_ctx *ctx);
 void fblts_destroy(fblts_ctx *ctx);

@@ -121,6 +121,35 @@ def fbrk32_step(mesh, h, u, dt, phys, split=True, stages=False):
     return out[1], out[0]
 
 
+def rk32_generic(Phi, Psi, u, h, dt):
+    """One step of RK(3,2), the three-stage second-order Runge-Kutta scheme of Wicker & Skamarock
+    (2002) that FB-RK(3,2) extends (subsec. fbrk32): every stage evaluates both
+    tendencies at the previous stage's (u, h), no forward-backward averaging:
+        stage 1:  h1 = h^n + dt/3 Psi(u^n, h^n);  u1 = u^n + dt/3 Phi(u^n, h^n)
+        stage 2:  h2 = h^n + dt/2 Psi(u1, h1);    u2 = u^n + dt/2 Phi(u1, h1)
+        stage 3:  h3 = h^n + dt   Psi(u2, h2);    u3 = u^n + dt   Phi(u2, h2)
+    For y' = lambda y the step multiplies by R(z) = 1 + z + z^2/2 + z^3/6 (z = lambda dt): stable on
+    the imaginary axis iff |z| <= sqrt(3).  Works on numpy arrays or exact fractions."""
+    c1 = dt / 3
+    c2 = dt / 2
+    c3 = dt
+    h1 = h + c1 * Psi(u, h)
+    u1 = u + c1 * Phi(u, h)
+    h2 = h + c2 * Psi(u1, h1)
+    u2 = u + c2 * Phi(u1, h1)
+    h3 = h + c3 * Psi(u2, h2)
+    u3 = u + c3 * Phi(u2, h2)
+    return u3, h3
+
+
+def rk32_step(mesh, h, u, dt, phys):
+    """RK(3,2) on the unsplit system (u, h), global (the baseline FB-RK(3,2) extends, P:L283-285;
+    the Table-1 analogue's third scheme)."""
+    Phi, Psi = mesh_tendencies(mesh, phys, None)
+    u3, h3 = rk32_generic(Phi, Psi, u, h, dt)
+    return h3, u3
+
+
 def rk4_generic(f, y, dt):
     """Classical four-stage RK4 ("classical, four-stage, fourth order")."""
     k1 = f(y)

@@ -47,7 +47,7 @@ class fblts_config(C.Structure):
                 ("scheme", C.c_int32), ("slow_refresh", C.c_int32), ("sal_beta", C.c_double),
                 ("unsplit", C.c_int32), ("pv_energy", C.c_int32)]
 
-SCHEMES = {"fblts": 0, "rk4": 1}
+SCHEMES = {"fblts": 0, "rk4": 1, "rk32": 2}
 
 
 class FbltsError(RuntimeError):
@@ -83,6 +83,7 @@ _lib_diag_mass = _sig("fblts_diagnostics_mass", C.c_int, _vp, _f64p)
 _lib_profile = _sig("fblts_profile", C.c_int, _vp, C.c_int32, _f64p, C.POINTER(C.c_int64))
 _lib_kname = _sig("fblts_kernel_name", C.c_char_p, C.c_int32)
 _lib_last_error = _sig("fblts_last_error", C.c_char_p, _vp)
+_lib_build_info = _sig("fblts_build_info", C.c_char_p)
 _lib_destroy = _sig("fblts_destroy", None, _vp)
 _i64p = C.POINTER(C.c_int64)
 _lib_halo = _sig("fblts_get_halo", C.c_int, _vp, C.c_int32, C.c_int32, _i64p, _i64p, _i64p, _i64p)
@@ -95,7 +96,7 @@ EXPORTED = ["fblts_create", "fblts_upload_mesh", "fblts_set_regions", "fblts_get
             "fblts_set_forcing", "fblts_set_hurricane", "fblts_set_state", "fblts_step", "fblts_step_group", "fblts_diagnostics_group",
             "fblts_sync", "fblts_get_state", "fblts_diagnostics", "fblts_diagnostics_async", "fblts_diagnostics_mass",
             "fblts_profile",
-            "fblts_kernel_name",
+            "fblts_kernel_name", "fblts_build_info",
             "fblts_last_error", "fblts_destroy"]
 
 
@@ -145,10 +146,12 @@ def fblts_upload_mesh(ctx, mesh):
               "bottomDepth", "xCell", "yCell", "zCell"):
         setattr(m, k, _ptr(f64(k), C.c_double))
     _check(ctx, _lib_upload(ctx, C.byref(m)))
+    _MESH_SIZES[_key(ctx)] = (int(mesh.nCells), int(mesh.nEdges))
 
 
 def fblts_set_regions(ctx, fine_mask):
     a = _arr(fine_mask, np.uint8)
+    _check_len(a, _sizes(ctx)[0], "fine_mask")
     _check(ctx, _lib_regions(ctx, _ptr(a, C.c_uint8)))
 
 
@@ -212,6 +215,7 @@ def fblts_set_forcing(ctx, tau_n):
         _check(ctx, _lib_forcing(ctx, None))
     else:
         a = _arr(tau_n, np.float64)
+        _check_len(a, _sizes(ctx)[1], "tau_n")
         _check(ctx, _lib_forcing(ctx, _ptr(a, C.c_double)))
 
 
@@ -221,22 +225,51 @@ def fblts_set_hurricane(ctx, uw_n, uw_t, cd, cw):
         _check(ctx, _lib_hurricane(ctx, None, None, 0.0, 0.0))
     else:
         a, b = _arr(uw_n, np.float64), _arr(uw_t, np.float64)
+        _check_len(a, _sizes(ctx)[1], "uw_n")
+        _check_len(b, _sizes(ctx)[1], "uw_t")
         _check(ctx, _lib_hurricane(ctx, _ptr(a, C.c_double), _ptr(b, C.c_double), float(cd), float(cw)))
 
 
-def _host_ptr(x):
-    """numpy array or (pinned) CPU torch tensor -> (pointer, keepalive)."""
+def _host_ptr(x, n=None, what="buffer"):
+    """numpy array or (pinned) CPU torch tensor -> (pointer, keepalive); n: required element count
+    (checked here, so a short host buffer raises instead of being overrun by the C side)."""
     if isinstance(x, np.ndarray):
         a = _arr(x, np.float64)
-        return _ptr(a, C.c_double), a
-    if x.dtype != __import__("torch").float64 or x.device.type != "cpu" or not x.is_contiguous():
-        raise ValueError("host buffers must be contiguous float64 CPU tensors or numpy arrays")
-    return C.cast(x.data_ptr(), _f64p), x
+        size = a.size
+        p = (_ptr(a, C.c_double), a)
+    else:
+        if x.dtype != __import__("torch").float64 or x.device.type != "cpu" or not x.is_contiguous():
+            raise ValueError("host buffers must be contiguous float64 CPU tensors or numpy arrays")
+        size = x.numel()
+        p = (C.cast(x.data_ptr(), _f64p), x)
+    if n is not None and size != n:
+        raise ValueError(f"{what}: {size} elements, expected {n}")
+    return p
+
+
+_MESH_SIZES = {}          # context handle -> (nCells, nEdges) of its uploaded (global) mesh
+
+
+def _key(ctx):
+    return ctx.value if isinstance(ctx, _vp) else ctx
+
+
+def _sizes(ctx):
+    """(nCells, nEdges) of the uploaded (global) mesh."""
+    if _key(ctx) not in _MESH_SIZES:
+        raise FbltsError(-8, "upload_mesh first (host buffer sizes unknown)")
+    return _MESH_SIZES[_key(ctx)]
+
+
+def _check_len(a, n, what):
+    if a.size != n:
+        raise ValueError(f"{what}: {a.size} elements, expected {n}")
 
 
 def fblts_set_state(ctx, h, u, t=0.0):
-    ph, kh = _host_ptr(h)
-    pu, ku = _host_ptr(u)
+    nC, nE = _sizes(ctx)
+    ph, kh = _host_ptr(h, nC, "h")
+    pu, ku = _host_ptr(u, nE, "u")
     _check(ctx, _lib_set_state(ctx, ph, pu, float(t)))
 
 
@@ -250,8 +283,9 @@ def fblts_sync(ctx):
 
 def fblts_get_state(ctx, h_out, u_out):
     """Fill host buffers (numpy arrays or CPU tensors) with the state; returns t."""
-    ph, kh = _host_ptr(h_out) if h_out is not None else (None, None)
-    pu, ku = _host_ptr(u_out) if u_out is not None else (None, None)
+    nC, nE = _sizes(ctx)
+    ph, kh = _host_ptr(h_out, nC, "h_out") if h_out is not None else (None, None)
+    pu, ku = _host_ptr(u_out, nE, "u_out") if u_out is not None else (None, None)
     if isinstance(h_out, np.ndarray) and kh is not h_out or isinstance(u_out, np.ndarray) and ku is not u_out:
         raise ValueError("get_state needs contiguous float64 numpy outputs")
     t = C.c_double()
@@ -287,6 +321,21 @@ def fblts_profile(ctx, n_coarse):
     return ms, cnt
 
 
+def fblts_build_info():
+    """Compile-time knobs of the loaded library as a dict, e.g. {"probe": "0", "check": "0", ...}."""
+    return dict(kv.split("=", 1) for kv in _lib_build_info().decode().split())
+
+
+def require_default_build():
+    """Raise unless the loaded library is a measurement build (no FBLTS_PROBE work skipping, no
+    FBLTS_CHECK bounds traps) -- bench.py calls this before timing anything."""
+    info = fblts_build_info()
+    if info.get("probe") != "0" or info.get("check") != "0":
+        raise RuntimeError(f"libfblts.so is a development build ({info}); rebuild with "
+                           "`python -m paper_2405_10505_b200.build --force` before measuring")
+    return info
+
+
 def fblts_kernel_name(kind):
     return _lib_kname(int(kind)).decode()
 
@@ -296,4 +345,5 @@ def fblts_last_error(ctx):
 
 
 def fblts_destroy(ctx):
+    _MESH_SIZES.pop(_key(ctx), None)
     _lib_destroy(ctx)

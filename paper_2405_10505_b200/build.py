@@ -38,25 +38,47 @@ def nvcc():
     return "nvcc"
 
 
-def up_to_date():
-    if not os.path.exists(LIB):
+STAMP = LIB + ".flags"          # the nvcc flags of the library on disk (a rebuild is due when they change)
+
+
+def _extra():
+    return os.environ.get("FBLTS_NVCC_EXTRA", "").split()      # development knobs, e.g. -DFBLTS_MINB=8
+
+
+def _flags_key(extra):
+    return " ".join(NVCC_FLAGS + extra)
+
+
+def up_to_date(extra=None):
+    """The library exists, is newer than every source and header, and was built with the same flags
+    (FBLTS_NVCC_EXTRA included): a development build (-DFBLTS_PROBE=1, ...) is never reused by a
+    default build()."""
+    extra = _extra() if extra is None else extra
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
         return False
+    with open(STAMP) as f:
+        if f.read().strip() != _flags_key(extra):
+            return False
     t = os.path.getmtime(LIB)
     return all(os.path.getmtime(s) <= t for s in SOURCES + HEADERS)
 
 
 def build(force=False, verbose=False):
-    if not force and up_to_date():
+    extra = _extra()
+    if not force and up_to_date(extra):
         return LIB
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    extra = os.environ.get("FBLTS_NVCC_EXTRA", "").split()      # development knobs, e.g. -DFBLTS_MINB=8
     nccl = nccl_root()
     cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(HERE, "csrc"),
            "-I" + os.path.join(nccl, "include"), "-o", LIB, *SOURCES,
            "-L" + os.path.join(nccl, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(nccl, "lib")]
     if verbose:
         print(" ".join(cmd), flush=True)
+    if os.path.exists(STAMP):
+        os.unlink(STAMP)
     subprocess.run(cmd, check=True)
+    with open(STAMP, "w") as f:
+        f.write(_flags_key(extra) + "\n")
     return LIB
 
 

@@ -281,8 +281,9 @@ int fblts_create(fblts_ctx **out, const fblts_config *cfg) {
         return FBLTS_ERR_INVALID_ARG;
     if (!(cfg->sal_beta >= 0.0 && cfg->sal_beta < 1.0)) return FBLTS_ERR_INVALID_ARG;
     if (cfg->nranks < 1 || cfg->nranks > 64 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return FBLTS_ERR_INVALID_ARG;
-    if (cfg->scheme != FBLTS_SCHEME_FBLTS && cfg->scheme != FBLTS_SCHEME_RK4) return FBLTS_ERR_INVALID_ARG;
-    if (cfg->scheme == FBLTS_SCHEME_RK4 && cfg->nranks != 1) return FBLTS_ERR_INVALID_ARG;   // reference scheme: one rank
+    if (cfg->scheme != FBLTS_SCHEME_FBLTS && cfg->scheme != FBLTS_SCHEME_RK4 && cfg->scheme != FBLTS_SCHEME_RK32)
+        return FBLTS_ERR_INVALID_ARG;
+    if (cfg->scheme != FBLTS_SCHEME_FBLTS && cfg->nranks != 1) return FBLTS_ERR_INVALID_ARG;   // reference schemes: one rank
     if (cfg->slow_refresh && (cfg->nranks != 1 || cfg->scheme != FBLTS_SCHEME_FBLTS)) return FBLTS_ERR_INVALID_ARG;
     if (cfg->unsplit && (cfg->nranks != 1 || cfg->scheme != FBLTS_SCHEME_FBLTS || cfg->slow_refresh))
         return FBLTS_ERR_INVALID_ARG;
@@ -888,6 +889,10 @@ int build_local(fblts_ctx *c, const std::vector<int32_t> &coc) {
     c->sE = pad32(L.nE);
     c->sV = pad32(L.nV);
     const int sE = c->sE, sV = c->sV, G = c->ecS = m.maxE <= 6 ? 6 : (m.maxE <= 8 ? 8 : 16);
+    // the kernels index the slot-major tables ([slot][stride]) and the cell rows in 32-bit int
+    if ((int64_t)std::max(m.maxE2, 1) * sE > INT32_MAX || 3LL * sV > INT32_MAX || (int64_t)L.nC * G * 2 > INT32_MAX)
+        return fail(c, FBLTS_ERR_MESH, "subdomain too large for 32-bit slot indices (nE=%d, maxEdges2=%d, nV=%d, "
+                    "nC=%d): partition over more ranks", L.nE, m.maxE2, L.nV, L.nC);
     c->d_nEoC.assign(L.nC, 0);
     c->d_ec.assign((size_t)L.nC * G * 2, 0);
     c->d_area.assign(L.nC, 0.0);
@@ -1174,7 +1179,7 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
     put(s.qe, c->cfg.pv_energy ? (size_t)L.nE : 1);
     put(s.accH, std::max(1, L.nOwnC));
     put(s.accU, std::max(1, L.eb.f - L.eb.if2));
-    const size_t nrk = c->cfg.scheme == FBLTS_SCHEME_RK4 ? nE1 : 1;
+    const size_t nrk = c->cfg.scheme != FBLTS_SCHEME_FBLTS ? nE1 : 1;
     put(s.rkU[0], nrk);
     put(s.rkU[1], nrk);
     put(s.rkAccU, nrk);
@@ -1326,7 +1331,15 @@ int fblts_bind_workspace(fblts_ctx *c, void *ptr, size_t bytes) {
         CUDA_TRY(c, up(sm.row, c->s_row.data(), c->s_row.size() * 2));
     }
     if (stage_tiled_smem_bytes_host(4, c->t_hmax, c->t_emax) > TILE_SMEM_MAX) c->split = true;    // size launches per block
-    if (stage_tiled_smem_bytes_host(4, c->t_hmax, c->t_emax) > TILE_SMEM_MAX && !c->split) c->tiled = false;
+    if (c->tiled) {   // stage_tiled_run halves a launch until it fits, down to one tile: every tile must fit alone
+        for (size_t t = 0; t + 1 < c->t_start.size(); ++t) {
+            const int32_t *r = &c->t_info[t * TINFO], *n = r + TINFO;
+            if (stage_tiled_smem_bytes_host(4, n[1] - r[1], r[3] - r[2] + n[4] - r[4]) > TILE_SMEM_MAX) {
+                c->tiled = false;        // untiled per-thread kernels instead (same arithmetic, same bits)
+                break;
+            }
+        }
+    }
     CUDA_TRY(c, cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->cfg.device));
     if (c->tiled) CUDA_TRY(c, (cudaError_t)stage_tiled_configure(d));
     CUDA_TRY(c, cudaStreamSynchronize(s));
@@ -1753,6 +1766,37 @@ int enqueue_rk4_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
     return FBLTS_OK;
 }
 
+// One RK(3,2) step (FBLTS_SCHEME_RK32, one rank; Wicker & Skamarock, the scheme FB-RK(3,2) extends,
+// P:L283-285; oracle fbrk32.rk32_step): stage s = 1, 2, 3 evaluates the slow terms at the previous
+// stage's (u, h), then one launch over every cell and edge writes (h, u)_s = (h, u)^n + c_s (Psi, Phi^fast
+// + S) with c_s = dt/3, dt/2, dt (no running sum: launch_rk4_stage with stage 0).
+int enqueue_rk32_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
+    const DevMesh &m = c->dm;
+    DevState st = c->ds;
+    const double *hN = c->hbuf[par], *uN = c->ubuf[par];
+    double *hNew = c->hbuf[1 - par], *uNew = c->ubuf[1 - par];
+    const double dt = c->cfg.dt;
+    const double cs[3] = {dt / 3.0, dt / 2.0, dt};
+    const double *hs = hN, *us = uN;
+    double *hb[2] = {st.h1, st.h2};
+    for (int stage = 1; stage <= 3; ++stage) {
+        if (c->cfg.slow) {
+            if (rec) rec->mark(K_SLOW_PRE, s);
+            launch_slow_pre(m, st, hs, us, s);
+            if (rec) rec->mark(K_SLOW_EDGE, s);
+            launch_slow_edge(m, st, hs, us, c->sc, s);
+        }
+        double *ho = stage < 3 ? hb[stage % 2] : hNew;
+        double *uo = stage < 3 ? st.rkU[stage % 2] : uNew;
+        if (rec) rec->mark(K_RK4_STAGE, s);
+        launch_rk4_stage(m, st, 0, hN, uN, hs, us, ho, uo, cs[stage - 1], 0.0, c->sc.g, s);
+        hs = ho;
+        us = uo;
+    }
+    if (rec) rec->mark(-1, s);
+    return FBLTS_OK;
+}
+
 // One unsplit FB-LTS coarse step (config unsplit, one rank): per stage a thickness
 // sweep with the stored stage velocity, the FB-averaged thickness (coarse) or the stage's HS and U
 // views (fine), the slow sweeps on the stage's extent and the velocity sweep (oracle lts.py split=False).
@@ -1842,6 +1886,7 @@ int enqueue_unsplit_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
 
 int enqueue_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
     if (c->cfg.scheme == FBLTS_SCHEME_RK4) return enqueue_rk4_step(c, par, s, rec);
+    if (c->cfg.scheme == FBLTS_SCHEME_RK32) return enqueue_rk32_step(c, par, s, rec);
     if (c->cfg.unsplit) return enqueue_unsplit_step(c, par, s, rec);
     const bool multi = c->cfg.nranks > 1;
     PhaseX px, px1;

@@ -894,6 +894,12 @@ __global__ void __launch_bounds__(TPB) k_rk4_stage(DevMesh m, int stage, const d
         acc = accU;
         out = uout;
     }
+    if (stage == 0) {                     // RK(3,2) stage: base + c_s k, no running sum
+        const double v = base + cnext * kx;
+        out[x] = v;
+        if (blockIdx.x < nbC && !(v > 0.0)) report(err, K_RK4_STAGE, stage, x, v);
+        return;
+    }
     double sum;
     if (stage == 1) sum = kx;
     else if (stage == 4) sum = acc[x] + kx;
@@ -1801,3 +1807,18 @@ void launch_un_fstage(const DevMesh &m, const DevState &st, int stage, const dou
     });
 }
 }  // namespace fblts
+
+// Build configuration of this library (fblts_build_info, include/fblts.h): the compile-time
+// knobs that change what the kernels do.  A development build (FBLTS_PROBE != 0 skips work,
+// FBLTS_CHECK != 0 adds device bounds traps) must never produce a bench number.
+#define FBLTS_STR2(x) #x
+#define FBLTS_STR(x) FBLTS_STR2(x)
+extern "C" const char *fblts_build_info(void) {
+    return "probe=" FBLTS_STR(FBLTS_PROBE) " check=" FBLTS_STR(FBLTS_CHECK) " tile=" FBLTS_STR(FBLTS_TILE)
+           " tile_minb=" FBLTS_STR(FBLTS_TILE_MINB) " tile_nbuf=" FBLTS_STR(FBLTS_TILE_NBUF)
+           " tile_nthr=" FBLTS_STR(FBLTS_TILE_NTHR) " minb=" FBLTS_STR(FBLTS_MINB)
+#if defined(__CUDACC__)
+           " fmad=off arch=sm_100a"
+#endif
+        ;
+}

@@ -3,10 +3,20 @@
 
 Calls only inputs/ and oracle/; writes configs/dt.json.  Predicate: 300 coarse steps, unstable if
 any value is non-finite or max|u| > 5 m/s.  Bracket [0.5, 1.0] x the step at which
-nu_loc = nu_max_FBRK = 3.8621532/sqrt(6).  The run uses dt = 0.9 x the largest stable step found.
+nu_loc = nu_max of the scheme (FB-RK(3,2): 3.8621532/sqrt(6); RK(3,2): sqrt(3)/sqrt(6); RK4:
+2 sqrt(2)/sqrt(6)); when the top of the bracket is still stable the bracket is widened (x 1.25, up to
+8 times) until a step is unstable, then bisected; if no unstable step is ever found the entry records
+unstable_dt = null and the scheme's dt is a lower bound.  The run uses dt = 0.9 x the largest stable
+step found.
 
-usage: python scripts/cfl_scan.py config1 [config2 config5]
+Schemes (suffix of the entry name): none = FB-LTS (frozen slow terms, the paper's split mode);
+_refresh = FB-LTS with the slow-term refresh at every fine level; _global = global
+FB-RK(3,2) (split, no fine cells, M = 1); _rk32 = global RK(3,2) (Wicker-Skamarock, unsplit,
+P:L283-285); _rk4 = global classical RK4 (unsplit).
+
+usage: python scripts/cfl_scan.py config1 [config2 config5 config5_rk4 ...]
 """
+import fcntl
 import json
 import os
 import sys
@@ -22,6 +32,8 @@ from oracle import fbrk32, lts                  # noqa: E402
 
 NU_MAX_FBRK = 3.8621532 / np.sqrt(6.0)
 NU_MAX_RK4 = 2.0 * np.sqrt(2.0) / np.sqrt(6.0)
+NU_MAX_RK32 = np.sqrt(3.0) / np.sqrt(6.0)
+SCHEMES = ("refresh", "global", "rk32", "rk4")
 OUT = configs.DT_TABLE
 
 
@@ -32,29 +44,41 @@ def stable(case, lab, dt, steps=300, scheme="fblts"):
         for _ in range(steps):
             if scheme == "rk4":
                 h, u = fbrk32.rk4_step(case.mesh, h, u, dt, phys)
+            elif scheme == "rk32":
+                h, u = fbrk32.rk32_step(case.mesh, h, u, dt, phys)
+            elif scheme == "global":
+                h, u = fbrk32.fbrk32_step(case.mesh, h, u, dt, phys)
             else:
-                h, u = lts.fblts_step(case.mesh, lab, h, u, dt, case.M, phys)
+                h, u = lts.fblts_step(case.mesh, lab, h, u, dt, case.M, phys, slow_refresh=scheme == "refresh")
             if not (np.all(np.isfinite(u)) and np.all(np.isfinite(h))) or np.max(np.abs(u)) > 5.0:
                 return False
     return True
 
 
-def scan(name, case, iters=6, scheme="fblts"):
-    """scheme "rk4": the global classical RK4 reference, bracket top at its imaginary-axis
-    limit 2 sqrt(2) / sqrt(6) of the hex gravity-wave Courant number."""
-    if scheme == "rk4":
+def scan(name, case, iters=6, scheme="fblts", widen=8):
+    """scheme rk4 / rk32 / global: a global reference scheme (no fine cells, M = 1), bracket top at
+    its own imaginary-axis limit in units of the hex gravity-wave Courant number."""
+    if scheme in ("rk4", "rk32", "global"):
         case.fine_mask = np.zeros(case.mesh.nCells, dtype=bool)
         case.M = 1
     lab = lts.label_regions(case.mesh, case.fine_mask)
     nu1 = dg.rest_courant(case.mesh, lab, 1.0, case.M, case.g)
-    top = (NU_MAX_RK4 if scheme == "rk4" else NU_MAX_FBRK) / nu1
+    nu_top = {"rk4": NU_MAX_RK4, "rk32": NU_MAX_RK32}.get(scheme, NU_MAX_FBRK)
+    top = nu_top / nu1
     lo, hi = 0.5 * top, 1.0 * top
     t0 = time.time()
     if not stable(case, lab, lo, scheme=scheme):
         raise RuntimeError(f"{name}: unstable at the bracket bottom {lo:.3f} s")
-    if stable(case, lab, hi, scheme=scheme):
+    n_widen = 0
+    while stable(case, lab, hi, scheme=scheme):        # widen until the top is unstable
         lo = hi
-    else:
+        if n_widen == widen:
+            hi = None
+            break
+        hi *= 1.25
+        n_widen += 1
+        print(f"  {name}: stable at {lo:.3f} s, widening to {hi:.3f} s  ({time.time() - t0:.0f} s)", flush=True)
+    if hi is not None:
         for _ in range(iters):
             mid = 0.5 * (lo + hi)
             if stable(case, lab, mid, scheme=scheme):
@@ -64,14 +88,17 @@ def scan(name, case, iters=6, scheme="fblts"):
             print(f"  {name}: [{lo:.3f}, {hi:.3f}] s  ({time.time() - t0:.0f} s)", flush=True)
     dt = 0.9 * lo
     return {"dt": dt, "stable_dt": lo, "unstable_dt": hi, "nu_loc_limit": lo * nu1,
-            "nu_loc_run": dt * nu1, "bracket_top_dt": top, "predicate": "300 steps, finite, max|u| <= 5",
-            "M": case.M, "nCells": case.mesh.nCells}
+            "nu_loc_run": dt * nu1, "bracket_top_dt": top, "widened": n_widen,
+            "bound_only": hi is None, "predicate": "300 steps, finite, max|u| <= 5",
+            "M": case.M, "nCells": case.mesh.nCells, "scan_seconds": round(time.time() - t0)}
 
 
 def main(names):
     for name in names:
-        scheme = "rk4" if name.endswith("_rk4") else "fblts"
-        base = name[:-4] if scheme == "rk4" else name
+        scheme, base = "fblts", name
+        for sch in SCHEMES:
+            if name.endswith("_" + sch):
+                scheme, base = sch, name[:-len(sch) - 1]
         if base == "config1":
             case = configs.config1(dt=1.0)
         elif base == "config2":
@@ -80,6 +107,11 @@ def main(names):
             # the level-5 dual (10,242 cells) of the config-3 recipe; the Courant limit nu_loc
             # is applied to the level-8 mesh by inputs.configs.config3
             case = configs.config3(level=5, dt=1.0)
+        elif base == "config4_full":
+            # the full config-4 mesh (N = 796,141): ~30 min of oracle time per 300-step trial
+            case = configs.config4(dt=1.0)
+        elif base == "config3_full":
+            case = configs.config3(dt=1.0)
         elif base == "config4":
             # the dx_scale = 8 reduction of the config-4 recipe (~12 k cells, same disk, shelf and
             # M = 8); the Courant limit nu_loc is applied to the full mesh by inputs.configs.config4
@@ -97,9 +129,13 @@ def main(names):
         if base == "config5":
             res["proxy"] = "512x296 cells (one 256-km x-tile, 128 km in y, dc = 500 m, 1 bump, seed 5)"
         print(name, res, flush=True)
-        table = json.load(open(OUT)) if os.path.exists(OUT) else {}
-        table[name] = res
-        json.dump(table, open(OUT, "w"), indent=2, sort_keys=True)
+        with open(OUT + ".lock", "w") as lk:            # several scans may run side by side
+            fcntl.flock(lk, fcntl.LOCK_EX)
+            table = json.load(open(OUT)) if os.path.exists(OUT) else {}
+            table[name] = res
+            with open(OUT, "w") as f:
+                json.dump(table, f, indent=2, sort_keys=True)
+                f.write("\n")
 
 
 if __name__ == "__main__":

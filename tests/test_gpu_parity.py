@@ -73,6 +73,7 @@ def test_parity_100_steps(Solver, which):
     s, hg, ug, t = run_gpu(Solver, c, n)
     eh, eu = assert_parity(hg, ug, ho, uo)
     print(f"{which}: eps_h={eh:.3e} eps_u={eu:.3e} bitwise={np.array_equal(hg, ho) and np.array_equal(ug, uo)}")
+    assert np.array_equal(hg, ho) and np.array_equal(ug, uo), "not bitwise (canonical arithmetic, --fmad=false)"
     assert t == pytest.approx(n * c.dt)
     cell, edge = s.labels()
     assert np.array_equal(cell, lab.cell) and np.array_equal(edge, lab.edge)
@@ -281,6 +282,7 @@ def test_parity_config5_full_size(Solver):
     s, hg, ug, _ = run_gpu(Solver, c, 1)
     eh, eu = assert_parity(hg, ug, ho, uo)
     print(f"config5 full size, 1 step: eps_h={eh:.3e} eps_u={eu:.3e} bitwise={np.array_equal(hg, ho) and np.array_equal(ug, uo)}")
+    assert np.array_equal(hg, ho) and np.array_equal(ug, uo), "not bitwise (canonical arithmetic, --fmad=false)"
     del ho, uo
     d0 = s.diagnostics()
     ref = dg.diagnostics(c.mesh, lab, hg, ug, c.dt, c.M, c.g)
@@ -389,6 +391,29 @@ def test_rk4_with_forcing_matches_oracle(Solver):
     assert np.array_equal(hg, h) and np.array_equal(ug, u)
 
 
+@pytest.mark.parametrize("which", ["config1", "shelf"])
+def test_rk32_scheme_matches_oracle(Solver, which):
+    """RK(3,2) of Wicker & Skamarock (FBLTS_SCHEME_RK32), the scheme FB-RK(3,2) extends,
+    on the unsplit system through the C ABI equals the oracle's rk32_step bit for bit (config 1:
+    slow terms, 50 steps; reduced shelf: wind-stress forcing, 30 steps)."""
+    if which == "config1":
+        c, dt, n = configs.config1(), 30.0, 50
+    else:
+        c, dt, n = configs.small_shelf(nx=48, ny=40, dt=25.0), 5.0, 30
+    phys = phys_of(c)
+    h, u = c.h0.copy(), c.u0.copy()
+    for _ in range(n):
+        h, u = fbrk32.rk32_step(c.mesh, h, u, dt, phys)
+    s = Solver(c.mesh, np.zeros(c.mesh.nCells, dtype=bool), dt, 1, g=c.g, beta=c.beta, rho0=c.rho0, slow=c.slow,
+               tau_n=c.tau_n, scheme="rk32")
+    s.set_state(c.h0, c.u0)
+    s.step(n)
+    hg, ug, _ = s.state()
+    s.close()
+    assert_parity(hg, ug, h, u)
+    assert np.array_equal(hg, h) and np.array_equal(ug, u)
+
+
 @pytest.mark.parametrize("which,M", [("config1", 4), ("shelf", 2), ("shelf", 3)])
 def test_slow_refresh_matches_oracle(Solver, which, M):
     """The slow-term refresh variant: S^k re-evaluated at every fine
@@ -404,6 +429,7 @@ def test_slow_refresh_matches_oracle(Solver, which, M):
     s.close()
     eh, eu = assert_parity(hg, ug, ho, uo)
     print(f"refresh {which} M={M}: eps_h={eh:.3e} eps_u={eu:.3e} bitwise={np.array_equal(hg, ho) and np.array_equal(ug, uo)}")
+    assert np.array_equal(hg, ho) and np.array_equal(ug, uo), "not bitwise (canonical arithmetic, --fmad=false)"
 
 
 @pytest.mark.parametrize("scheme", ["fblts", "rk4"])
@@ -432,6 +458,7 @@ def test_hurricane_terms_match_oracle(Solver, scheme):
     s.close()
     eh, eu = assert_parity(hg, ug, ho, uo)
     print(f"hurricane {scheme}: eps_h={eh:.3e} eps_u={eu:.3e} bitwise={np.array_equal(hg, ho) and np.array_equal(ug, uo)}")
+    assert np.array_equal(hg, ho) and np.array_equal(ug, uo), "not bitwise (canonical arithmetic, --fmad=false)"
 
 
 @pytest.mark.parametrize("which,M", [("config1", 4), ("shelf", 2), ("shelf", 3), ("shelf", 1)])
@@ -451,6 +478,7 @@ def test_unsplit_matches_oracle(Solver, which, M):
     s.close()
     eh, eu = assert_parity(hg, ug, ho, uo)
     print(f"unsplit {which} M={M}: eps_h={eh:.3e} eps_u={eu:.3e} bitwise={np.array_equal(hg, ho) and np.array_equal(ug, uo)}")
+    assert np.array_equal(hg, ho) and np.array_equal(ug, uo), "not bitwise (canonical arithmetic, --fmad=false)"
 
 
 @pytest.mark.parametrize("M", [1, 2, 4])

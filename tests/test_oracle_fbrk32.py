@@ -59,6 +59,60 @@ def test_stability_limit_and_weights():
     assert 7.0 < err[0] / err[1] < 9.0
 
 
+def test_rk32_scalar_oscillator_closed_form():
+    """True RK(3,2) (Wicker-Skamarock) on u' = -h, h' = u: with A = [[0, -1], [1, 0]]
+    (A^2 = -I, A^3 = -A) the step is R(zA) = (1 - z^2/2) I + (z - z^3/6) A, written out here by hand;
+    so (0, 1) at z = 0.1 -> (-(0.1 - 0.001/6), 0.995), exact in rationals."""
+    z = Fraction(1, 10)
+    u1, h1 = fbrk32.rk32_generic(lambda u, h: -h, lambda u, h: u, Fraction(0), Fraction(1), z)
+    assert u1 == -(z - z ** 3 / 6) and h1 == 1 - z ** 2 / 2
+    assert float(u1) == pytest.approx(-0.09983333333333333, abs=1e-17) and float(h1) == 0.995
+    for zf in (0.05, 0.7, 1.7):
+        for col, (u0, h0) in enumerate([(1.0, 0.0), (0.0, 1.0)]):
+            u1, h1 = fbrk32.rk32_generic(lambda u, h: -h, lambda u, h: u, u0, h0, zf)
+            a, b = 1 - zf ** 2 / 2, zf - zf ** 3 / 6
+            G = np.array([[a, -b], [b, a]])
+            np.testing.assert_allclose([u1, h1], G[:, col], rtol=0, atol=8 * np.spacing(1.0))
+
+
+def test_rk32_imaginary_axis_limit_is_sqrt3():
+    """|R(iz)|^2 = (1 - z^2/2)^2 + (z - z^3/6)^2 = 1 - z^4/12 + z^6/36 <= 1 iff z <= sqrt(3): the
+    amplification of one oracle step on the oscillator (its growth factor per step, measured by
+    stepping) is <= 1 just below sqrt(3) and > 1 just above -- the CFL gap FB-RK(3,2) closes
+    (3.8621532 / sqrt(3) = 2.23, P:L299-300 'between factors of 1.6 and 2.2')."""
+    def growth(z):
+        u, h = 0.0, 1.0
+        for _ in range(2000):
+            u, h = fbrk32.rk32_generic(lambda u, h: -h, lambda u, h: u, u, h, z)
+        return np.hypot(u, h) ** (1 / 2000)
+    s3 = np.sqrt(3.0)
+    assert growth(s3 * (1 - 1e-3)) <= 1.0
+    assert growth(s3 * (1 + 1e-3)) > 1.0
+    # on LINEAR problems R(z) matches exp(z) through z^3 (Wicker-Skamarock: third order for linear,
+    # second for nonlinear), so the local error vs the exact rotation is O(z^4): ratio 16 per halving
+    err = []
+    for z in (0.02, 0.01):
+        u1, h1 = fbrk32.rk32_generic(lambda u, h: -h, lambda u, h: u, 0.0, 1.0, z)
+        err.append(np.hypot(u1 + np.sin(z), h1 - np.cos(z)))
+    assert 15.0 < err[0] / err[1] < 17.0
+    # scalar decay y' = -y: R(-z) = 1 - z + z^2/2 - z^3/6 (z = 0.1 -> 0.9048333...)
+    y = fbrk32.rk32_generic(lambda u, h: -u, lambda u, h: 0.0 * h, 1.0, 0.0, 0.1)[0]
+    assert y == pytest.approx(1 - 0.1 + 0.005 - 0.001 / 6, abs=1e-16)
+
+
+def test_rk32_conserves_mass_on_mesh():
+    """RK(3,2) on the TRiSK mesh (unsplit, global): mass sum A_i h_i is conserved to roundoff
+    (Theorem 1's argument holds for any explicit RK combination of Psi)."""
+    c = small_shelf(nx=24, ny=20)
+    phys = fbrk32.Phys(tau_n=c.tau_n)
+    h, u = c.h0.copy(), c.u0.copy()
+    m0 = float(np.sum(c.mesh.areaCell * h))
+    for _ in range(10):
+        h, u = fbrk32.rk32_step(c.mesh, h, u, 4.0, phys)
+    assert abs(float(np.sum(c.mesh.areaCell * h)) - m0) <= 1e-13 * m0
+    assert np.all(np.isfinite(u)) and np.max(np.abs(u)) > 0
+
+
 def test_rk4_scalar():
     """Classical RK4 on h' = -h, dt = 0.1 -> 0.9048375."""
     r = GOLD["rk4_exp"]

@@ -185,3 +185,54 @@ def test_courant_and_rms_examples():
     assert dg.rms_error(r["s"], r["m"]) == pytest.approx(r["rms"], rel=1e-8)
     with pytest.raises(ValueError):
         dg.rms_error([1.0], [1.0, 2.0])
+
+
+def test_vertex_thickness_linear_field_on_hex():
+    """h_v on the regular hex: the three kites of a vertex are equal (A_v/3, P19), so
+    h_v is the mean of the three cell values, which for a LINEAR h is h at the triangle's centroid --
+    the vertex itself.  Checked with h = b + a.x on every vertex whose three cells are not wrapped by
+    the periodicity; then q_v = f / h(x_v) at rest."""
+    m = build_periodic_hex_mesh(12, 10, 10e3)
+    a, b = np.array([3.0e-3, -2.0e-3]), 1000.0
+    H = b + a[0] * m.xCell + a[1] * m.yCell
+    hv = trisk.vertex_thickness(m, H)
+    cx = m.xCell[m.cellsOnVertex]
+    cy = m.yCell[m.cellsOnVertex]
+    ok = (np.max(np.abs(cx - m.xVertex[:, None]), axis=1) < 2e4) & (np.max(np.abs(cy - m.yVertex[:, None]), axis=1) < 2e4)
+    assert ok.sum() > 0.5 * m.nVertices
+    exact = b + a[0] * m.xVertex + a[1] * m.yVertex
+    np.testing.assert_allclose(hv[ok], exact[ok], rtol=1e-13)
+    f = np.full(m.nVertices, 1e-4)
+    m.fVertex = f
+    q = trisk.potential_vorticity(m, np.zeros(m.nEdges), H)
+    np.testing.assert_allclose(q[ok], f[ok] / exact[ok], rtol=1e-13)
+
+
+def _mesh_with_unequal_kites():
+    from inputs.icosmesh import build_icosahedral_mesh
+    return build_icosahedral_mesh(3)
+
+
+def test_vertex_thickness_integral_identity_nonuniform_kites():
+    """sum_v A_v h_v = sum_v sum_j kite_{v,j} h_{c_j} = sum_i h_i (sum of the kites of cell i) = sum_i A_i h_i
+    for ANY h, because the kites of a cell tile it (P:L1150-1151 with P19's sum of kites).  On a mesh
+    whose kites differ (icosahedral level 3: pentagons, distorted triangles) this pins the kite <-> cell
+    pairing of the oracle's h_v: pairing a kite with a neighbouring cell breaks it by O(1e-3).  Then
+    q_v at rest: sum_v A_v h_v q_v = sum_v A_v f_v exactly in real arithmetic."""
+    m = _mesh_with_unequal_kites()
+    rng = np.random.default_rng(3)
+    kites = m.kiteAreasOnVertex
+    assert np.ptp(kites) > 1e-3 * np.mean(kites)                  # the kites really differ
+    H = 4000.0 + 500.0 * rng.standard_normal(m.nCells)
+    hv = trisk.vertex_thickness(m, H)
+    lhs = float(np.sum(m.areaTriangle * hv))
+    rhs = float(np.sum(m.areaCell * H))
+    assert abs(lhs - rhs) <= 1e-13 * abs(rhs)
+    # the same sum with the kites rotated one slot against cellsOnVertex fails
+    bad = np.sum(np.roll(kites, 1, axis=1) * H[m.cellsOnVertex], axis=1)
+    assert abs(float(np.sum(bad)) - rhs) > 1e-9 * abs(rhs)
+    m.fVertex = 1e-4 * m.zVertex / m.radius
+    q = trisk.potential_vorticity(m, np.zeros(m.nEdges), H)
+    fsum = float(np.sum(m.areaTriangle * m.fVertex))
+    scale = float(np.sum(m.areaTriangle * np.abs(m.fVertex)))
+    assert abs(float(np.sum(m.areaTriangle * hv * q)) - fsum) <= 1e-13 * scale
