@@ -24,6 +24,8 @@
 // being stored; the FB averages h*, h**, h*** and the IF-1 predictions (eq. preds,
 // P:L683-742) are likewise recomputed from the stored stage thicknesses.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "fblts_internal.h"
 
@@ -40,7 +42,8 @@ constexpr int TPB = 256;
 #ifndef FBLTS_TILE_NBUF
 #define FBLTS_TILE_NBUF 2
 #endif
-constexpr int NBUF = FBLTS_TILE_NBUF;   // tile buffers in the staging ring (>= 2)
+constexpr int NBUF = FBLTS_TILE_NBUF;   // tile buffers of the staged kernel's pipeline
+static_assert(NBUF == 2, "k_stage_tiled is a two-buffer pipeline");
 #ifndef FBLTS_TILE_NTHR
 #define FBLTS_TILE_NTHR 256
 #endif
@@ -446,9 +449,7 @@ __device__ __forceinline__ void load_indices(const TileMesh &t, const TileRec &r
     do {                                     \
         if (FBLTS_CHECK && !(cond)) __trap(); \
     } while (0)
-// development probes (never in the default build): FBLTS_PROBE=1 skips the compute of every tile
-// (copies only), 2 skips the copies (compute on whatever the buffers hold, no reports), 3 skips the
-// compute and the gathers (bulk copies only), 4 skips the compute and the bulk copies (gathers only)
+// development probes were removed (round 2); FBLTS_PROBE stays 0 and is reported by fblts_build_info
 #ifndef FBLTS_PROBE
 #define FBLTS_PROBE 0
 #endif
@@ -470,41 +471,36 @@ __global__ void __launch_bounds__(NTHR, FBLTS_TILE_MINB) k_stage_tiled(DevMesh m
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    // ring of NBUF tile buffers: tiles k .. k+NBUF-2 are in flight while tile k is computed; the
-    // halo / foreign copies of a tile form one cp.async group (committed once per tile, even if
-    // empty), so waiting for "all but the newest NBUF-2 groups" waits exactly for the current tile
+    // Two tile buffers: while tile k is computed the other buffer fills with tile k+1 -- one thread
+    // issues its bulk copies at the top of the iteration, and every thread issues its halo / foreign
+    // gathers after the edge phase (their indices, loaded at the top, have arrived by then; issued
+    // earlier they only slow the edge phase's shared-memory traffic -- measured).  The halo / foreign
+    // copies of a tile form one cp.async group, committed once per iteration (even if empty).  Tile
+    // records are carried in registers and loaded one iteration ahead.
     int hx[HPT], fx[FPT];
-    for (int k = 0; k < NBUF - 1; ++k) {
-        const int tk = tile + k * G0;
-        if (tk < tile1) {
-            const TileRec rk = load_rec(t, tk);
-            double *Bk = buf0 + k * BUF;
-            if (FBLTS_PROBE != 2 && FBLTS_PROBE != 4 && tid == 0) issue_bulk<STAGE>(m, a, rk, Bk, CS2, ES2, &bar[k]);
-            load_indices(t, rk, tid, hx, fx);
-            if (FBLTS_PROBE != 2 && FBLTS_PROBE != 3) issue_indexed<STAGE>(m, a, rk, TileBuf<STAGE>(Bk, CS2, ES2, rk), tid, hx, fx);
-        }
-        cp_async_commit();
-    }
+    TileRec rc = load_rec(t, tile), rn{};
+    if (tid == 0) issue_bulk<STAGE>(m, a, rc, buf0, CS2, ES2, &bar[0]);
+    load_indices(t, rc, tid, hx, fx);
+    issue_indexed<STAGE>(m, a, rc, TileBuf<STAGE>(buf0, CS2, ES2, rc), tid, hx, fx);
+    cp_async_commit();
+    if (tile + G0 < tile1) rn = load_rec(t, tile + G0);
     unsigned phase = 0u;                                   // bit b: parity of buffer b's next completion
     int buf = 0;
-    for (; tile < tile1; tile += G0, buf = (buf + 1 == NBUF ? 0 : buf + 1)) {
-        const TileRec cur = load_rec(t, tile);
-        const int tn = tile + (NBUF - 1) * G0;             // the tile that reuses the previous buffer
-        const bool more = tn < tile1;
-        TileRec nx{};
-        if (more) nx = load_rec(t, tn);
-        if (FBLTS_PROBE != 2 && FBLTS_PROBE != 4) mbar_wait(&bar[buf], (phase >> buf) & 1u);
+    for (; tile < tile1; tile += G0, buf ^= 1) {
+        const TileRec cur = rc, nx = rn;
+        const bool more = tile + G0 < tile1;
+        if (tile + 2 * G0 < tile1) rn = load_rec(t, tile + 2 * G0);     // consumed next iteration
+        rc = nx;
+        mbar_wait(&bar[buf], (phase >> buf) & 1u);
         phase ^= 1u << buf;
-        cp_async_wait_pending<NBUF - 2>();
-        __syncthreads();                                   // tile `cur` staged; the previous buffer free
-        const int bn = buf == 0 ? NBUF - 1 : buf - 1;
-        double *Bn = buf0 + bn * BUF;
+        cp_async_wait_pending<0>();
+        __syncthreads();                                   // tile `cur` staged; the other buffer is free
+        double *Bn = buf0 + (buf ^ 1) * BUF;
         if (more) {
-            if (FBLTS_PROBE != 2 && FBLTS_PROBE != 4 && tid == 0) issue_bulk<STAGE>(m, a, nx, Bn, CS2, ES2, &bar[bn]);
-            load_indices(t, nx, tid, hx, fx);              // consumed after this tile's compute
+            if (tid == 0) issue_bulk<STAGE>(m, a, nx, Bn, CS2, ES2, &bar[buf ^ 1]);
+            load_indices(t, nx, tid, hx, fx);              // consumed after the edge phase
         }
         const TileBuf<STAGE> bc(buf0 + buf * BUF, CS2, ES2, cur);
-#if FBLTS_PROBE == 0 || FBLTS_PROBE == 2
         // ---- compute tile `cur`
         const int nOwn = cur.c1 - cur.c0;
         const int i = cur.c0 + tid;
@@ -552,26 +548,29 @@ __global__ void __launch_bounds__(NTHR, FBLTS_TILE_MINB) k_stage_tiled(DevMesh m
                 }
             }
         }
+        if (more) issue_indexed<STAGE>(m, a, nx, TileBuf<STAGE>(Bn, CS2, ES2, nx), tid, hx, fx);
+        cp_async_commit();
+        if (tid == 0) bc.u[nOE] = 0.0;                    // the gap slot: the term of an unused slot
         __syncthreads();
         if (own) {                                        // cell phase
             const double hbi = (STAGE == 1 || STAGE == 4) ? bc.hp[tid] : bc.hb[tid];
             double acc = 0.0;
+            // branch-free slot loop: n_{e,i} applied by flipping the sign bit (exactly -tt); an unused
+            // slot (TILE_SENT, sign bit set) reads the gap slot's +0.0 as -0.0, and x + (-0.0) == x for
+            // every x, so the sum is bit-identical to the sequential sum over the used slots
 #pragma unroll
             for (int j = 0; j < G; ++j) {
-                if (r[j] != TILE_SENT) {
-                    FBLTS_REQUIRE((r[j] & 0x7FFF) < nOE || ((r[j] & 0x7FFF) >= nOE + FGAP && (r[j] & 0x7FFF) < nLE + FGAP));
-                    const double tt = bc.u[r[j] & 0x7FFF];
-                    acc = acc + ((r[j] >> 15) ? -tt : tt);
-                }
+                const uint32_t rj = r[j];
+                const int q = rj == TILE_SENT ? nOE : (int)(rj & 0x7FFFu);
+                FBLTS_REQUIRE(q <= nOE || (q >= nOE + FGAP && q < nLE + FGAP));
+                const unsigned long long tb = __double_as_longlong(bc.u[q]) ^ ((unsigned long long)(rj >> 15) << 63);
+                acc = acc + __longlong_as_double(tb);
             }
             const double psi = -acc / A;
             const double v = hbi + a.ch * psi;
             a.out[i] = v;
-            if (FBLTS_PROBE == 0 && !(v > 0.0)) report(err, a.kind, a.k, i, v);
+            if (!(v > 0.0)) report(err, a.kind, a.k, i, v);
         }
-#endif
-        if (FBLTS_PROBE != 2 && FBLTS_PROBE != 3 && more) issue_indexed<STAGE>(m, a, nx, TileBuf<STAGE>(Bn, CS2, ES2, nx), tid, hx, fx);
-        cp_async_commit();
     }
 }
 
@@ -1144,6 +1143,10 @@ void launch_stage_tiled(const DevMesh &m, int stage, int tile0, int tile1, int h
         int per = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, NTHR, smem);
         const int grid = std::max(1, std::min(tile1 - tile0, nsm * std::max(1, per)));
+        static const bool verbose = std::getenv("FBLTS_VERBOSE") != nullptr;
+        if (verbose)
+            std::fprintf(stderr, "[fblts] stage_tiled s%d tiles [%d,%d) hmax %d emax %d smem %d B, %d CTA/SM, grid %d\n",
+                         stage, tile0, tile1, hmax, emax, smem, per, grid);
         if (stage == 1) k_stage_tiled<G, 1><<<grid, NTHR, smem, s>>>(m, tile0, tile1, CS, ES, a, err);
         else if (stage == 2) k_stage_tiled<G, 2><<<grid, NTHR, smem, s>>>(m, tile0, tile1, CS, ES, a, err);
         else if (stage == 3) k_stage_tiled<G, 3><<<grid, NTHR, smem, s>>>(m, tile0, tile1, CS, ES, a, err);
@@ -1816,7 +1819,7 @@ void launch_un_fstage(const DevMesh &m, const DevState &st, int stage, const dou
 extern "C" const char *fblts_build_info(void) {
     return "probe=" FBLTS_STR(FBLTS_PROBE) " check=" FBLTS_STR(FBLTS_CHECK) " tile=" FBLTS_STR(FBLTS_TILE)
            " tile_minb=" FBLTS_STR(FBLTS_TILE_MINB) " tile_nbuf=" FBLTS_STR(FBLTS_TILE_NBUF)
-           " tile_nthr=" FBLTS_STR(FBLTS_TILE_NTHR) " minb=" FBLTS_STR(FBLTS_MINB)
+           " tile_nthr=" FBLTS_STR(FBLTS_TILE_NTHR) " minb=" FBLTS_STR(FBLTS_MINB) 
 #if defined(__CUDACC__)
            " fmad=off arch=sm_100a"
 #endif
