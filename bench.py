@@ -133,18 +133,35 @@ def _finite(x):
     return x
 
 
-def rk4_dt(c, name):
-    """0.9 x the RK4 Courant limit nu_loc bisected with the oracle on this config (or its proxy),
-    applied to this mesh's max_e sqrt(g max H) / d_e; (None, why) if no scan is recorded."""
+def scheme_dt(c, name, scheme):
+    """0.9 x the Courant limit nu_loc of `scheme` ("global" FB-RK(3,2), "rk32", "rk4") bisected with the
+    oracle on this config or its proxy (configs/dt.json "<config>_<scheme>", scripts/cfl_scan.py), applied
+    to this mesh's max_e sqrt(g max H) / d_e; (None, why) if no scan is recorded."""
     try:
         with open(os.path.join(ROOT, "configs", "dt.json")) as f:
-            nu = float(json.load(f)[f"{name}_rk4"]["nu_loc_limit"])
+            ent = json.load(f)[f"{name}_{scheme}"]
+        nu = float(ent["nu_loc_limit"])
     except (OSError, KeyError, ValueError):
-        return None, f"no {name}_rk4 entry in configs/dt.json"
+        return None, f"no {name}_{scheme} entry in configs/dt.json"
     H = c.mesh.bottomDepth
     c0, c1 = c.mesh.cellsOnEdge[:, 0], c.mesh.cellsOnEdge[:, 1]
     cmax = float(np.max(np.sqrt(c.g * np.maximum(H[c0], H[c1])) / c.mesh.dcEdge))
-    return 0.9 * nu / cmax, f"0.9 x nu_loc {nu:.4f} (configs/dt.json {name}_rk4)"
+    bound = " (lower bound: no unstable step found)" if ent.get("bound_only") or ent.get("unstable_dt") is None \
+        or ent.get("unstable_dt") == ent.get("stable_dt") else ""
+    return 0.9 * nu / cmax, f"0.9 x nu_loc {nu:.4f} (configs/dt.json {name}_{scheme}){bound}"
+
+
+def host_cpu():
+    model = "?"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"model": model, "logical_cpus": os.cpu_count()}
 
 
 def load_peaks():
@@ -224,21 +241,21 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
-def run_cpu_baseline(steps=3, warmup=1):
+def run_cpu_baseline(c, workload, steps=1, slow_refresh=False, split=True):
+    """The oracle as it stands (oracle/lts.py, numpy fp64, single-threaded) on the SAME workload at full
+    size: `steps` coarse steps after labelling (labelling excluded, as the GPU's setup is)."""
     from oracle import fbrk32, lts
-    c, sample = cpu_sample_case()
     lab = lts.label_regions(c.mesh, c.fine_mask)
     phys = fbrk32.Phys(g=c.g, beta=c.beta, slow=c.slow, tau_n=c.tau_n, rho0=c.rho0)
     h, u = c.h0, c.u0
-    for _ in range(warmup):
-        h, u = lts.fblts_step(c.mesh, lab, h, u, c.dt, c.M, phys)
     t0 = time.perf_counter()
     for _ in range(steps):
-        h, u = lts.fblts_step(c.mesh, lab, h, u, c.dt, c.M, phys)
+        h, u = lts.fblts_step(c.mesh, lab, h, u, c.dt, c.M, phys, slow_refresh=slow_refresh, split=split)
     t = time.perf_counter() - t0
     return {"value": c.mesh.nCells * c.M * steps / t, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{sample}; {steps} coarse steps after {warmup} warm-up, numpy single-threaded",
-            "seconds": t}
+            "sample": f"{workload} at full size ({c.mesh.nCells} cells, M = {c.M}): {steps} coarse step(s) of the "
+                      "oracle (oracle/lts.py fblts_step), numpy single-threaded, labelling excluded",
+            "seconds": t, "host_cpu": host_cpu()}
 
 
 def arm_reference(args):
@@ -380,57 +397,50 @@ def arm_native(args):
                       "back every step) + diagnostics() (mass, Gamma, min h, max nu) + get_state(pinned host)"}
         assert all(np.all(np.isfinite(r)) for r in records)
 
-    # ---------------- the same workload as global FB-RK(3,2) at the fine step (no LTS), same GPU:
-    # the paper's speedup framing (FB-LTS vs a global scheme at the step the fine region needs,
-    # P:L1367-1403) measured on the device; FB-LTS advances dt per coarse step, the global scheme
-    # dt / M per step, so the speedup at equal simulated time is M * T_global / T_lts.
-    lts_vs_global = None
-    if world == 1 and not args.no_global and c.M > 1:
+    # ---------------- the paper's speedup framing (Tables 1 and 3) on one GPU:
+    # the same mesh and state advanced by each reference scheme at ITS OWN stable step (0.9 x the Courant
+    # limit bisected with the oracle, configs/dt.json "<config>_<scheme>") -- global FB-RK(3,2) (no LTS),
+    # RK(3,2) (Wicker-Skamarock, unsplit) and classical RK4 (unsplit) -- and FB-LTS at its own coarse step;
+    # speedup at equal simulated time = (ms per step / dt)_scheme / (ms per step / dt)_FB-LTS.
+    schemes = None
+    if world == 1 and not args.no_global and not args.unsplit and not args.slow_refresh:
         s.close()
         del s
         torch.cuda.empty_cache()
-        sg = Solver(c.mesh, np.zeros(c.mesh.nCells, dtype=bool), c.dt / c.M, 1, g=c.g, beta=c.beta, rho0=c.rho0,
-                    slow=c.slow, tau_n=c.tau_n)
-        sg.set_state(c.h0, c.u0, 0.0)
-        sg.step(3)
-        torch.cuda.synchronize()
-        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        g0.record(stream)
-        sg.step(args.steps)
-        g1.record(stream)
-        torch.cuda.synchronize()
-        sg.sync()
-        tg = g0.elapsed_time(g1) / args.steps
-        lts_vs_global = {"global_fbrk32_ms_per_step": tg, "global_dt": c.dt / c.M,
-                         "global_cell_updates_per_s": c.mesh.nCells / (tg * 1e-3),
-                         "lts_speedup_at_equal_simulated_time": c.M * tg / ms_step,
-                         "how": "same mesh and state, no fine cells, dt/M, K steps, CUDA events"}
-        sg.close()
-        del sg
-        torch.cuda.empty_cache()
-        # the paper's reference scheme: classical RK4 on the unsplit system at ITS stable step
-        # (0.9 x the oracle-bisected Courant limit, configs/dt.json "<config>_rk4")
-        dt4, src4 = rk4_dt(c, args.config)
-        if dt4 is not None:
-            sr = Solver(c.mesh, np.zeros(c.mesh.nCells, dtype=bool), dt4, 1, g=c.g, beta=c.beta, rho0=c.rho0,
-                        slow=c.slow, tau_n=c.tau_n, scheme="rk4")
-            sr.set_state(c.h0, c.u0, 0.0)
-            sr.step(3)
+        lts_cost = ms_step / c.dt                      # device ms per simulated second
+        schemes = {"fblts": {"dt": c.dt, "M": c.M, "ms_per_step": ms_step, "ms_per_sim_s": lts_cost,
+                             "dt_source": "0.9 x nu_loc (configs/dt.json %s)" % args.config}}
+        base = args.config
+        for name, kw in (("global", {"scheme": "fblts"}), ("rk32", {"scheme": "rk32"}), ("rk4", {"scheme": "rk4"})):
+            dtx, src = scheme_dt(c, base, name)
+            if dtx is None:
+                schemes[name] = {"skipped": src}
+                continue
+            sx = Solver(c.mesh, np.zeros(c.mesh.nCells, dtype=bool), dtx, 1, g=c.g, beta=c.beta, rho0=c.rho0,
+                        slow=c.slow, tau_n=c.tau_n, **kw)
+            sx.set_state(c.h0, c.u0, 0.0)
+            sx.step(3)
             torch.cuda.synchronize()
-            r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            r0.record(stream)
-            sr.step(args.steps)
-            r1.record(stream)
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            sx.step(args.steps)
+            g1.record(stream)
             torch.cuda.synchronize()
-            sr.sync()
-            tr = r0.elapsed_time(r1) / args.steps
-            sr.close()
-            lts_vs_global.update({"rk4_ms_per_step": tr, "rk4_dt": dt4, "rk4_dt_source": src4,
-                                  "lts_speedup_vs_rk4_at_equal_simulated_time": (c.dt / ms_step) / (dt4 / tr)})
+            sx.sync()
+            tx = g0.elapsed_time(g1) / args.steps
+            sx.close()
+            del sx
+            torch.cuda.empty_cache()
+            schemes[name] = {"dt": dtx, "dt_source": src, "ms_per_step": tx, "ms_per_sim_s": tx / dtx,
+                             "cell_updates_per_s": c.mesh.nCells / (tx * 1e-3),
+                             "fblts_speedup_at_equal_simulated_time": (tx / dtx) / lts_cost}
+        schemes["how"] = ("same mesh and initial state, K steps each, CUDA events on the launching stream; global = "
+                          "FB-RK(3,2) with no fine cells (M = 1), rk32 / rk4 on the unsplit system; each at 0.9 x its "
+                          "own oracle-bisected Courant limit (scripts/cfl_scan.py)")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = run_cpu_baseline()
+        cpu = run_cpu_baseline(c, args.config, slow_refresh=args.slow_refresh, split=not args.unsplit)
     if rank != 0:
         return
     line = {
@@ -458,7 +468,7 @@ def arm_native(args):
                         "GBps": bm[k] / (tms / n_prof * 1e-3) / 1e9}
                     for k, (tms, n) in prof.items() if n},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(round(launches_per_step * args.steps)),
-        "lts_vs_global": lts_vs_global,
+        "schemes": schemes,
         "clocks": clocks,
     }
     print(json.dumps(_finite(line)), flush=True)

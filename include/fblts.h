@@ -129,6 +129,12 @@ typedef struct {
                             of reading Q2): q_hat_e F_perp_e is replaced by
                             sum_j W_{e,j} F_{e_j} (q_hat_e + q_hat_{e_j}) / 2, which does no work
                             (sum_e l_e d_e F_e PV_e = 0); one rank, no slow refresh.  0: centred q_hat */
+    int32_t vorticity;   /* 1: advance the prognostic absolute vorticity companion eta_v with every step
+                            (Theorem 2; SPEC step_prognostic_vorticity S:L472-480): the PV-flux
+                            term q_hat_e F_perp_e of every velocity update, integrated per edge as the velocity
+                            integrates it (int_E: dt PV of coarse stage 3; F_E: sum_k dt/M PV^k; IF edges:
+                            dt/M sum_k PV^k), gives eta_v += (sum_j t_{e_j,v} d_{e_j} dP_{e_j}) / A_v.  Needs
+                            unsplit = 1 and one rank; set / read with fblts_set_vorticity / fblts_get_vorticity */
 } fblts_config;
 
 #define FBLTS_SCHEME_FBLTS 0
@@ -200,6 +206,13 @@ int fblts_set_hurricane(fblts_ctx *ctx, const double *uw_n, const double *uw_t, 
  * set_state), ORDER, CUDA. */
 int fblts_set_state(fblts_ctx *ctx, const double *h, const double *u, double t);
 
+/* Prognostic absolute vorticity (cfg.vorticity = 1): eta [nVertices] in ORIGINAL vertex order, HOST
+ * arrays, copied (synchronous).  set after fblts_set_state (e.g. the diagnostic curl u + f of the initial
+ * state); get synchronises and reports device errors like fblts_get_state.  Errors: INVALID_ARG, ORDER
+ * (no cfg.vorticity, or no state), STATE (non-finite eta), CUDA. */
+int fblts_set_vorticity(fblts_ctx *ctx, const double *eta);
+int fblts_get_vorticity(fblts_ctx *ctx, double *eta);
+
 /* Enqueue n_coarse coarse steps on cfg.stream (asynchronous, CUDA-graph replay). */
 int fblts_step(fblts_ctx *ctx, int32_t n_coarse);
 
@@ -227,6 +240,12 @@ int fblts_diagnostics(fblts_ctx *ctx, double out[4]);
  * (one pass over h and areaCell).  Synchronises;
  * several ranks: NCCL all-gather, combined in rank order.  Errors: ORDER, CUDA, NCCL, POSITIVITY. */
 int fblts_diagnostics_mass(fblts_ctx *ctx, double out[2]);
+
+/* *out = the volume integral of potential vorticity sum_v A_v h_v q_v (Remark rmk:volume_conservation_pv,
+ * eq. vol_integral_pv), h_v = (sum_j kite_{v,j} h_{c_j}) / A_v, q_v = (zeta_v + f_v) / h_v:
+ * equal to Gamma up to rounding, hence conserved wherever Theorem 2 holds.  Deterministic double-double
+ * reduction (synchronises; several ranks: NCCL all-gather combined in rank order).  Errors: ORDER, CUDA. */
+int fblts_diagnostics_pv(fblts_ctx *ctx, double *out);
 
 /* The same four numbers as fblts_diagnostics (Thms 1-2, eq. cfl) for the state after the steps
  * enqueued so far, WITHOUT synchronising

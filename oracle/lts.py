@@ -142,7 +142,7 @@ def predict_stage(co, x_new, x_stage, x_n):
     return co["a"] * x_new + co["b"] * x_stage + co["c"] * x_n
 
 
-def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper", slow_refresh=False, split=True):
+def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper", slow_refresh=False, split=True, eta=None):
     """One FB-LTS coarse step in split mode, literal (P:L551-787 inside P:L1548-1561).
 
     slow_refresh=True: the variant the paper proposes to lift the splitting's coarse-step cap
@@ -160,6 +160,15 @@ def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper", slow_refresh=False
     Y1 = C_E u F^4_E, Y2 = C_E u F^2_E, Y3 = IF-1_E u int_E (whose slow stencils stay inside
     X1 = C u F^5, X2 = C u F^3, X3 = C u F^1); fine: U0, U1, U2 of the view table (P:L784-785);
     correction summand Phi(U2, HS3) on the IF edges.
+
+    eta (vertex array, optional): the prognostic absolute vorticity companion (Theorem 2, P:L1038-1137;
+    SPEC step_prognostic_vorticity S:L472-480) advanced with the step: every velocity update's PV-flux
+    term PV_e = q_hat_e F_perp_e (trisk.pv_flux; inside S in split mode, at each stage's (U, HS) in
+    unsplit mode) is integrated per edge exactly as the velocity integrates it -- int_E: dt PV(coarse
+    stage 3); F_E: sum_k dt/M PV^k (fine velocity stage 3 of every subcycle, ascending k); IF-1_E and
+    IF-2_E: dt/M sum_k PV^k (the correction's sum, reading Q14) -- and eta_v += (sum_j t d dP) / A_v
+    (trisk.vorticity_update).  One dP per edge, shared by its two dual cells with opposite t_{e,v}: the
+    total sum_v A_v eta_v is conserved (Theorem 2).  Then returns (h^{n+1}, u^{n+1}, eta^{n+1}).
 
     extents="paper": the shrinking F^5/F^4/F^3/F^2/F^1 extents of P:L557-661.
     extents="all_fine": the MPAS simplification of P:L1284-1286 (every coarse
@@ -198,6 +207,16 @@ def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper", slow_refresh=False
 
     # ---------- slow terms at t^n, frozen for the whole coarse step ----------
     S = trisk.slow_tendency(mesh, u, h, phys) if split else None
+    track = eta is not None
+
+    def PVf(U, HS, mask):
+        """PV-flux part of the slow term on the edges of mask (0 with the slow terms off)."""
+        if not phys.slow:
+            return np.zeros(int(np.count_nonzero(mask)))
+        with np.errstate(invalid="ignore"):
+            return trisk.pv_flux(mesh, U, HS, phys)[mask]
+
+    PS = trisk.pv_flux(mesh, u, h, phys) if (track and split and phys.slow) else np.zeros(nE)
 
     def Slow(U, HS, mask):
         """Phi^slow(U, HS) on the edges of mask (unsplit); NaN in the views poisons misuse."""
@@ -228,6 +247,11 @@ def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper", slow_refresh=False
     h_new, u_new = nan_c(), nan_e()
     h_new[INTc] = h3[INTc]                                   # interior coarse data is final
     u_new[INT_E] = u3[INT_E]
+    if track:                                                # eta companion: int_E from coarse stage 3
+        dP = nan_e()
+        dP[INT_E] = c3 * (PS[INT_E] if split else PVf(u2, hs3, INT_E))
+        dPF = np.where(F_E, 0.0, np.nan)
+        accP = np.where(IF1_E | IF2_E, 0.0, np.nan)
 
     # ---------- Phases 2 + 3: Interface Prediction per k and Fine Advancement ----------
     hk, uk = nan_c(), nan_e()
@@ -301,6 +325,14 @@ def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper", slow_refresh=False
         ukn[e] = uk[e] + c3f * (phi + (Sk[e] if split else Slow(U2, HS3, F_E)))
         e, phi = PhiF(HS3, IFe)                                         # correction summand (eq. if_correction)
         accU[e] = accU[e] + (phi + (S[e] if split else Slow(U2, HS3, IFe)))
+        if track:
+            if split:
+                PkF = PVf(Uk, Hk, F_E) if slow_refresh else PS[F_E]
+                PkI = PS[IFe]
+            else:
+                PkF, PkI = PVf(U2, HS3, F_E), PVf(U2, HS3, IFe)
+            dPF[F_E] = dPF[F_E] + c3f * PkF
+            accP[IFe] = accP[IFe] + PkI
         hk, uk = hkn, ukn
 
     h_new[F] = hk[F]                                                    # h^{n+1} := h^{n,M}
@@ -309,10 +341,17 @@ def fblts_step(mesh, lab, h, u, dt, M, phys, extents="paper", slow_refresh=False
     # ---------- Phase 4: Interface Correction (reading Q14) ----------
     h_new[IFc] = h[IFc] + c3f * accH[IFc]
     u_new[IFe] = u[IFe] + c3f * accU[IFe]
+    if track:
+        dP[F_E] = dPF[F_E]
+        dP[IFe] = c3f * accP[IFe]
+        return h_new, u_new, trisk.vorticity_update(mesh, eta, dP)
     return h_new, u_new
 
 
-def run(mesh, lab, h, u, dt, M, phys, n_steps, extents="paper", slow_refresh=False, split=True):
+def run(mesh, lab, h, u, dt, M, phys, n_steps, extents="paper", slow_refresh=False, split=True, eta=None):
     for _ in range(n_steps):
-        h, u = fblts_step(mesh, lab, h, u, dt, M, phys, extents, slow_refresh=slow_refresh, split=split)
-    return h, u
+        out = fblts_step(mesh, lab, h, u, dt, M, phys, extents, slow_refresh=slow_refresh, split=split, eta=eta)
+        h, u = out[0], out[1]
+        if eta is not None:
+            eta = out[2]
+    return (h, u) if eta is None else (h, u, eta)

@@ -180,6 +180,36 @@ def hurricane_terms(mesh, U, h_e, phys):
     return D, W
 
 
+def pv_flux(mesh, U, H, phys=None):
+    """PV_e = q_hat_e F_perp_e on every edge: the absolute-vorticity flux of the momentum equation
+    (eq. trisk_vorticity, the term whose curl is Theta_v), q_hat_e = 0.5 (q[v0] + q[v1])
+    (reading Q2); phys.pv == "energy": the energy-conserving pv_flux_energy."""
+    e = np.arange(mesh.nEdges)
+    F = edge_flux(mesh, U, H, e)
+    q = potential_vorticity(mesh, U, H)
+    v0 = mesh.verticesOnEdge[:, 0]
+    v1 = mesh.verticesOnEdge[:, 1]
+    q_hat = 0.5 * (q[v0] + q[v1])
+    if phys is not None and phys.pv == "energy":
+        return pv_flux_energy(mesh, F, q_hat, e)
+    return q_hat * perp_flux(mesh, F, e)
+
+
+def vorticity_update(mesh, eta, dP):
+    """Prognostic absolute vorticity on the dual cells (eq. trisk_vorticity):
+    eta_v^{n+1} = eta_v^n + (sum_j t_{e_j,v} d_{e_j} dP_{e_j}) / A_v  over edgesOnVertex in slot order,
+    with dP_e the time-integrated PV flux the step applied to edge e (lts.fblts_step(eta=...)) and
+    t_{e,v} = +1 if v = verticesOnEdge[e][1] (the +t_e side) else -1 -- the circulation sign, so that
+    the prognostic eta tracks the diagnostic (curl u + f) (Ringler et al. 2010)."""
+    acc = np.zeros(mesh.nVertices)
+    v = np.arange(mesh.nVertices)
+    for k in range(3):
+        e = mesh.edgesOnVertex[:, k]
+        s = np.where(mesh.verticesOnEdge[e, 1] == v, 1.0, -1.0)
+        acc = acc + s * mesh.dcEdge[e] * dP[e]
+    return eta + acc / mesh.areaTriangle
+
+
 def slow_momentum(mesh, U, H, tau_n, rho0, phys=None):
     """Phi^slow_e(u, h) on every edge: the non-gravity-wave momentum terms.
 
@@ -192,16 +222,7 @@ def slow_momentum(mesh, U, H, tau_n, rho0, phys=None):
     the energy-conserving pv_flux_energy.
     Evaluated as  (PV_e - (K1 - K0) / d_e) + G_e,  PV_e = q_hat * F_perp (centred).
     """
-    e = np.arange(mesh.nEdges)
-    F = edge_flux(mesh, U, H, e)
-    q = potential_vorticity(mesh, U, H)
-    v0 = mesh.verticesOnEdge[:, 0]
-    v1 = mesh.verticesOnEdge[:, 1]
-    q_hat = 0.5 * (q[v0] + q[v1])
-    if phys is not None and phys.pv == "energy":
-        PV = pv_flux_energy(mesh, F, q_hat, e)
-    else:
-        PV = q_hat * perp_flux(mesh, F, e)
+    PV = pv_flux(mesh, U, H, phys)
     K = kinetic_energy(mesh, U)
     c0 = mesh.cellsOnEdge[:, 0]
     c1 = mesh.cellsOnEdge[:, 1]

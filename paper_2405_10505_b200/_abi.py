@@ -45,7 +45,7 @@ class fblts_config(C.Structure):
                 ("M", C.c_int32), ("r", C.c_int32), ("slow", C.c_int32), ("device", C.c_int32),
                 ("stream", C.c_void_p), ("rank", C.c_int32), ("nranks", C.c_int32), ("nccl_id", C.c_void_p),
                 ("scheme", C.c_int32), ("slow_refresh", C.c_int32), ("sal_beta", C.c_double),
-                ("unsplit", C.c_int32), ("pv_energy", C.c_int32)]
+                ("unsplit", C.c_int32), ("pv_energy", C.c_int32), ("vorticity", C.c_int32)]
 
 SCHEMES = {"fblts": 0, "rk4": 1, "rk32": 2}
 
@@ -84,6 +84,9 @@ _lib_profile = _sig("fblts_profile", C.c_int, _vp, C.c_int32, _f64p, C.POINTER(C
 _lib_kname = _sig("fblts_kernel_name", C.c_char_p, C.c_int32)
 _lib_last_error = _sig("fblts_last_error", C.c_char_p, _vp)
 _lib_build_info = _sig("fblts_build_info", C.c_char_p)
+_lib_diag_pv = _sig("fblts_diagnostics_pv", C.c_int, _vp, _f64p)
+_lib_set_vort = _sig("fblts_set_vorticity", C.c_int, _vp, _f64p)
+_lib_get_vort = _sig("fblts_get_vorticity", C.c_int, _vp, _f64p)
 _lib_destroy = _sig("fblts_destroy", None, _vp)
 _i64p = C.POINTER(C.c_int64)
 _lib_halo = _sig("fblts_get_halo", C.c_int, _vp, C.c_int32, C.c_int32, _i64p, _i64p, _i64p, _i64p)
@@ -96,7 +99,7 @@ EXPORTED = ["fblts_create", "fblts_upload_mesh", "fblts_set_regions", "fblts_get
             "fblts_set_forcing", "fblts_set_hurricane", "fblts_set_state", "fblts_step", "fblts_step_group", "fblts_diagnostics_group",
             "fblts_sync", "fblts_get_state", "fblts_diagnostics", "fblts_diagnostics_async", "fblts_diagnostics_mass",
             "fblts_profile",
-            "fblts_kernel_name", "fblts_build_info",
+            "fblts_kernel_name", "fblts_build_info", "fblts_set_vorticity", "fblts_get_vorticity", "fblts_diagnostics_pv",
             "fblts_last_error", "fblts_destroy"]
 
 
@@ -117,14 +120,15 @@ def _arr(a, dtype):
 # ------------------------------------------------------------------ entry points
 def fblts_create(dt, M, g=9.81, beta=(0.531, 0.531, 0.313), rho0=1000.0, r=2, slow=True, device=0,
                  stream=None, rank=0, nranks=1, nccl_id=None, scheme="fblts", slow_refresh=False, sal=0.0, unsplit=False,
-                 pv="centered"):
+                 pv="centered", vorticity=False):
     """nccl_id: 128 bytes from fblts_nccl_unique_id() on rank 0 (None: single rank or loopback group)."""
     idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id is not None else None
     cfg = fblts_config(dt=float(dt), g=float(g), beta=(C.c_double * 3)(*beta), rho0=float(rho0), M=int(M),
                        r=int(r), slow=1 if slow else 0, device=int(device), stream=stream, rank=int(rank),
                        nranks=int(nranks), nccl_id=C.cast(idbuf, C.c_void_p) if idbuf is not None else None,
                        scheme=SCHEMES[scheme], slow_refresh=1 if slow_refresh else 0, sal_beta=float(sal),
-                       unsplit=1 if unsplit else 0, pv_energy={"centered": 0, "energy": 1}[pv])
+                       unsplit=1 if unsplit else 0, pv_energy={"centered": 0, "energy": 1}[pv],
+                       vorticity=1 if vorticity else 0)
     ctx = _vp()
     rc = _lib_create(C.byref(ctx), C.byref(cfg))
     if rc != FBLTS_OK:
@@ -273,6 +277,18 @@ def fblts_set_state(ctx, h, u, t=0.0):
     _check(ctx, _lib_set_state(ctx, ph, pu, float(t)))
 
 
+def fblts_set_vorticity(ctx, eta, nVertices):
+    a = _arr(eta, np.float64)
+    _check_len(a, nVertices, "eta")
+    _check(ctx, _lib_set_vort(ctx, _ptr(a, C.c_double)))
+
+
+def fblts_get_vorticity(ctx, nVertices):
+    out = np.empty(nVertices)
+    _check(ctx, _lib_get_vort(ctx, _ptr(out, C.c_double)))
+    return out
+
+
 def fblts_step(ctx, n_coarse):
     _check(ctx, _lib_step(ctx, int(n_coarse)))
 
@@ -297,6 +313,12 @@ def fblts_diagnostics(ctx):
     out = np.zeros(4)
     _check(ctx, _lib_diag(ctx, _ptr(out, C.c_double)))
     return out
+
+
+def fblts_diagnostics_pv(ctx):
+    out = np.zeros(1)
+    _check(ctx, _lib_diag_pv(ctx, _ptr(out, C.c_double)))
+    return float(out[0])
 
 
 def fblts_diagnostics_mass(ctx):

@@ -175,6 +175,8 @@ struct DevState {
     double *un[3];                      // unsplit: stored coarse stage velocities u~1, u~2, u~3
     double *unk[2];                     // unsplit: stored fine stage velocities uk1, uk2
     double *hT2;                        // fused subcycle: third fine level buffer (levels k-1, k, k+1 distinct)
+    double *eta, *dP, *accP, *Pv;       // vorticity companion: eta per vertex, integrated PV flux per edge,
+                                        // its IF-edge sum, the PV-flux part of the last slow sweep
     double *h2alt;                      // fused subcycle: stage-2 thickness of F\F^2 before it is published
     double *stage;                      // staging for set/get_state (max(nC, nE) doubles)
     int32_t *cellOld, *edgeOld;         // new -> old permutation (device)
@@ -229,7 +231,12 @@ void launch_slow_edge(const DevMesh &m, const DevState &st, const double *h, con
 void launch_slow_pre_range(const DevMesh &m, const DevState &st, const double *h, const double *u, int v0, int c0,
                            int e0, cudaStream_t s);
 void launch_slow_edge_range(const DevMesh &m, const DevState &st, const double *h, const double *u, double *out,
-                            int e0, int e1, const StepConst &sc, cudaStream_t s);
+                            int e0, int e1, const StepConst &sc, cudaStream_t s, double *pvout = nullptr);
+// prognostic absolute vorticity companion (unsplit, config vorticity): kernels.cu
+void launch_vort_int(const DevState &st, double c3, int e1, cudaStream_t s);
+void launch_vort_fine(const DevMesh &m, const DevState &st, double c3f, int first, cudaStream_t s);
+void launch_vort_close(const DevMesh &m, const DevState &st, double c3f, cudaStream_t s);
+void launch_vort_update(const DevMesh &m, const DevState &st, cudaStream_t s);
 // slow-term refresh views at t^{n,k} into st.hv (cells) and st.uv (edges)
 void launch_refresh_views(const DevMesh &m, const DevState &st, const double *hN, const double *hNew,
                           const double *hk, const double *uN, const double *uk, const StepConst &sc,
@@ -285,7 +292,8 @@ void launch_validate(const double *v, int n, int positive, int *bad, cudaStream_
 void launch_pack(const int32_t *idx, const double *a, double *buf, int n, cudaStream_t s);
 void launch_unpack(const int32_t *idx, const double *buf, double *a, int n, cudaStream_t s);
 // cells_only: the mass and min h partials alone (Gamma and max nu come back as 0)
+// pv: the vertex role sums the PV volume integral A_v h_v q_v instead of Gamma (out[1])
 void launch_diagnostics(const DevMesh &m, const double *h, const double *u, const StepConst &sc, double *part,
-                        double *out_dev, cudaStream_t s, bool cells_only = false);
+                        double *out_dev, cudaStream_t s, bool cells_only = false, bool pv = false);
 
 }  // namespace fblts

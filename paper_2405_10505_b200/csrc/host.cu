@@ -288,6 +288,7 @@ int fblts_create(fblts_ctx **out, const fblts_config *cfg) {
     if (cfg->unsplit && (cfg->nranks != 1 || cfg->scheme != FBLTS_SCHEME_FBLTS || cfg->slow_refresh))
         return FBLTS_ERR_INVALID_ARG;
     if (cfg->pv_energy && (cfg->nranks != 1 || cfg->slow_refresh)) return FBLTS_ERR_INVALID_ARG;
+    if (cfg->vorticity && (!cfg->unsplit || cfg->nranks != 1)) return FBLTS_ERR_INVALID_ARG;
     // No CUDA call here: mesh upload, labelling and renumbering are host work, so a context
     // can be created (and its labels inspected) on a machine without a GPU.
     fblts_ctx *c = new fblts_ctx();
@@ -1190,6 +1191,12 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
     const size_t nun = c->cfg.unsplit ? nE1 : 1;
     for (int q = 0; q < 3; ++q) put(s.un[q], nun);
     for (int q = 0; q < 2; ++q) put(s.unk[q], nun);
+    const bool vt = c->cfg.vorticity != 0;
+    put(s.eta, vt ? (size_t)std::max(1, L.nV) : 1);
+    put(s.dP, vt ? nE1 : 1);
+    put(s.accP, vt ? (size_t)std::max(1, L.eb.f - L.eb.if2) : 1);
+    put(s.Pv, vt ? nE1 : 1);
+    if (base && !vt) s.eta = s.dP = s.accP = s.Pv = nullptr;
     if (base) s.Sf = c->cfg.slow_refresh ? s.Sk : s.S;
     put(s.stage, std::max(m.nC, m.nE));
     put(s.cellOld, L.nC);
@@ -1438,6 +1445,22 @@ int fblts_set_state(fblts_ctx *c, const double *h, const double *u, double t) {
     c->phase = P_STATE;
     return FBLTS_OK;
 }
+
+int fblts_set_vorticity(fblts_ctx *c, const double *eta) {
+    if (!c || !eta) return FBLTS_ERR_INVALID_ARG;
+    if (!c->cfg.vorticity) return fail(c, FBLTS_ERR_ORDER, "set_vorticity: context created without cfg.vorticity");
+    if (c->phase != P_STATE) return fail(c, FBLTS_ERR_ORDER, "set_vorticity: set_state first");
+    const Local &L = c->lo;
+    std::vector<double> tmp(L.nV);
+    for (int v = 0; v < L.nV; ++v) {
+        tmp[v] = eta[L.vertGlob[v]];
+        if (!std::isfinite(tmp[v])) return fail(c, FBLTS_ERR_STATE, "set_vorticity: eta[%d] not finite", L.vertGlob[v]);
+    }
+    CUDA_TRY(c, cudaMemcpyAsync(c->ds.eta, tmp.data(), (size_t)L.nV * 8, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return FBLTS_OK;
+}
+
 
 }  // extern "C"
 
@@ -1822,9 +1845,11 @@ int enqueue_unsplit_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
         pc.c = 1.0 - (double)(k + 1) / (double)M;
         return pc;
     };
-    auto slow = [&](const double *U, int e0, int e1) {          // Phi^slow(U, st.hv) on [e0, e1) -> st.Sk
+    const bool vort = c->cfg.vorticity != 0;
+    auto slow = [&](const double *U, int e0, int e1, double *pvout = nullptr) {   // Phi^slow(U, st.hv) on [e0, e1) -> st.Sk
         if (!c->cfg.slow) {
             if (e1 > e0) cudaMemsetAsync(st.Sk + e0, 0, (size_t)(e1 - e0) * 8, s);
+            if (pvout && e1 > e0) cudaMemsetAsync(pvout + e0, 0, (size_t)(e1 - e0) * 8, s);
             return;
         }
         mark(K_SLOW_PRE);
@@ -1834,7 +1859,7 @@ int enqueue_unsplit_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
         if (e0 >= m.eb.f && !sc.pve) launch_slow_pre_range(m, st, st.hv, U, c->vminF, m.cb.if1, m.eb.if1, s);
         else launch_slow_pre_range(m, st, st.hv, U, 0, 0, 0, s);
         mark(K_SLOW_EDGE);
-        launch_slow_edge_range(m, st, st.hv, U, st.Sk, e0, e1, sc, s);
+        launch_slow_edge_range(m, st, st.hv, U, st.Sk, e0, e1, sc, s, pvout);
     };
     // ---- coarse phase: extents X1 = C u F^5, Y1 = C_E u F^4_E, X2 = C u F^3, Y2 = C_E u F^2_E,
     //      X3 = C u F^1, Y3 = IF-1_E u int_E (IF-2_E computed as scratch)
@@ -1847,9 +1872,10 @@ int enqueue_unsplit_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
     for (int q = 0; q < 3; ++q) {
         mark(kinds[q]);
         launch_un_cstage(m, st, q + 1, hN, Hs[q], Us[q], Hout[q], sc, Xend[q], s);
-        slow(Us[q], 0, Yend[q]);
+        slow(Us[q], 0, Yend[q], vort && q == 2 ? st.Pv : nullptr);
         mark(K_COARSE_VEL);
         launch_un_vel(m, st, uN, st.un[q], cs[q], 0, Yend[q], nullptr, 0, 0, 0, sc, s);
+        if (vort && q == 2) launch_vort_int(st, sc.c3, m.eb.if2, s);     // eta companion: int_E, dt PV
     }
     if (m.eb.if2 > 0) CUDA_TRY(c, cudaMemcpyAsync(uNew, st.un[2], (size_t)m.eb.if2 * 8, cudaMemcpyDeviceToDevice, s));
     // ---- fine phase
@@ -1873,13 +1899,16 @@ int enqueue_unsplit_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
             launch_un_views(m, st, 3, hN, hNew, hk, hk, uN, st.unk[1], sc, pc, s);   // U2 view for the sweep
             launch_un_fstage(m, st, 3, hN, hNew, hk, st.uv, hb(k), sc, pc, k, s);
             launch_un_views(m, st, 3, hN, hNew, hk, hb(k), uN, st.unk[1], sc, pc, s);
-            slow(st.uv, m.eb.if2, m.eb.end);
+            slow(st.uv, m.eb.if2, m.eb.end, vort ? st.Pv : nullptr);
             mark(K_FINE_VEL);
             launch_un_vel(m, st, uk, ub(k), sc.c3f, m.eb.if2, m.eb.end, st.accU, m.eb.if2, m.eb.f, k == 0, sc, s);
+            if (vort) launch_vort_fine(m, st, sc.c3f, k == 0, s);   // F_E: += dt/M PV^k; IF edges: sum_k PV^k
         }
         mark(K_CORRECT);
         launch_correct(m, st, hN, uN, hNew, uNew, sc, s, m.cb, true);
+        if (vort) launch_vort_close(m, st, sc.c3f, s);             // IF edges: dt/M sum_k PV^k
     }
+    if (vort) launch_vort_update(m, st, s);                        // eta_v += (sum t d dP) / A_v
     mark(-1);
     return FBLTS_OK;
 }
@@ -1947,9 +1976,9 @@ void dd_merge_host(double &ah, double &al, double bh, double bl) {
     ah = hi;
 }
 
-int diag_partial(fblts_ctx *c, double out6[6], bool cells_only = false) {
+int diag_partial(fblts_ctx *c, double out6[6], bool cells_only = false, bool pv = false) {
     launch_diagnostics(c->dm, c->hbuf[c->parity], c->ubuf[c->parity], c->sc, c->ds.diag, c->diag_out, c->stream,
-                       cells_only);
+                       cells_only, pv);
     CUDA_TRY(c, cudaGetLastError());
     CUDA_TRY(c, cudaMemcpyAsync(out6, c->diag_out, 6 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -2099,6 +2128,18 @@ int fblts_get_state(fblts_ctx *c, double *h, double *u, double *t) {
     return check_device_error(c);
 }
 
+int fblts_get_vorticity(fblts_ctx *c, double *eta) {
+    if (!c || !eta) return FBLTS_ERR_INVALID_ARG;
+    if (!c->cfg.vorticity) return fail(c, FBLTS_ERR_ORDER, "get_vorticity: context created without cfg.vorticity");
+    if (c->phase != P_STATE) return fail(c, FBLTS_ERR_ORDER, "get_vorticity: no state set");
+    const Local &L = c->lo;
+    std::vector<double> tmp(L.nV);
+    CUDA_TRY(c, cudaMemcpyAsync(tmp.data(), c->ds.eta, (size_t)L.nV * 8, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    for (int v = 0; v < L.nV; ++v) eta[L.vertGlob[v]] = tmp[v];
+    return check_device_error(c);
+}
+
 int fblts_diagnostics_async(fblts_ctx *c, double *out) {
     if (!c || !out) return FBLTS_ERR_INVALID_ARG;
     if (c->phase != P_STATE) return fail(c, FBLTS_ERR_ORDER, "diagnostics_async: no state set");
@@ -2145,6 +2186,28 @@ int fblts_diagnostics(fblts_ctx *c, double out[4]) {
         if (rc) return rc;
         diag_combine(all.data(), c->cfg.nranks, out);
     }
+    return check_device_error(c);
+}
+
+// PV volume integral sum_v A_v h_v q_v (Remark rmk:volume_conservation_pv, eq. vol_integral_pv).
+int fblts_diagnostics_pv(fblts_ctx *c, double *out) {
+    if (!c || !out) return FBLTS_ERR_INVALID_ARG;
+    if (c->phase != P_STATE) return fail(c, FBLTS_ERR_ORDER, "diagnostics_pv: no state set");
+    if (c->cfg.nranks > 1 && !c->nccl)
+        return fail(c, FBLTS_ERR_ORDER, "diagnostics_pv: loopback contexts are not supported");
+    if (c->dstream) CUDA_TRY(c, cudaStreamSynchronize(c->dstream));
+    double part[6], four[4];
+    int rc = diag_partial(c, part, false, true);
+    if (rc) return rc;
+    if (c->cfg.nranks == 1) {
+        diag_combine(part, 1, four);
+    } else {
+        std::vector<double> all(6 * (size_t)c->cfg.nranks);
+        rc = allgather_nccl(c, part, all.data());
+        if (rc) return rc;
+        diag_combine(all.data(), c->cfg.nranks, four);
+    }
+    *out = four[1];
     return check_device_error(c);
 }
 

@@ -43,7 +43,7 @@ constexpr int TPB = 256;
 #define FBLTS_TILE_NBUF 2
 #endif
 constexpr int NBUF = FBLTS_TILE_NBUF;   // tile buffers of the staged kernel's pipeline
-static_assert(NBUF == 2, "k_stage_tiled is a two-buffer pipeline");
+static_assert(NBUF == 2 || NBUF == 3, "k_stage_tiled pipelines 2 or 3 tile buffers");
 #ifndef FBLTS_TILE_NTHR
 #define FBLTS_TILE_NTHR 256
 #endif
@@ -171,8 +171,8 @@ __global__ void __launch_bounds__(TPB, FBLTS_SLOW_MINB) k_slow_edge(DevMesh m, c
                                                    const double *__restrict__ q, const double *__restrict__ K,
                                                    const double *__restrict__ F, const double *__restrict__ u,
                                                    const double *__restrict__ qe,
-                                                   double *__restrict__ S, double rho0, double cd, double cw,
-                                                   int e0, int e1) {
+                                                   double *__restrict__ S, double *__restrict__ pvout,
+                                                   double rho0, double cd, double cw, int e0, int e1) {
     const int e = e0 + blockIdx.x * TPB + threadIdx.x;
     if (e >= e1) return;
     const int n = m.nEoE[e];
@@ -211,6 +211,7 @@ __global__ void __launch_bounds__(TPB, FBLTS_SLOW_MINB) k_slow_edge(DevMesh m, c
         const double qh = 0.5 * (q[v.x] + q[v.y]);
         pv = qh * fp;
     }
+    if (pvout) pvout[e] = pv;                 // vorticity companion: the PV-flux part alone
     const double he = 0.5 * (h[c.x] + h[c.y]);
     const double G = m.tau[e] / (rho0 * he);
     double s = pv - (K[c.y] - K[c.x]) / m.dc[e] + G;
@@ -471,33 +472,46 @@ __global__ void __launch_bounds__(NTHR, FBLTS_TILE_MINB) k_stage_tiled(DevMesh m
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    // Two tile buffers: while tile k is computed the other buffer fills with tile k+1 -- one thread
-    // issues its bulk copies at the top of the iteration, and every thread issues its halo / foreign
-    // gathers after the edge phase (their indices, loaded at the top, have arrived by then; issued
-    // earlier they only slow the edge phase's shared-memory traffic -- measured).  The halo / foreign
-    // copies of a tile form one cp.async group, committed once per iteration (even if empty).  Tile
-    // records are carried in registers and loaded one iteration ahead.
+    // NBUF tile buffers (2 or 3): while tile k is computed, tiles k+1 .. k+NBUF-1 are in flight.  At
+    // the top of the iteration for tile k one thread issues the bulk copies of tile k+NBUF-1 into the
+    // buffer tile k-1 just freed, and every thread issues that tile's halo / foreign gathers after the
+    // edge phase (their indices, loaded at the top, have arrived by then; issued earlier they only slow
+    // the edge phase's shared-memory traffic -- measured).  The gathers of a tile form one cp.async
+    // group, committed once per iteration (even if empty), so "all but the newest NBUF-2 groups" is
+    // exactly tile k's.  Tile records are carried in registers, loaded NBUF tiles ahead.
     int hx[HPT], fx[FPT];
-    TileRec rc = load_rec(t, tile), rn{};
-    if (tid == 0) issue_bulk<STAGE>(m, a, rc, buf0, CS2, ES2, &bar[0]);
-    load_indices(t, rc, tid, hx, fx);
-    issue_indexed<STAGE>(m, a, rc, TileBuf<STAGE>(buf0, CS2, ES2, rc), tid, hx, fx);
-    cp_async_commit();
-    if (tile + G0 < tile1) rn = load_rec(t, tile + G0);
+    TileRec r0 = load_rec(t, tile), r1{}, r2{};
+    if (tile + G0 < tile1) r1 = load_rec(t, tile + G0);
+    if (NBUF == 3 && tile + 2 * G0 < tile1) r2 = load_rec(t, tile + 2 * G0);
+    for (int k = 0; k < NBUF - 1; ++k) {                  // prologue: tiles 0 .. NBUF-2
+        const TileRec &rk = k == 0 ? r0 : r1;
+        if (tile + k * G0 < tile1) {
+            double *Bk = buf0 + k * BUF;
+            if (tid == 0) issue_bulk<STAGE>(m, a, rk, Bk, CS2, ES2, &bar[k]);
+            load_indices(t, rk, tid, hx, fx);
+            issue_indexed<STAGE>(m, a, rk, TileBuf<STAGE>(Bk, CS2, ES2, rk), tid, hx, fx);
+        }
+        cp_async_commit();
+    }
     unsigned phase = 0u;                                   // bit b: parity of buffer b's next completion
     int buf = 0;
-    for (; tile < tile1; tile += G0, buf ^= 1) {
-        const TileRec cur = rc, nx = rn;
-        const bool more = tile + G0 < tile1;
-        if (tile + 2 * G0 < tile1) rn = load_rec(t, tile + 2 * G0);     // consumed next iteration
-        rc = nx;
+    for (; tile < tile1; tile += G0, buf = (buf + 1 == NBUF ? 0 : buf + 1)) {
+        const TileRec cur = r0;
+        const TileRec nx = NBUF == 2 ? r1 : r2;            // tile + (NBUF-1) G0, issued this iteration
+        const int tn = tile + (NBUF - 1) * G0;
+        const bool more = tn < tile1;
+        TileRec rl{};
+        if (tn + G0 < tile1) rl = load_rec(t, tn + G0);    // consumed next iteration
+        r0 = r1;
+        if (NBUF == 2) r1 = rl; else r1 = r2, r2 = rl;
         mbar_wait(&bar[buf], (phase >> buf) & 1u);
         phase ^= 1u << buf;
-        cp_async_wait_pending<0>();
-        __syncthreads();                                   // tile `cur` staged; the other buffer is free
-        double *Bn = buf0 + (buf ^ 1) * BUF;
+        cp_async_wait_pending<NBUF - 2>();
+        __syncthreads();                                   // tile `cur` staged; tile k-1's buffer is free
+        const int bn = buf == 0 ? NBUF - 1 : buf - 1;
+        double *Bn = buf0 + bn * BUF;
         if (more) {
-            if (tid == 0) issue_bulk<STAGE>(m, a, nx, Bn, CS2, ES2, &bar[buf ^ 1]);
+            if (tid == 0) issue_bulk<STAGE>(m, a, nx, Bn, CS2, ES2, &bar[bn]);
             load_indices(t, nx, tid, hx, fx);              // consumed after the edge phase
         }
         const TileBuf<STAGE> bc(buf0 + buf * BUF, CS2, ES2, cur);
@@ -976,7 +990,7 @@ __device__ __forceinline__ DD dd_merge(DD a, DD b) {
 // deterministic function of the state.
 __global__ void __launch_bounds__(TPB) k_diag_partial(DevMesh m, const double *__restrict__ h,
                                                       const double *__restrict__ u, StepConst sc,
-                                                      double *__restrict__ part) {
+                                                      double *__restrict__ part, int pvmode) {
     const int role = blockIdx.x / DIAG_RB;
     const int tid = (blockIdx.x - role * DIAG_RB) * TPB + threadIdx.x;
     const int T = DIAG_RB * TPB;
@@ -1001,7 +1015,17 @@ __global__ void __launch_bounds__(TPB) k_diag_partial(DevMesh m, const double *_
                 const double t = m.dc[e] * u[e];
                 circ = circ + (pos ? t : -t);
             }
-            dd_add(gam, circ + m.areaTri[v] * m.fV[v]);
+            if (pvmode) {   // PV volume integral term A_v h_v q_v (Remark rmk:volume_conservation_pv)
+                const double A = m.areaTri[v];
+                double hv = 0.0;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) hv = hv + m.kite[k * m.strideV + v] * h[m.cov[k * m.strideV + v]];
+                hv = hv / A;
+                const double q = (circ / A + m.fV[v]) / hv;
+                dd_add(gam, A * hv * q);
+            } else {
+                dd_add(gam, circ + m.areaTri[v] * m.fV[v]);
+            }
         }
     } else {
 #pragma unroll 4
@@ -1488,12 +1512,12 @@ __global__ void __launch_bounds__(TPB) k_qhat(DevMesh m, const double *__restric
 }
 
 void launch_slow_edge_range(const DevMesh &m, const DevState &st, const double *h, const double *u, double *out,
-                            int e0, int e1, const StepConst &sc, cudaStream_t s) {
+                            int e0, int e1, const StepConst &sc, cudaStream_t s, double *pvout) {
     if (e1 <= e0) return;
     const unsigned nb = nblocks(e1 - e0);
     if (sc.pve) k_qhat<<<nblocks(m.nE), TPB, 0, s>>>(m, st.q, st.qe);
 #define FBLTS_SLOW_EDGE3(ME2, HU, PV)                                                                              \
-    k_slow_edge<ME2, HU, PV><<<nb, TPB, 0, s>>>(m, h, st.q, st.K, st.F, u, st.qe, out, sc.rho0, sc.cd, sc.cw, e0, e1)
+    k_slow_edge<ME2, HU, PV><<<nb, TPB, 0, s>>>(m, h, st.q, st.K, st.F, u, st.qe, out, pvout, sc.rho0, sc.cd, sc.cw, e0, e1)
 #define FBLTS_SLOW_EDGE(ME2)                                                                                     \
     do {                                                                                                         \
         if (sc.pve) {                                                                                            \
@@ -1630,9 +1654,9 @@ void launch_unpack(const int32_t *idx, const double *buf, double *a, int n, cuda
     if (n > 0) k_unpack<<<nblocks(n), TPB, 0, s>>>(idx, buf, a, n);
 }
 void launch_diagnostics(const DevMesh &m, const double *h, const double *u, const StepConst &sc, double *part,
-                        double *out_dev, cudaStream_t s, bool cells_only) {
+                        double *out_dev, cudaStream_t s, bool cells_only, bool pv) {
     const int nb = cells_only ? DIAG_RB : DIAG_BLOCKS;     // role 0 (mass, min h) is blocks [0, DIAG_RB)
-    k_diag_partial<<<nb, TPB, 0, s>>>(m, h, u, sc, part);
+    k_diag_partial<<<nb, TPB, 0, s>>>(m, h, u, sc, part, pv ? 1 : 0);
     k_diag_final<<<1, TPB, 0, s>>>(part, nb, out_dev);
 }
 
@@ -1808,6 +1832,53 @@ void launch_un_fstage(const DevMesh &m, const DevState &st, int stage, const dou
         else
             k_un_fstage<G, 3><<<nblocks(end - b0), TPB, 0, s>>>(m, a, U, out, st.accH, sc, pc, k, b0, end, st.err);
     });
+}
+
+// ---------------------------------------------------------------- prognostic absolute vorticity (N1)
+// Theorem 2, SPEC step_prognostic_vorticity: the PV-flux term of every
+// velocity update is integrated per edge exactly as the velocity integrates it (oracle lts.fblts_step
+// eta=...): int_E dP = dt PV (coarse stage 3); F_E dP = sum_k dt/M PV^k (ascending k from +0.0);
+// IF-1_E u IF-2_E dP = dt/M sum_k PV^k; then eta_v += (sum_j t_{e_j,v} d_{e_j} dP_{e_j}) / A_v.
+__global__ void k_vort_int(double *__restrict__ dP, const double *__restrict__ P, double c3, int e1) {
+    const int e = blockIdx.x * TPB + threadIdx.x;
+    if (e < e1) dP[e] = c3 * P[e];
+}
+__global__ void k_vort_fine(double *__restrict__ dP, double *__restrict__ accP, const double *__restrict__ P,
+                            double c3f, int if2, int f, int end, int first) {
+    const int e = if2 + blockIdx.x * TPB + threadIdx.x;
+    if (e >= end) return;
+    if (e < f) accP[e - if2] = (first ? 0.0 : accP[e - if2]) + P[e];
+    else dP[e] = (first ? 0.0 : dP[e]) + c3f * P[e];
+}
+__global__ void k_vort_close(double *__restrict__ dP, const double *__restrict__ accP, double c3f, int if2, int f) {
+    const int e = if2 + blockIdx.x * TPB + threadIdx.x;
+    if (e < f) dP[e] = c3f * accP[e - if2];
+}
+__global__ void k_vort_update(DevMesh m, double *__restrict__ eta, const double *__restrict__ dP) {
+    const int v = blockIdx.x * TPB + threadIdx.x;
+    if (v >= m.nV) return;
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        bool pos;
+        const int e = decode(m.eov[k * m.strideV + v], pos);
+        const double t = m.dc[e] * dP[e];
+        acc = acc + (pos ? t : -t);
+    }
+    eta[v] = eta[v] + acc / m.areaTri[v];
+}
+void launch_vort_int(const DevState &st, double c3, int e1, cudaStream_t s) {
+    if (e1 > 0) k_vort_int<<<nblocks(e1), TPB, 0, s>>>(st.dP, st.Pv, c3, e1);
+}
+void launch_vort_fine(const DevMesh &m, const DevState &st, double c3f, int first, cudaStream_t s) {
+    if (m.eb.end > m.eb.if2)
+        k_vort_fine<<<nblocks(m.eb.end - m.eb.if2), TPB, 0, s>>>(st.dP, st.accP, st.Pv, c3f, m.eb.if2, m.eb.f, m.eb.end, first);
+}
+void launch_vort_close(const DevMesh &m, const DevState &st, double c3f, cudaStream_t s) {
+    if (m.eb.f > m.eb.if2) k_vort_close<<<nblocks(m.eb.f - m.eb.if2), TPB, 0, s>>>(st.dP, st.accP, c3f, m.eb.if2, m.eb.f);
+}
+void launch_vort_update(const DevMesh &m, const DevState &st, cudaStream_t s) {
+    if (m.nV > 0) k_vort_update<<<nblocks(m.nV), TPB, 0, s>>>(m, st.eta, st.dP);
 }
 }  // namespace fblts
 

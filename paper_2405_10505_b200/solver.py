@@ -21,16 +21,17 @@ from . import _abi as abi
 class Solver:
     def __init__(self, mesh, fine_mask, dt, M, *, g=9.81, beta=(0.531, 0.531, 0.313), rho0=1000.0, r=2,
                  slow=True, tau_n=None, device=None, stream=None, rank=0, nranks=1, nccl_id=None, scheme="fblts",
-                 slow_refresh=False, hurricane=None, unsplit=False, pv="centered"):
+                 slow_refresh=False, hurricane=None, unsplit=False, pv="centered", vorticity=False):
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2405_10505_b200.Solver needs a CUDA device (no CPU fallback)")
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
-        self.nCells, self.nEdges = int(mesh.nCells), int(mesh.nEdges)
+        self.nCells, self.nEdges, self.nVertices = int(mesh.nCells), int(mesh.nEdges), int(mesh.nVertices)
         self.ctx = abi.fblts_create(dt, M, g=g, beta=beta, rho0=rho0, r=r, slow=slow, device=self.device.index,
                                     stream=self.stream.cuda_stream, rank=rank, nranks=nranks, nccl_id=nccl_id,
                                     scheme=scheme, slow_refresh=slow_refresh,
-                                    sal=(hurricane or {}).get("sal", 0.0), unsplit=unsplit, pv=pv)
+                                    sal=(hurricane or {}).get("sal", 0.0), unsplit=unsplit, pv=pv,
+                                    vorticity=vorticity)
         self.rank, self.nranks = rank, nranks
         try:
             abi.fblts_upload_mesh(self.ctx, mesh)
@@ -66,6 +67,13 @@ class Solver:
     def set_state(self, h, u, t=0.0):
         abi.fblts_set_state(self.ctx, h, u, t)
 
+    def set_vorticity(self, eta):
+        """Prognostic absolute vorticity per vertex (vorticity=True contexts; Theorem 2 companion)."""
+        abi.fblts_set_vorticity(self.ctx, eta, self.nVertices)
+
+    def vorticity(self):
+        return abi.fblts_get_vorticity(self.ctx, self.nVertices)
+
     def set_forcing(self, tau_n):
         abi.fblts_set_forcing(self.ctx, tau_n)
 
@@ -87,6 +95,10 @@ class Solver:
         d = abi.fblts_diagnostics(self.ctx)
         self._pending.clear()
         return d
+
+    def pv_volume(self):
+        """sum_v A_v h_v q_v, the volume integral of PV (Remark rmk:volume_conservation_pv)."""
+        return abi.fblts_diagnostics_pv(self.ctx)
 
     def diagnostics_mass(self):
         """(total mass, min h) of the current state: the cell part of diagnostics(), same bits."""

@@ -13,7 +13,7 @@ import pytest
 
 from inputs import configs
 from oracle import diagnostics as dg
-from oracle import fbrk32, lts
+from oracle import fbrk32, lts, trisk
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-11
@@ -481,6 +481,37 @@ def test_unsplit_matches_oracle(Solver, which, M):
     assert np.array_equal(hg, ho) and np.array_equal(ug, uo), "not bitwise (canonical arithmetic, --fmad=false)"
 
 
+@pytest.mark.parametrize("which,M", [("config1", 4), ("shelf", 3), ("shelf", 1)])
+def test_vorticity_companion_theorem2(Solver, which, M):
+    """Prognostic absolute vorticity companion in unsplit mode (Theorem 2; SPEC
+    step_prognostic_vorticity): through the C ABI (cfg.vorticity) the eta the GPU
+    advances -- the PV flux of every coarse / fine / correction velocity update, integrated per edge --
+    equals the oracle's fblts_step(eta=...) bit for bit after 30 steps, and its total sum_v A_v eta_v
+    is conserved to roundoff (Theorem 2); h and u stay bitwise equal too."""
+    c = configs.config1() if which == "config1" else configs.small_shelf(nx=64, ny=48, seed=5,
+                                                                          dt=20.0 if M > 1 else 5.0)
+    m = c.mesh
+    n = 30
+    lab = lts.label_regions(m, c.fine_mask)
+    eta0 = trisk.relative_vorticity(m, c.u0) + m.fVertex
+    ho, uo, eo = lts.run(m, lab, c.h0, c.u0, c.dt, M, phys_of(c), n, split=False, eta=eta0)
+    s = Solver(m, c.fine_mask, c.dt, M, g=c.g, beta=c.beta, rho0=c.rho0, slow=c.slow, tau_n=c.tau_n,
+               unsplit=True, vorticity=True)
+    s.set_state(c.h0, c.u0)
+    s.set_vorticity(eta0)
+    s.step(n)
+    hg, ug, _ = s.state()
+    eg = s.vorticity()
+    s.close()
+    assert np.array_equal(hg, ho) and np.array_equal(ug, uo)
+    assert np.array_equal(eg, eo), float(np.max(np.abs(eg - eo)))
+    scale = float(np.sum(m.areaTriangle * np.abs(eta0)))
+    drift = abs(float(np.sum(m.areaTriangle * eg)) - float(np.sum(m.areaTriangle * eta0))) / scale
+    print(f"vorticity companion {which} M={M}: bitwise, Theorem-2 drift {drift:.2e}")
+    assert drift <= 1e-13
+    assert np.max(np.abs(eg - eta0)) > 0.0
+
+
 @pytest.mark.parametrize("M", [1, 2, 4])
 def test_fused_subcycle_matches_oracle(Solver, monkeypatch, M):
     """The fused fine subcycle (one CTA advances a tile of F\\F^5 -- or of F\\F^2 with
@@ -590,3 +621,23 @@ def test_fused_subcycle_on_scvt_sphere(Solver, monkeypatch):
         pytest.skip(f"no subcycle tiles on this mesh ({cnt['cells_by_region']})")
     assert_parity(hg, ug, ho, uo)
     assert np.array_equal(hg, ho) and np.array_equal(ug, uo)
+
+
+def test_pv_volume_integral_on_gpu(Solver):
+    """The PV volume integral sum_v A_v h_v q_v (Remark rmk:volume_conservation_pv)
+    computed on the device (fblts_diagnostics_pv) equals the oracle's total_pv_volume to 1e-14 relative
+    on a stepped state, and is conserved over 50 FB-LTS steps to 1e-13 of sum_v A_v |f_v| (it equals
+    Gamma up to rounding, Theorem 2)."""
+    c = configs.small_shelf(nx=48, ny=40, dt=25.0)
+    s = Solver(c.mesh, c.fine_mask, c.dt, c.M, g=c.g, beta=c.beta, rho0=c.rho0, slow=c.slow, tau_n=c.tau_n)
+    s.set_state(c.h0, c.u0)
+    p0 = s.pv_volume()
+    s.step(50)
+    h, u, _ = s.state()
+    p1 = s.pv_volume()
+    s.close()
+    ref = dg.total_pv_volume(c.mesh, h, u)
+    scale = float(np.sum(c.mesh.areaTriangle * np.abs(c.mesh.fVertex)))
+    assert abs(p1 - ref) <= 1e-14 * scale
+    assert abs(p0 - dg.total_pv_volume(c.mesh, c.h0, c.u0)) <= 1e-14 * scale
+    assert abs(p1 - p0) <= 1e-13 * scale
