@@ -296,9 +296,19 @@ def arm_native(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # NCCL's init lines (ranks, transports) on stderr
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     t_setup = time.perf_counter()
-    c = make_case(args.config, rank)
+    weak = world > 1 and args.scaling == "weak" and args.config == "config5"
+    piece = None
+    if weak:
+        # weak scaling (reading Q25): config 5 stacked N times in y, each rank generating, labelling and
+        # partitioning ONLY its piece (its 4096 x 4096 block plus a 16-row margin), O(block) set-up
+        from inputs import configs
+        piece = configs.config5_weak_piece(rank, world)
+        c = piece.case
+    else:
+        c = make_case(args.config, rank)
     nccl_id = None
     if world > 1:                    # partitioned run: the library's own NCCL communicator for the halos
         from paper_2405_10505_b200 import abi
@@ -306,7 +316,8 @@ def arm_native(args):
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     s = Solver(c.mesh, c.fine_mask, c.dt, c.M, g=c.g, beta=c.beta, rho0=c.rho0, slow=c.slow, tau_n=c.tau_n,
-               rank=rank, nranks=world, nccl_id=nccl_id, slow_refresh=args.slow_refresh, unsplit=args.unsplit)
+               rank=rank, nranks=world, nccl_id=nccl_id, slow_refresh=args.slow_refresh, unsplit=args.unsplit,
+               partition=(piece.owner, piece.gid) if piece is not None else None)
     s.set_state(c.h0, c.u0, 0.0)
     counts = s.counts()
     t_setup = time.perf_counter() - t_setup
@@ -337,7 +348,8 @@ def arm_native(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    units = c.mesh.nCells * c.M * args.steps        # the whole mesh is advanced once per step (all ranks)
+    n_whole = len(piece.own) * world if piece is not None else c.mesh.nCells   # cells of the whole mesh
+    units = n_whole * c.M * args.steps              # the whole mesh is advanced once per step (all ranks)
     value = units / (ms * 1e-3)
 
     # ---------------- instrumented replay: per-kernel device time (events on the same stream)
@@ -446,18 +458,22 @@ def arm_native(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak" if world == 1 else "strong",
+        "scaling": "weak" if (world == 1 or weak) else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "scaling_note": "strong: the same config-5 mesh is partitioned over N GPUs (a weak-scaled 4096 x 4096N "
-                        "mesh needs a distributed mesh upload, DESIGN.md section 7)" if world > 1 else None,
-        "config": {"workload": args.config, "slow_refresh": bool(args.slow_refresh), "unsplit": bool(args.unsplit),
-                   "cells": c.mesh.nCells, "edges": c.mesh.nEdges,
+        "scaling_note": ("weak: config 5 stacked N times in y (4096 x 4096N cells), a 4096 x 4096 block per GPU; "
+                         "each rank builds only its piece (fblts_set_partition)") if weak else
+                        ("strong: the same config-5 mesh partitioned over N GPUs (dual-set SFC partition)"
+                         if world > 1 else None),
+        "config": {"workload": args.config + ("_weak" if weak else ""), "slow_refresh": bool(args.slow_refresh),
+                   "unsplit": bool(args.unsplit),
+                   "cells": n_whole, "cells_per_rank_piece": c.mesh.nCells if weak else None, "edges": c.mesh.nEdges,
                    "vertices": c.mesh.nVertices, "M": c.M, "dt": c.dt,
                    "cells_by_region": counts["cells_by_region"],
                    "l2": "inputs larger than L2 (no flush needed)" if c.mesh.nCells > 2_000_000 else
                          "working set may be L2-resident (no flush)",
                    "parallelism": "1 GPU" if world == 1 else
-                   f"{world} GPUs, dual-set SFC partition of one mesh, NCCL halo exchange per stage",
+                   (f"{world} GPUs, one 4096 x 4096 row block each, NCCL halo exchange per stage" if weak else
+                    f"{world} GPUs, dual-set SFC partition of one mesh, NCCL halo exchange per stage"),
                    "setup_s": round(t_setup, 1), "build": build_info},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "bytes_per_launch": bm[dom] / launches_dom,
@@ -484,6 +500,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--config", default="config5")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1 on config5: weak (a 4096 x 4096 block per GPU, default) or strong (one 4096^2 mesh)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-global", action="store_true", help="skip the global FB-RK(3,2) comparison run")

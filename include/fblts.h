@@ -172,9 +172,23 @@ int fblts_get_counts(fblts_ctx *ctx, int64_t *out);
 /* Halo exchange lists of this rank with `peer` (host logic, no device needed): which = 0 ring-1
  * cells (after every thickness stage), 1 = rings 1-2 cells (end of step), 2 = remote-owned edges
  * (end of step).  *n_send / *n_recv receive the counts; send_ids / recv_ids (may be NULL) receive
- * the GLOBAL ids in exchange order (ascending global id, identical on both sides). */
+ * the GLOBAL ids in exchange order (ascending global id, identical on both sides); after
+ * fblts_set_partition the whole-mesh ids (cells: gid; edges: (min gid << 32) | max gid). */
 int fblts_get_halo(fblts_ctx *ctx, int32_t which, int32_t peer, int64_t *n_send, int64_t *n_recv,
                    int64_t *send_ids, int64_t *recv_ids);
+
+/* Distributed set-up (optional; after upload_mesh, before set_regions): the uploaded mesh is this rank's
+ * PIECE of a larger mesh -- the cells it owns plus a margin of cells owned by other ranks, closed (every
+ * edge has two cells) -- and owner[i] / cell_gid[i] [nCells] give the owning rank and the id in the whole
+ * mesh of piece cell i.  set_regions then labels the piece (exact for every cell whose
+ * (2 + 5r)-ring neighbourhood lies in the piece -- keep the margin >= 2 + 5r + 2 rings wide), uses
+ * `owner` instead of the dual-set partition, and orders every halo list by whole-mesh ids (cells: gid;
+ * edges: (min gid << 32) | max gid of the edge's cells), so ranks that each hold only their piece agree
+ * element by element.  Every rank's piece must contain fine cells if the whole mesh does.  State I/O
+ * (set_state / get_state) is then in piece order.  Also valid with the whole mesh as the piece (an
+ * externally chosen partition).  Errors: INVALID_ARG (owner outside [0, nranks), gid < 0 or >= 2^31 or
+ * repeated, no owned cell), ORDER. */
+int fblts_set_partition(fblts_ctx *ctx, const int32_t *owner, const int64_t *cell_gid);
 
 /* 128-byte ncclUniqueId for a multi-rank context (call on rank 0, broadcast, pass as cfg.nccl_id). */
 int fblts_nccl_unique_id(void *out128);

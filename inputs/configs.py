@@ -12,6 +12,7 @@ from __future__ import annotations
 import dataclasses
 import json
 import os
+import types
 
 import numpy as np
 
@@ -104,6 +105,37 @@ def load_dt(name, default):
         return default
 
 
+def lattice_positions(nx, ny, dc):
+    """Cell centres of the odd-r periodic hex lattice, the formula of hexmesh.build_periodic_hex_mesh(_fast):
+    (x, y) = ((i + (j mod 2)/2) dc, j dc sqrt(3)/2) for cell c = j nx + i."""
+    c = np.arange(nx * ny, dtype=np.int64)
+    jj, ii = np.divmod(c, nx)
+    xc = (ii + 0.5 * (jj & 1)) * dc
+    yc = jj * (dc * np.sqrt(3.0) / 2.0)
+    return xc, yc, nx * dc, ny * dc * np.sqrt(3.0) / 2.0
+
+
+def shelf_fields(xc, yc, Lx, Ly, nx, ny, dc, rng, *, n_tiles=1, H_lo=10.0, H_hi=4000.0, W=20e3, rough=0.05,
+                 corr=20e3, fine_H=250.0, bumps_per_tile=8, sigma=40e3, amp=(0.5, 2.0)):
+    """Bathymetry H, initial surface eta and the fine mask of the shelf recipe on the lattice cells
+    (readings Q20-Q23); draws from rng in a fixed order (GRF, then the bumps)."""
+    Lt = Lx / n_tiles
+    S = periodic_step(np.mod(xc, Lt), Lt, W)
+    H = H_lo + (H_hi - H_lo) * S
+    if rough:
+        xi = grf_periodic(nx, ny, dc, dc * np.sqrt(3) / 2, corr, rng)
+        H = H * (1.0 + rough * xi)
+    centres, amps = [], []
+    for t in range(n_tiles):
+        cx = rng.uniform(t * Lt, (t + 1) * Lt, bumps_per_tile)
+        cy = rng.uniform(0, Ly, bumps_per_tile)
+        centres += list(zip(cx, cy))
+        amps += list(rng.uniform(amp[0], amp[1], bumps_per_tile))
+    grid = types.SimpleNamespace(nCells=xc.size, xCell=xc, yCell=yc, Lx=Lx, Ly=Ly)
+    eta = periodic_gaussians(grid, centres, amps, sigma)
+    return H, eta, H > fine_H
+
+
 def shelf_case(name, nx, ny, dc, seed, *, n_tiles=1, H_lo=10.0, H_hi=4000.0, W=20e3,
                rough=0.05, corr=20e3, fine_H=250.0, bumps_per_tile=8, sigma=40e3,
                amp=(0.5, 2.0), forcing=True, M=4, n_steps=200, dt=None, slow=True,
@@ -116,25 +148,14 @@ def shelf_case(name, nx, ny, dc, seed, *, n_tiles=1, H_lo=10.0, H_hi=4000.0, W=2
     """
     rng = np.random.default_rng(seed)
     mesh = (build_periodic_hex_mesh_fast if builder == "lattice" else build_periodic_hex_mesh)(nx, ny, dc)
-    Lt = mesh.Lx / n_tiles
-    S = periodic_step(np.mod(mesh.xCell, Lt), Lt, W)
-    H = H_lo + (H_hi - H_lo) * S
-    if rough:
-        xi = grf_periodic(nx, ny, dc, dc * np.sqrt(3) / 2, corr, rng)
-        H = H * (1.0 + rough * xi)
+    H, eta, fine = shelf_fields(mesh.xCell, mesh.yCell, mesh.Lx, mesh.Ly, nx, ny, dc, rng, n_tiles=n_tiles,
+                                H_lo=H_lo, H_hi=H_hi, W=W, rough=rough, corr=corr, fine_H=fine_H,
+                                bumps_per_tile=bumps_per_tile, sigma=sigma, amp=amp)
     mesh.bottomDepth = H
     mesh.fVertex = np.full(mesh.nVertices, F_PLANE)
-    centres, amps = [], []
-    for t in range(n_tiles):
-        cx = rng.uniform(t * Lt, (t + 1) * Lt, bumps_per_tile)
-        cy = rng.uniform(0, mesh.Ly, bumps_per_tile)
-        centres += list(zip(cx, cy))
-        amps += list(rng.uniform(amp[0], amp[1], bumps_per_tile))
-    eta = periodic_gaussians(mesh, centres, amps, sigma)
     h0 = H + eta
     u0 = np.zeros(mesh.nEdges)
     tau_n = TAU_X * mesh.edgeNormal[:, 0] if forcing else np.zeros(mesh.nEdges)
-    fine = H > fine_H
     if dt is None:
         dt = load_dt(name, 0.5 * dc / np.sqrt(G * H_hi * 1.1))
     return Case(name=name, mesh=mesh, h0=h0, u0=u0, fine_mask=fine, tau_n=tau_n, M=M,
@@ -167,6 +188,50 @@ def config5(seed=5, dt=None, nx=4096, ny=4096) -> Case:
     """BASELINE config 5: 4096x4096, dc = 500 m, config 2's profile per 256-km x-tile (8 tiles)."""
     n_tiles = max(1, int(round(nx * 500.0 / 256e3)))
     return shelf_case("config5", nx, ny, 500.0, seed, n_tiles=n_tiles, n_steps=50, dt=dt, builder="lattice")
+
+
+WEAK_MARGIN = 16     # rows of neighbouring blocks in a weak piece: >= 2 halo rings + 5r label rings + 4
+
+
+@dataclasses.dataclass
+class Piece:
+    """Rank `rank`'s piece of the weak-scaled config 5 (reading Q25): the N x 1 stack in y of the
+    config-5 block, 4096 x 4096N cells; the piece holds rows [r 4096 - m, (r+1) 4096 + m) of it as a
+    closed y-periodic strip (the wrap joins the two far margin rows only).  owner / gid per piece cell
+    (fblts_set_partition); block_cell maps a piece cell to its config-5 block cell, own its owned cells."""
+    case: Case
+    owner: np.ndarray
+    gid: np.ndarray
+    block_cell: np.ndarray
+    own: np.ndarray
+
+
+def config5_weak_piece(rank, nranks, seed=5, nx=4096, ny=4096, margin=WEAK_MARGIN, dt=None) -> Piece:
+    """Weak scaling of config 5 (BASELINE "Weak/strong scaling at 1/2/4/8"; reading Q25: a 4096 x 4096
+    block per GPU, composition preserved): the whole mesh is the config-5 block repeated nranks times in
+    y -- every field periodic with the block, so each block evolves exactly as config 5 does on its own
+    and rank r's owned rows must reproduce the one-GPU config-5 state bit for bit.  Each rank builds only
+    its piece: the block's fields (the config-5 recipe and seed, drawn on the block's lattice) indexed by
+    row, on a (ny + 2 margin)-row lattice mesh.  INPUT GENERATION ONLY."""
+    if margin % 2 or margin < 14:
+        raise ValueError("margin must be even (row parity) and >= 14")
+    n_tiles = max(1, int(round(nx * 500.0 / 256e3)))
+    xc, yc, Lx, Ly = lattice_positions(nx, ny, 500.0)
+    H_b, eta_b, fine_b = shelf_fields(xc, yc, Lx, Ly, nx, ny, 500.0, np.random.default_rng(seed), n_tiles=n_tiles)
+    nyp = ny + 2 * margin if nranks > 1 else ny
+    mesh = build_periodic_hex_mesh_fast(nx, nyp, 500.0)
+    j, i = np.divmod(np.arange(nx * nyp, dtype=np.int64), nx)
+    grow = (rank * ny - (margin if nranks > 1 else 0) + j) % (ny * nranks)     # row in the whole mesh
+    bcell = (grow % ny) * nx + i
+    mesh.bottomDepth = H_b[bcell]
+    mesh.fVertex = np.full(mesh.nVertices, F_PLANE)
+    owner = (grow // ny).astype(np.int32)
+    gid = grow * nx + i
+    if dt is None:
+        dt = load_dt("config5", 0.5 * 500.0 / np.sqrt(G * 4000.0 * 1.1))
+    case = Case(name="config5_weak", mesh=mesh, h0=H_b[bcell] + eta_b[bcell], u0=np.zeros(mesh.nEdges),
+                fine_mask=fine_b[bcell], tau_n=TAU_X * mesh.edgeNormal[:, 0], M=4, dt=dt, n_steps=50, seed=seed)
+    return Piece(case=case, owner=owner, gid=gid, block_cell=bcell, own=np.nonzero(owner == rank)[0])
 
 
 def small_shelf(seed=7, nx=48, ny=40, dc=2e3, **kw) -> Case:

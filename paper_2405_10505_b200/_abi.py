@@ -84,6 +84,7 @@ _lib_profile = _sig("fblts_profile", C.c_int, _vp, C.c_int32, _f64p, C.POINTER(C
 _lib_kname = _sig("fblts_kernel_name", C.c_char_p, C.c_int32)
 _lib_last_error = _sig("fblts_last_error", C.c_char_p, _vp)
 _lib_build_info = _sig("fblts_build_info", C.c_char_p)
+_lib_set_part = _sig("fblts_set_partition", C.c_int, _vp, C.POINTER(C.c_int32), C.POINTER(C.c_int64))
 _lib_diag_pv = _sig("fblts_diagnostics_pv", C.c_int, _vp, _f64p)
 _lib_set_vort = _sig("fblts_set_vorticity", C.c_int, _vp, _f64p)
 _lib_get_vort = _sig("fblts_get_vorticity", C.c_int, _vp, _f64p)
@@ -99,7 +100,7 @@ EXPORTED = ["fblts_create", "fblts_upload_mesh", "fblts_set_regions", "fblts_get
             "fblts_set_forcing", "fblts_set_hurricane", "fblts_set_state", "fblts_step", "fblts_step_group", "fblts_diagnostics_group",
             "fblts_sync", "fblts_get_state", "fblts_diagnostics", "fblts_diagnostics_async", "fblts_diagnostics_mass",
             "fblts_profile",
-            "fblts_kernel_name", "fblts_build_info", "fblts_set_vorticity", "fblts_get_vorticity", "fblts_diagnostics_pv",
+            "fblts_kernel_name", "fblts_build_info", "fblts_set_vorticity", "fblts_get_vorticity", "fblts_diagnostics_pv", "fblts_set_partition",
             "fblts_last_error", "fblts_destroy"]
 
 
@@ -157,6 +158,15 @@ def fblts_set_regions(ctx, fine_mask):
     a = _arr(fine_mask, np.uint8)
     _check_len(a, _sizes(ctx)[0], "fine_mask")
     _check(ctx, _lib_regions(ctx, _ptr(a, C.c_uint8)))
+
+
+def fblts_set_partition(ctx, owner, cell_gid):
+    """Distributed set-up: the uploaded mesh is this rank's piece; owner / cell_gid per piece cell."""
+    o, g = _arr(owner, np.int32), _arr(cell_gid, np.int64)
+    nC = _sizes(ctx)[0]
+    _check_len(o, nC, "owner")
+    _check_len(g, nC, "cell_gid")
+    _check(ctx, _lib_set_part(ctx, _ptr(o, C.c_int32), _ptr(g, C.c_int64)))
 
 
 def fblts_get_labels(ctx, nCells, nEdges):

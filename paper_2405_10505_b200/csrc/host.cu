@@ -75,6 +75,11 @@ struct fblts_ctx {
     bool band_side = true;
     std::string err;
     int phase = P_CREATED;
+    // fblts_set_partition: the uploaded mesh is this rank's PIECE of a larger mesh (its owned cells plus
+    // a margin), ext_part[i] = owning rank of piece cell i, gid[i] = its id in the whole mesh
+    bool piece = false;
+    std::vector<int32_t> ext_part;
+    std::vector<int64_t> gid;
     HostMesh hm;
     Region rg;
     Local lo;
@@ -761,7 +766,7 @@ int build_local(fblts_ctx *c, const std::vector<int32_t> &coc) {
     Local &L = c->lo;
     const int R = c->cfg.nranks, me = c->cfg.rank;
     const std::vector<uint64_t> key = sfc_keys(m);
-    const std::vector<int32_t> part = partition(m, g, key, R);
+    const std::vector<int32_t> part = c->piece ? c->ext_part : partition(m, g, key, R);
     const std::vector<int8_t> dme = dist_from(m, coc, part, me);
     // ---- cells: owned (region-major, SFC) then halo rings 1-2 (region-major, ring, SFC)
     std::vector<int32_t> own, halo;
@@ -987,12 +992,22 @@ int build_local(fblts_ctx *c, const std::vector<int32_t> &coc) {
                 if (dp[a] >= 1 && dp[b] >= 1 && std::min(dp[a], dp[b]) == 1) sendG[X_E][p].push_back(o);
             }
         }
+        // both sides order a list by the entities' ids in the WHOLE mesh: the index itself for a global
+        // upload; for pieces the cell's gid and, for an edge, the pair (min gid, max gid) of its cells
+        // (two cells share at most one edge), so every rank derives the same order from its own piece
+        auto ckey = [&](int i) -> int64_t { return c->piece ? c->gid[i] : (int64_t)i; };
+        auto ekey = [&](int e) -> int64_t {
+            if (!c->piece) return (int64_t)e;
+            const int64_t a = c->gid[m.coe[2 * e]], b = c->gid[m.coe[2 * e + 1]];
+            return (std::min(a, b) << 32) | std::max(a, b);
+        };
         for (int x = 0; x < X_NUM; ++x) {
             const std::vector<int32_t> &loc = x == X_E ? edgeLoc : cellLoc;
             Xchg &X = L.x[x];
             for (int p = 0; p < R; ++p) {
-                std::sort(sendG[x][p].begin(), sendG[x][p].end());
-                std::sort(recvG[x][p].begin(), recvG[x][p].end());
+                auto by = [&](int a, int b) { return x == X_E ? ekey(a) < ekey(b) : ckey(a) < ckey(b); };
+                std::sort(sendG[x][p].begin(), sendG[x][p].end(), by);
+                std::sort(recvG[x][p].begin(), recvG[x][p].end(), by);
                 for (int gid : sendG[x][p]) X.sendIdx.push_back(loc[gid]);
                 for (int gid : recvG[x][p]) X.recvIdx.push_back(loc[gid]);
                 X.sendOff[p + 1] = (int64_t)X.sendIdx.size();
@@ -1106,10 +1121,42 @@ int fblts_get_halo(fblts_ctx *c, int32_t which, int32_t peer, int64_t *n_send, i
     const int64_t s0 = X.sendOff[peer], s1 = X.sendOff[peer + 1], r0 = X.recvOff[peer], r1 = X.recvOff[peer + 1];
     if (n_send) *n_send = s1 - s0;
     if (n_recv) *n_recv = r1 - r0;
+    // ids in the whole mesh: the uploaded index, or with fblts_set_partition the cell gid and for an
+    // edge the key (min gid << 32) | max gid of its two cells
+    auto id = [&](int32_t loc) -> int64_t {
+        const int o = glob[loc];
+        if (!c->piece) return o;
+        if (which != X_E) return c->gid[o];
+        const int64_t a = c->gid[c->hm.coe[2 * o]], b = c->gid[c->hm.coe[2 * o + 1]];
+        return (std::min(a, b) << 32) | std::max(a, b);
+    };
     if (send_ids)
-        for (int64_t k = s0; k < s1; ++k) send_ids[k - s0] = glob[X.sendIdx[k]];
+        for (int64_t k = s0; k < s1; ++k) send_ids[k - s0] = id(X.sendIdx[k]);
     if (recv_ids)
-        for (int64_t k = r0; k < r1; ++k) recv_ids[k - r0] = glob[X.recvIdx[k]];
+        for (int64_t k = r0; k < r1; ++k) recv_ids[k - r0] = id(X.recvIdx[k]);
+    return FBLTS_OK;
+}
+
+int fblts_set_partition(fblts_ctx *c, const int32_t *owner, const int64_t *cell_gid) {
+    if (!c || !owner || !cell_gid) return FBLTS_ERR_INVALID_ARG;
+    if (c->phase != P_MESH) return fail(c, FBLTS_ERR_ORDER, "set_partition: after upload_mesh, before set_regions");
+    const int nC = c->hm.nC, R = c->cfg.nranks;
+    std::vector<int32_t> part(owner, owner + nC);
+    std::vector<int64_t> g(cell_gid, cell_gid + nC);
+    int64_t mine = 0;
+    for (int i = 0; i < nC; ++i) {
+        if (part[i] < 0 || part[i] >= R) return fail(c, FBLTS_ERR_INVALID_ARG, "set_partition: owner[%d]=%d", i, part[i]);
+        if (g[i] < 0 || g[i] >= ((int64_t)1 << 31)) return fail(c, FBLTS_ERR_INVALID_ARG, "set_partition: gid[%d] out of range", i);
+        mine += part[i] == c->cfg.rank;
+    }
+    if (mine == 0) return fail(c, FBLTS_ERR_INVALID_ARG, "set_partition: rank %d owns no cell of its piece", c->cfg.rank);
+    std::vector<int64_t> sorted(g);
+    std::sort(sorted.begin(), sorted.end());
+    for (int i = 1; i < nC; ++i)
+        if (sorted[i] == sorted[i - 1]) return fail(c, FBLTS_ERR_INVALID_ARG, "set_partition: gid %lld repeated", (long long)sorted[i]);
+    c->ext_part.swap(part);
+    c->gid.swap(g);
+    c->piece = true;
     return FBLTS_OK;
 }
 

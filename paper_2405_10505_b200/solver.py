@@ -21,7 +21,8 @@ from . import _abi as abi
 class Solver:
     def __init__(self, mesh, fine_mask, dt, M, *, g=9.81, beta=(0.531, 0.531, 0.313), rho0=1000.0, r=2,
                  slow=True, tau_n=None, device=None, stream=None, rank=0, nranks=1, nccl_id=None, scheme="fblts",
-                 slow_refresh=False, hurricane=None, unsplit=False, pv="centered", vorticity=False):
+                 slow_refresh=False, hurricane=None, unsplit=False, pv="centered", vorticity=False,
+                 partition=None):
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2405_10505_b200.Solver needs a CUDA device (no CPU fallback)")
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
@@ -35,6 +36,8 @@ class Solver:
         self.rank, self.nranks = rank, nranks
         try:
             abi.fblts_upload_mesh(self.ctx, mesh)
+            if partition is not None:          # (owner, gid): `mesh` is this rank's piece (fblts_set_partition)
+                abi.fblts_set_partition(self.ctx, partition[0], partition[1])
             abi.fblts_set_regions(self.ctx, fine_mask)
             nbytes = abi.fblts_workspace_size(self.ctx)
             self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
@@ -136,6 +139,17 @@ class SolverGroup:
     def __init__(self, mesh, fine_mask, dt, M, nranks, **kw):
         self.solvers = [Solver(mesh, fine_mask, dt, M, rank=r, nranks=nranks, **kw) for r in range(nranks)]
         self.nCells, self.nEdges = int(mesh.nCells), int(mesh.nEdges)
+
+    @classmethod
+    def from_pieces(cls, pieces, dt, M, **kw):
+        """Rank r's context from its own piece (inputs.configs.Piece: mesh, fine mask, owner, gid) --
+        the distributed set-up of fblts_set_partition, exercised in one process.  State I/O per rank."""
+        g = cls.__new__(cls)
+        n = len(pieces)
+        g.solvers = [Solver(p.case.mesh, p.case.fine_mask, dt, M, rank=r, nranks=n, partition=(p.owner, p.gid), **kw)
+                     for r, p in enumerate(pieces)]
+        g.nCells = g.nEdges = None
+        return g
 
     def set_state(self, h, u, t=0.0):
         for s in self.solvers:

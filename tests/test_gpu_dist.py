@@ -78,3 +78,36 @@ def test_group_on_sphere(mods):
     h, u, _ = g.state()
     assert np.array_equal(h, h1) and np.array_equal(u, u1)
     g.close()
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 4])
+def test_weak_pieces_reproduce_the_block(mods, nranks):
+    """Weak scaling's distributed set-up (reading Q25; fblts_set_partition): nranks ranks each build
+    ONLY their piece of the config-5 recipe stacked nranks times in y (inputs.configs.config5_weak_piece)
+    and step together through the loopback group.  The whole mesh is periodic with the block, so every
+    rank's owned rows must equal the one-rank run of the block itself bit for bit -- the weak-scaled
+    multi-GPU path computes exactly config 5's arithmetic on every GPU."""
+    Solver, SolverGroup = mods
+    nx = ny = 128
+    n = 6
+    blk = configs.config5_weak_piece(0, 1, nx=nx, ny=ny).case
+    h1, u1, _ = single(Solver, blk, n)
+    pieces = [configs.config5_weak_piece(r, nranks, nx=nx, ny=ny) for r in range(nranks)]
+    c0 = pieces[0].case
+    g = SolverGroup.from_pieces(pieces, c0.dt, c0.M, g=c0.g, beta=c0.beta, rho0=c0.rho0, slow=c0.slow,
+                                tau_n=c0.tau_n)
+    for s, p in zip(g.solvers, pieces):
+        s.set_state(p.case.h0, p.case.u0)
+    g.step(n)
+    for s, p in zip(g.solvers, pieces):
+        h = np.full(p.case.mesh.nCells, np.nan)
+        u = np.full(p.case.mesh.nEdges, np.nan)
+        s.state(h, u)
+        assert np.array_equal(h[p.own], h1[p.block_cell[p.own]])
+        # edges 3c+k belong to cell c in the lattice numbering: the owned cells' edges
+        e = (3 * p.own[:, None] + np.arange(3)[None, :]).ravel()
+        eb = (3 * p.block_cell[p.own][:, None] + np.arange(3)[None, :]).ravel()
+        assert np.array_equal(u[e], u1[eb])
+    d = g.diagnostics()
+    assert np.isfinite(d).all()
+    g.close()
