@@ -4,6 +4,7 @@
 // replay with NCCL halo exchanges, state I/O and diagnostics.
 #include <algorithm>
 #include <cmath>
+#include <nvtx3/nvToolsExt.h>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -188,6 +189,10 @@ uint64_t spread3(uint64_t v) {
 
 std::vector<uint64_t> sfc_keys(const HostMesh &m) {
     std::vector<uint64_t> key(m.nC);
+    // spherical meshes: 3-D Morton (default) or Hilbert per cube face (FBLTS_SFC=hilbert_face); the order
+    // changes only the layout, never the arithmetic (every per-cell sum keeps its slot order)
+    const char *sfc = std::getenv("FBLTS_SFC");
+    const bool sphere_hilbert = sfc && std::string(sfc) == "hilbert_face";
     bool planar = true;
     for (int i = 0; i < m.nC && planar; ++i) planar = m.z[i] == 0.0;
     auto q = [](double v, double lo, double hi, double n) {
@@ -206,6 +211,19 @@ std::vector<uint64_t> sfc_keys(const HostMesh &m) {
     for (int i = 0; i < m.nC; ++i) {
         if (planar) {
             key[i] = hilbert2(q(m.x[i], lo[0], hi[0], 65536.0), q(m.y[i], lo[1], hi[1], 65536.0), 16);
+        } else if (sphere_hilbert) {
+            // Hilbert curve per cube face: the face of the largest |coordinate|, the other two
+            // coordinates projected gnomonically to [-1, 1], a 2^20-grid Hilbert index inside the face;
+            // faces concatenated in the order +x, +y, -x, -y, +z, -z
+            const double p[3] = {m.x[i], m.y[i], m.z[i]};
+            int a = 0;
+            for (int k = 1; k < 3; ++k)
+                if (std::fabs(p[k]) > std::fabs(p[a])) a = k;
+            const bool neg = p[a] < 0.0;
+            const int face = a == 2 ? (neg ? 5 : 4) : (neg ? 2 + a : a);
+            const double w = std::fabs(p[a]);
+            const double pu = p[(a + 1) % 3] / w, pv = p[(a + 2) % 3] / w;
+            key[i] = (uint64_t)face << 40 | hilbert2(q(pu, -1.0, 1.0, 1048576.0), q(pv, -1.0, 1.0, 1048576.0), 20);
         } else {
             key[i] = spread3(q(m.x[i], lo[0], hi[0], 2097152.0)) | spread3(q(m.y[i], lo[1], hi[1], 2097152.0)) << 1 |
                      spread3(q(m.z[i], lo[2], hi[2], 2097152.0)) << 2;
@@ -1513,15 +1531,24 @@ int fblts_set_vorticity(fblts_ctx *c, const double *eta) {
 
 namespace {
 
+// Instrumented replay (fblts_profile): an event at every kernel-kind boundary, and an NVTX range per
+// kernel kind (named as in fblts_kernel_name) around its enqueues, for nsys / ncu range filtering.
 struct Recorder {
     std::vector<cudaEvent_t> ev;
     std::vector<int> kind;
+    bool open = false;
     void mark(int k, cudaStream_t s) {
         cudaEvent_t a;
         cudaEventCreate(&a);
         cudaEventRecord(a, s);
         ev.push_back(a);
         kind.push_back(k);
+        if (open) nvtxRangePop();
+        open = k >= 0;
+        if (open) nvtxRangePushA(kKernelNames[k]);
+    }
+    ~Recorder() {
+        if (open) nvtxRangePop();
     }
 };
 
@@ -2076,12 +2103,18 @@ int fblts_step(fblts_ctx *c, int32_t n) {
             const int rc = capture(c, p);
             if (rc) return rc;
         }
+    nvtxRangePushA("fblts_step");           // one NVTX range per call (n graph replays, one per coarse step)
     for (int i = 0; i < n; ++i) {
         diag_wait(c, 1 - c->parity);
-        CUDA_TRY(c, cudaGraphLaunch(c->exec[c->parity], c->stream));
+        const cudaError_t e = cudaGraphLaunch(c->exec[c->parity], c->stream);
+        if (e != cudaSuccess) {
+            nvtxRangePop();
+            return fail(c, FBLTS_ERR_CUDA, "cudaGraphLaunch: %s", cudaGetErrorString(e));
+        }
         c->parity ^= 1;
         c->t += c->cfg.dt;
     }
+    nvtxRangePop();
     return FBLTS_OK;
 }
 

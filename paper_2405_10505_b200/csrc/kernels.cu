@@ -982,6 +982,51 @@ __device__ __forceinline__ DD dd_merge(DD a, DD b) {
     return r;
 }
 
+// Deterministic block reduction of the diagnostics record (mass and Gamma as double-double, min h, max
+// nu) with warp shuffles: a fixed shuffle-down tree inside each warp (lane i merges lane i + 16, 8, 4,
+// 2, 1), the per-warp results through shared memory, then the same tree in warp 0.  Result in thread 0.
+struct DiagRec {
+    DD mass, gam;
+    double hmin, numax;
+};
+__device__ __forceinline__ DiagRec diag_shfl(const DiagRec &a, int off) {
+    DiagRec b;
+    b.mass.hi = __shfl_down_sync(0xffffffffu, a.mass.hi, off);
+    b.mass.lo = __shfl_down_sync(0xffffffffu, a.mass.lo, off);
+    b.gam.hi = __shfl_down_sync(0xffffffffu, a.gam.hi, off);
+    b.gam.lo = __shfl_down_sync(0xffffffffu, a.gam.lo, off);
+    b.hmin = __shfl_down_sync(0xffffffffu, a.hmin, off);
+    b.numax = __shfl_down_sync(0xffffffffu, a.numax, off);
+    return b;
+}
+__device__ __forceinline__ void diag_merge(DiagRec &a, const DiagRec &b) {
+    a.mass = dd_merge(a.mass, b.mass);
+    a.gam = dd_merge(a.gam, b.gam);
+    a.hmin = fmin(a.hmin, b.hmin);
+    a.numax = fmax(a.numax, b.numax);
+}
+__device__ __forceinline__ DiagRec diag_block_reduce(DiagRec r) {
+    constexpr int NW = TPB / 32;
+    __shared__ DiagRec warp_part[NW];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const DiagRec o = diag_shfl(r, off);
+        if (lane < off) diag_merge(r, o);
+    }
+    if (lane == 0) warp_part[wid] = r;
+    __syncthreads();
+    if (wid == 0) {
+        r = lane < NW ? warp_part[lane] : DiagRec{{0.0, 0.0}, {0.0, 0.0}, (double)INFINITY, 0.0};
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const DiagRec o = diag_shfl(r, off);
+            if (lane < off) diag_merge(r, o);
+        }
+    }
+    return r;
+}
+
 
 // Diagnostics, pass 1: three roles by block range -- blocks [0, DIAG_RB) sum A_i h_i and min h over
 // the owned cells, [DIAG_RB, 2 DIAG_RB) the absolute circulation of the owned vertices, the rest the
@@ -1038,31 +1083,11 @@ __global__ void __launch_bounds__(TPB) k_diag_partial(DevMesh m, const double *_
             numax = fmax(numax, nu);
         }
     }
-    __shared__ double sh[6][TPB];
-    sh[0][threadIdx.x] = mass.hi;
-    sh[1][threadIdx.x] = mass.lo;
-    sh[2][threadIdx.x] = gam.hi;
-    sh[3][threadIdx.x] = gam.lo;
-    sh[4][threadIdx.x] = hmin;
-    sh[5][threadIdx.x] = numax;
-    __syncthreads();
-    for (int w = TPB / 2; w > 0; w >>= 1) {
-        if (threadIdx.x < w) {
-            const int o = threadIdx.x + w;
-            DD a{sh[0][threadIdx.x], sh[1][threadIdx.x]}, b{sh[0][o], sh[1][o]};
-            DD r = dd_merge(a, b);
-            sh[0][threadIdx.x] = r.hi;
-            sh[1][threadIdx.x] = r.lo;
-            DD c{sh[2][threadIdx.x], sh[3][threadIdx.x]}, d{sh[2][o], sh[3][o]};
-            DD r2 = dd_merge(c, d);
-            sh[2][threadIdx.x] = r2.hi;
-            sh[3][threadIdx.x] = r2.lo;
-            sh[4][threadIdx.x] = fmin(sh[4][threadIdx.x], sh[4][o]);
-            sh[5][threadIdx.x] = fmax(sh[5][threadIdx.x], sh[5][o]);
-        }
-        __syncthreads();
+    const DiagRec r = diag_block_reduce(DiagRec{mass, gam, hmin, numax});
+    if (threadIdx.x == 0) {
+        double *o = part + blockIdx.x * 6;
+        o[0] = r.mass.hi, o[1] = r.mass.lo, o[2] = r.gam.hi, o[3] = r.gam.lo, o[4] = r.hmin, o[5] = r.numax;
     }
-    if (threadIdx.x < 6) part[blockIdx.x * 6 + threadIdx.x] = sh[threadIdx.x][0];
 }
 
 // Pass 2 (one block): thread t merges the partials of blocks t, t + TPB, ... in order, then a fixed
@@ -1076,30 +1101,11 @@ __global__ void __launch_bounds__(TPB) k_diag_final(const double *__restrict__ p
         hmin = fmin(hmin, part[b * 6 + 4]);
         numax = fmax(numax, part[b * 6 + 5]);
     }
-    __shared__ double sh[6][TPB];
-    sh[0][threadIdx.x] = mass.hi;
-    sh[1][threadIdx.x] = mass.lo;
-    sh[2][threadIdx.x] = gam.hi;
-    sh[3][threadIdx.x] = gam.lo;
-    sh[4][threadIdx.x] = hmin;
-    sh[5][threadIdx.x] = numax;
-    __syncthreads();
-    for (int w = TPB / 2; w > 0; w >>= 1) {
-        if (threadIdx.x < w) {
-            const int o = threadIdx.x + w;
-            DD r = dd_merge(DD{sh[0][threadIdx.x], sh[1][threadIdx.x]}, DD{sh[0][o], sh[1][o]});
-            sh[0][threadIdx.x] = r.hi;
-            sh[1][threadIdx.x] = r.lo;
-            DD r2 = dd_merge(DD{sh[2][threadIdx.x], sh[3][threadIdx.x]}, DD{sh[2][o], sh[3][o]});
-            sh[2][threadIdx.x] = r2.hi;
-            sh[3][threadIdx.x] = r2.lo;
-            sh[4][threadIdx.x] = fmin(sh[4][threadIdx.x], sh[4][o]);
-            sh[5][threadIdx.x] = fmax(sh[5][threadIdx.x], sh[5][o]);
-        }
-        __syncthreads();
-    }
     // raw double-double parts: ranks are combined on the host in rank order
-    if (threadIdx.x < 6) out[threadIdx.x] = sh[threadIdx.x][0];
+    const DiagRec r = diag_block_reduce(DiagRec{mass, gam, hmin, numax});
+    if (threadIdx.x == 0) {
+        out[0] = r.mass.hi, out[1] = r.mass.lo, out[2] = r.gam.hi, out[3] = r.gam.lo, out[4] = r.hmin, out[5] = r.numax;
+    }
 }
 
 // ---------------------------------------------------------------- launchers
