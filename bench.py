@@ -122,6 +122,42 @@ def byte_model(counts, M, fused, sub=0, maxE=6, maxE2=10):
     return b
 
 
+def unsplit_byte_model(counts, M, maxE=6, maxE2=10):
+    """Algorithmic bytes PER STEP of each kernel kind of the unsplit FB-LTS step (SURVEY 8(f) N1;
+    host.cu enqueue_unsplit_step), with the split model's per-entity costs:
+    every velocity update is preceded by a slow sweep (slow_pre over the mesh -- or, for fine stages 1-2,
+    over the F_E stencil -- and slow_edge over the update's edge range); the thickness sweeps read the
+    stored stage velocity instead of recomputing it (cell row + h_prev, h_base, A, write; per edge U, l);
+    the view kernels write the HS / U views of the stage's stencil (8 B per cell and per edge each way)."""
+    C, E = counts["owned_cells"], counts["owned_edges"]
+    V = counts["nVertices"] * C // max(1, counts["nCells"])
+    cc, ec = counts["cells_by_region"], counts["edges_by_region"]
+    cells = lambda lo, hi: sum(cc[lo:hi + 1])
+    edges = lambda lo, hi: sum(ec[lo:hi + 1])
+    slotC = 4 + 4 * maxE + 4 * maxE
+    pre_full = V * (12 + 12 + 24 + 8 + 8) + C * (4 + 4 * maxE + 8 + 8) + E * (8 + 8 + 8 + 8)
+    fstencil = cells(2, 8) / max(1, C)                              # F u IF-1 share of the mesh
+    pre_fine = pre_full * fstencil
+    edge_b = 4 + 4 * maxE2 + 8 * maxE2 + 8 * 5 + 8 * 2              # slow_edge per edge (+ q, K, h gathers)
+    th = lambda n_c, n_e: n_c * (slotC + 8 * 4) + n_e * 16             # thickness sweep with stored U
+    vel = lambda n_e: n_e * (8 * 4 + 8) + n_e * 8                       # un_vel: coe, S, base, d, write (+ HS)
+    view = lambda n_c, n_e: (n_c + n_e) * 16
+    b = {}
+    yE = [edges(0, 6), edges(0, 4), edges(0, 2)]                       # Y1 = C_E u F^4_E, Y2, Y3
+    xC = [cells(0, 7), cells(0, 5), cells(0, 3)]                       # X1 = C u F^5, X2, X3
+    b["coarse_s1"], b["coarse_s2"], b["coarse_s3"] = (th(xC[q], yE[q]) for q in range(3))
+    b["slow_pre"] = 3 * pre_full + M * (2 * pre_fine + pre_full)
+    fE, ifE = edges(3, 8), edges(1, 8)
+    b["slow_edge"] = edge_b * (sum(yE) + M * (2 * fE + ifE))
+    b["coarse_vel"] = sum(vel(n) for n in yE)
+    b["fine_s1"] = M * (th(cells(3, 8), fE) + view(cells(1, 8), ifE))
+    b["fine_s2"] = M * (th(cells(3, 8), fE) + view(cells(1, 8), ifE))
+    b["fine_s3"] = M * (th(cells(1, 8), ifE) + 2 * view(cells(1, 8), ifE))
+    b["fine_vel"] = M * (2 * vel(fE) + vel(ifE))
+    b["correct_if"] = cells(1, 2) * 24 + edges(1, 2) * 24
+    return b
+
+
 def _finite(x):
     """JSON-safe copy: NaN / inf -> null."""
     if isinstance(x, dict):
@@ -359,8 +395,8 @@ def arm_native(args):
     sub = 5 if prof.get("fine_sub", (0.0, 0))[1] > 0 else 0
     sub = int(os.environ.get("FBLTS_SUB_LEVEL", sub)) if sub else 0
     bm = byte_model(counts, c.M, fused, sub)                # bytes per step per kind
-    if args.unsplit:                                        # different sweep structure: no per-kind byte model
-        bm = {k: float("nan") for k in bm}
+    if args.unsplit:                                        # the unsplit step's own sweep structure
+        bm = {**{k: float("nan") for k in bm}, **unsplit_byte_model(counts, c.M)}
     t_step = {k: tms / n_prof for k, (tms, n) in prof.items() if n}
     dom = max(t_step, key=lambda k: t_step[k])
     launches_dom = prof[dom][1] / n_prof
