@@ -271,6 +271,12 @@ int fblts_diagnostics_pv(fblts_ctx *ctx, double *out);
  * nranks > 1), CUDA. */
 int fblts_diagnostics_async(fblts_ctx *ctx, double *out);
 
+/* out[2] = { total mass, min h } of the state after the steps enqueued so far, WITHOUT synchronising: the
+ * cell part of fblts_diagnostics_async (same reduction and bits as fblts_diagnostics_mass), a per-step
+ * monitor that does not stall the step pipeline.  Same contract as fblts_diagnostics_async (one rank; out
+ * valid after the next synchronising call).  Errors: ORDER, CUDA. */
+int fblts_diagnostics_mass_async(fblts_ctx *ctx, double *out);
+
 /* Instrumented replay for the roofline: runs n_coarse steps WITHOUT the graph, with
  * CUDA events around every launch on cfg.stream; ms[k] = total device ms of kernel
  * kind k, launches[k] = launch count, for k < FBLTS_NUM_KERNELS.  Advances the state. */

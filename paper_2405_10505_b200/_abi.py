@@ -80,6 +80,7 @@ _lib_get_state = _sig("fblts_get_state", C.c_int, _vp, _f64p, _f64p, C.POINTER(C
 _lib_diag = _sig("fblts_diagnostics", C.c_int, _vp, _f64p)
 _lib_diag_async = _sig("fblts_diagnostics_async", C.c_int, _vp, _f64p)
 _lib_diag_mass = _sig("fblts_diagnostics_mass", C.c_int, _vp, _f64p)
+_lib_diag_mass_async = _sig("fblts_diagnostics_mass_async", C.c_int, _vp, _f64p)
 _lib_profile = _sig("fblts_profile", C.c_int, _vp, C.c_int32, _f64p, C.POINTER(C.c_int64))
 _lib_kname = _sig("fblts_kernel_name", C.c_char_p, C.c_int32)
 _lib_last_error = _sig("fblts_last_error", C.c_char_p, _vp)
@@ -100,7 +101,7 @@ EXPORTED = ["fblts_create", "fblts_upload_mesh", "fblts_set_regions", "fblts_get
             "fblts_set_forcing", "fblts_set_hurricane", "fblts_set_state", "fblts_step", "fblts_step_group", "fblts_diagnostics_group",
             "fblts_sync", "fblts_get_state", "fblts_diagnostics", "fblts_diagnostics_async", "fblts_diagnostics_mass",
             "fblts_profile",
-            "fblts_kernel_name", "fblts_build_info", "fblts_set_vorticity", "fblts_get_vorticity", "fblts_diagnostics_pv", "fblts_set_partition",
+            "fblts_kernel_name", "fblts_build_info", "fblts_set_vorticity", "fblts_get_vorticity", "fblts_diagnostics_pv", "fblts_set_partition", "fblts_diagnostics_mass_async",
             "fblts_last_error", "fblts_destroy"]
 
 
@@ -343,6 +344,15 @@ def fblts_diagnostics_async(ctx, out):
     if not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.size >= 4 and out.flags.c_contiguous):
         raise ValueError("diagnostics_async needs a contiguous float64 numpy array of 4")
     _check(ctx, _lib_diag_async(ctx, _ptr(out, C.c_double)))
+    return out
+
+
+def fblts_diagnostics_mass_async(ctx, out):
+    """Enqueue (mass, min h) of the current state; `out` (contiguous float64 numpy array of 2, kept alive by
+    the caller) holds them after the next synchronising call."""
+    if not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.size >= 2 and out.flags.c_contiguous):
+        raise ValueError("diagnostics_mass_async needs a contiguous float64 numpy array of 2")
+    _check(ctx, _lib_diag_mass_async(ctx, _ptr(out, C.c_double)))
     return out
 
 

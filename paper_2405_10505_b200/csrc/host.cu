@@ -107,6 +107,7 @@ struct fblts_ctx {
     struct DiagJob {
         const double *slot;
         double *out;
+        bool mass_only;            // out[2] = {mass, min h} instead of the four numbers
     } *djobs = nullptr;
     uint64_t ndiag = 0;
     unsigned char nccl_id[128]{};
@@ -2072,7 +2073,14 @@ void diag_wait(fblts_ctx *c, int b) {
 void diag_combine(const double *parts, int n, double out[4]);
 void CUDART_CB diag_host_fn(void *p) {
     const fblts_ctx::DiagJob *j = static_cast<const fblts_ctx::DiagJob *>(p);
-    diag_combine(j->slot, 1, j->out);
+    if (j->mass_only) {
+        double four[4];
+        diag_combine(j->slot, 1, four);
+        j->out[0] = four[0];
+        j->out[1] = four[2];
+    } else {
+        diag_combine(j->slot, 1, j->out);
+    }
 }
 
 void diag_combine(const double *parts, int n, double out[4]) {
@@ -2221,7 +2229,10 @@ int fblts_get_vorticity(fblts_ctx *c, double *eta) {
     return check_device_error(c);
 }
 
-int fblts_diagnostics_async(fblts_ctx *c, double *out) {
+static int diagnostics_async(fblts_ctx *c, double *out, bool mass_only);
+int fblts_diagnostics_async(fblts_ctx *c, double *out) { return diagnostics_async(c, out, false); }
+int fblts_diagnostics_mass_async(fblts_ctx *c, double *out) { return diagnostics_async(c, out, true); }
+static int diagnostics_async(fblts_ctx *c, double *out, bool mass_only) {
     if (!c || !out) return FBLTS_ERR_INVALID_ARG;
     if (c->phase != P_STATE) return fail(c, FBLTS_ERR_ORDER, "diagnostics_async: no state set");
     if (c->cfg.nranks > 1) return fail(c, FBLTS_ERR_ORDER, "diagnostics_async: one rank (use fblts_diagnostics)");
@@ -2239,13 +2250,13 @@ int fblts_diagnostics_async(fblts_ctx *c, double *out) {
     CUDA_TRY(c, cudaEventRecord(c->evHead, c->stream));                // the state the caller sees now
     CUDA_TRY(c, cudaStreamWaitEvent(c->dstream, c->evHead, 0));
     double *dout = c->ds.diagA + DIAG_BLOCKS * 6;
-    launch_diagnostics(c->dm, c->hbuf[b], c->ubuf[b], c->sc, c->ds.diagA, dout, c->dstream);
+    launch_diagnostics(c->dm, c->hbuf[b], c->ubuf[b], c->sc, c->ds.diagA, dout, c->dstream, mass_only);
     CUDA_TRY(c, cudaGetLastError());
     CUDA_TRY(c, cudaEventRecord(c->evDiag[b], c->dstream));
     c->diagPending[b] = true;
     double *hs = c->dhost + 6 * (size_t)slot;
     CUDA_TRY(c, cudaMemcpyAsync(hs, dout, 6 * sizeof(double), cudaMemcpyDeviceToHost, c->dstream));
-    c->djobs[slot] = fblts_ctx::DiagJob{hs, out};
+    c->djobs[slot] = fblts_ctx::DiagJob{hs, out, mass_only};
     CUDA_TRY(c, cudaLaunchHostFunc(c->dstream, diag_host_fn, &c->djobs[slot]));
     return FBLTS_OK;
 }

@@ -107,6 +107,13 @@ class Solver:
         """(total mass, min h) of the current state: the cell part of diagnostics(), same bits."""
         return abi.fblts_diagnostics_mass(self.ctx)
 
+    def diagnostics_mass_async(self):
+        """(mass, min h) of the current state without synchronising: valid after the next sync() / state()."""
+        out = np.full(2, np.nan)
+        self._pending.append(out)
+        abi.fblts_diagnostics_mass_async(self.ctx, out)
+        return out
+
     def diagnostics_async(self):
         """(mass, Gamma, min h, max nu) of the current state, filled in without synchronising: the
         returned array holds the values after the next sync() / state() / diagnostics()."""

@@ -593,6 +593,28 @@ def test_diagnostics_async_match_sync(Solver):
     assert np.all(np.isfinite(h))
 
 
+def test_diagnostics_mass_async_match_sync(Solver):
+    """fblts_diagnostics_mass_async (the bench's per-step monitor) gives, bit for bit, the (mass, min h)
+    fblts_diagnostics_mass gives for the state at the call, with later steps enqueued before any sync."""
+    c = configs.small_shelf(nx=48, ny=40, dt=25.0)
+    s = Solver(c.mesh, c.fine_mask, c.dt, c.M, g=c.g, beta=c.beta, rho0=c.rho0, tau_n=c.tau_n)
+    s.set_state(c.h0, c.u0)
+    want = [s.diagnostics_mass()]
+    for _ in range(8):
+        s.step(1)
+        want.append(s.diagnostics_mass())
+    s.set_state(c.h0, c.u0)
+    got = [s.diagnostics_mass_async()]
+    for _ in range(8):
+        s.step(1)
+        got.append(s.diagnostics_mass_async())
+    s.step(3)
+    s.sync()
+    for g_, w in zip(got, want):
+        assert np.array_equal(g_, w), (g_, w)
+    s.close()
+
+
 def test_diagnostics_mass_is_cell_part(Solver):
     """fblts_diagnostics_mass = (mass, min h) of fblts_diagnostics, bit for bit, and the oracle's."""
     c = configs.config1()
