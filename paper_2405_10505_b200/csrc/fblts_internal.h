@@ -43,8 +43,9 @@ struct Bounds {
 // individually copied halo / foreign entries.  Per local edge (in list order, no gap),
 //   ecl = (local cell of c1) << 16 | (local cell of c0),
 // and per cell a slot-major 16-bit slot table  row[j * strideRow + i] = neg << 15 | local edge
-// (TILE_SENT for j >= nEdgesOnCell).  info[t * TINFO + k], k = c0, h0, eo0, eo1, f0, l0 (offsets
-// into the cell range, halo list, edge range, foreign list and ecl); record t + 1 gives the ends.
+// (TILE_SENT for j >= nEdgesOnCell).  info[t * TINFO + k], k = c0, h0, eo0, eo1, f0, l0, g0, ge0
+// (offsets into the cell range, halo list, edge range, foreign list, ecl, cell ghosts, edge ghosts);
+// record t + 1 gives the ends.
 #ifndef FBLTS_TILE
 #define FBLTS_TILE 256
 #endif
@@ -63,6 +64,16 @@ struct TileMesh {
     const int32_t *__restrict__ fedge;      // foreign edges of all tiles
     const uint32_t *__restrict__ ecl;       // local-edge cell pairs of all tiles
     const uint16_t *__restrict__ row;       // [maxE][strideRow]
+    // ghosts (round 2): the values a tile needs from its halo cells / foreign edges that do not change
+    // during a step, stored per tile contiguously so that they arrive by bulk copies.  Tile t's halo cell
+    // q at ghost index info[t*TINFO+6] + q (the range starts at the parity of the tile's first cell),
+    // foreign edge q at info[t*TINFO+7] + q (parity of the owned run's end); gcidx / geidx give the
+    // source of every ghost slot (-1: padding).  Gz, Gl, Gd are filled at bind; S's ghosts per step.
+    const int32_t *__restrict__ gcidx;
+    const int32_t *__restrict__ geidx;
+    const double *__restrict__ Gz;
+    const double *__restrict__ Gl;
+    const double *__restrict__ Gd;
 };
 
 // Subcycle tiles (fused fine subcycle): the tiles of the deep fine region
@@ -204,7 +215,10 @@ struct StageArgs {
     int32_t kind, k;
     const double *h2 = nullptr;   // STAGE 4
     double *unew = nullptr;       // STAGE 4
+    const double *gS = nullptr;   // ghosts of S (TileMesh), filled before the launch
 };
+// dst[k] = idx[k] >= 0 ? src[idx[k]] : 0 for k in [k0, k1) (ghost fill)
+void launch_ghost_fill(const int32_t *idx, const double *src, double *dst, int k0, int k1, cudaStream_t s);
 // Fused fine subcycle k on the subcycle tiles (kernels.cu k_fine_sub): with vel (k >= 1) first
 //   u^{n,k}_e = u^{n,k-1}_e + dt/M (Phi^fast_e(h***) + S_e),  h*** = b3 h^{n,k} + (1-2b3) h2 + b3 h^{n,k-1}
 // on the edges of rings 0-2 (written on the owned run), else u^{n,k} = ubase; then the three

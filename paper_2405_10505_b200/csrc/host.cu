@@ -121,6 +121,12 @@ struct fblts_ctx {
     std::vector<uint32_t> t_ecl;
     std::vector<uint16_t> t_row;
     int t_sRow = 32, t_hmax = 0, t_emax = 0;
+    std::vector<int32_t> g_cidx, g_eidx;     // ghost slot sources (cells / edges), -1 = padding
+    double *GS = nullptr;                    // ghosts of S (per step)
+    int32_t *dGe = nullptr;                  // device copy of g_eidx
+    struct GhostKey { const double *src = nullptr; int k0 = 0, k1 = 0; int64_t epoch = -1; };
+    GhostKey gkS;                            // S ghost fill already enqueued in the current step
+    int64_t step_epoch = 0;
     size_t t_nHalo = 0, t_nFedge = 0, t_nEcl = 0;
     bool deep_runs_ok = false;
     int vminF = 0;
@@ -582,6 +588,30 @@ int build_tiles(fblts_ctx *c) {
     int32_t *rec = &c->t_info[(size_t)nT * TINFO];
     rec[0] = L.nOwnC, rec[1] = (int32_t)c->t_halo.size(), rec[4] = (int32_t)c->t_fedge.size();
     rec[5] = (int32_t)c->t_ecl.size();
+    // ghost layout: tile t's halo cells at [g0, g0 + nH) with g0 of the parity of its first cell, its
+    // foreign edges at [ge0, ge0 + nF) with ge0 of the parity of its owned run's end (the bulk copies'
+    // 16-byte alignment, kernels.cu issue_bulk); a padding slot may precede and follow each range
+    {
+        c->g_cidx.assign(1, -1);
+        c->g_eidx.assign(1, -1);
+        for (int t = 0; t < nT; ++t) {
+            int32_t *r = &c->t_info[(size_t)t * TINFO];
+            const int32_t *n = r + TINFO;
+            const int oc = r[0] & 1, pe = r[3] & 1;
+            if (((int)c->g_cidx.size() & 1) != oc) c->g_cidx.push_back(-1);
+            r[6] = (int32_t)c->g_cidx.size();
+            for (int q = r[1]; q < n[1]; ++q) c->g_cidx.push_back(c->t_halo[q]);
+            if (((int)c->g_eidx.size() & 1) != pe) c->g_eidx.push_back(-1);
+            r[7] = (int32_t)c->g_eidx.size();
+            for (int q = r[4]; q < n[4]; ++q) c->g_eidx.push_back(c->t_fedge[q]);
+        }
+        rec[6] = (int32_t)c->g_cidx.size();
+        rec[7] = (int32_t)c->g_eidx.size();
+        for (int k = 0; k < 3; ++k) {            // slack of the last ranges' even-length copies
+            c->g_cidx.push_back(-1);
+            c->g_eidx.push_back(-1);
+        }
+    }
     // the fused deep velocity + stage-1 sweep writes each deep edge from the tile whose owned run
     // holds it: usable only if those runs tile [eb.fl[1], eb.end) exactly
     {
@@ -1284,6 +1314,16 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
     put(tFedge, std::max<size_t>(1, c->t_nFedge));
     put(tEcl, std::max<size_t>(1, c->t_nEcl));
     put(tRow, (size_t)c->hm.maxE * c->t_sRow);
+    // ghost slots of the staged sweeps: sources, static ghosts (z_b, l_e, d_e), S's ghosts
+    const size_t nGc = std::max<size_t>(1, c->g_cidx.size()), nGe = std::max<size_t>(1, c->g_eidx.size());
+    int32_t *gCi, *gEi;
+    double *gz, *gl, *gd;
+    put(gCi, nGc);
+    put(gEi, nGe);
+    put(gz, nGc);
+    put(gl, nGe);
+    put(gd, nGe);
+    put(c->GS, nGe);
     const bool fs = c->fuse_sub;
     put(s.hT2, fs ? (size_t)L.nC : 1);
     put(s.h2alt, fs ? (size_t)L.nC : 1);
@@ -1309,6 +1349,8 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
         tm.hmax = c->t_hmax;
         tm.emax = c->t_emax;
         tm.info = tInfo, tm.halo = tHalo, tm.fedge = tFedge, tm.ecl = tEcl, tm.row = tRow;
+        tm.gcidx = gCi, tm.geidx = gEi, tm.Gz = gz, tm.Gl = gl, tm.Gd = gd;
+        c->dGe = gEi;
     }
     if (base) {
         d.nC = L.nC, d.nE = L.nE, d.nV = L.nV, d.nOwnC = L.nOwnC, d.nOwnE = L.nOwnE;
@@ -1396,6 +1438,12 @@ int fblts_bind_workspace(fblts_ctx *c, void *ptr, size_t bytes) {
     CUDA_TRY(c, up(tm.fedge, c->t_fedge.data(), c->t_fedge.size() * 4));
     CUDA_TRY(c, up(tm.ecl, c->t_ecl.data(), c->t_ecl.size() * 4));
     CUDA_TRY(c, up(tm.row, c->t_row.data(), c->t_row.size() * 2));
+    CUDA_TRY(c, up(tm.gcidx, c->g_cidx.data(), c->g_cidx.size() * 4));
+    CUDA_TRY(c, up(tm.geidx, c->g_eidx.data(), c->g_eidx.size() * 4));
+    launch_ghost_fill(tm.gcidx, d.zb, const_cast<double *>(tm.Gz), 0, (int)c->g_cidx.size(), s);   // static ghosts
+    launch_ghost_fill(tm.geidx, d.dv, const_cast<double *>(tm.Gl), 0, (int)c->g_eidx.size(), s);
+    launch_ghost_fill(tm.geidx, d.dc, const_cast<double *>(tm.Gd), 0, (int)c->g_eidx.size(), s);
+    CUDA_TRY(c, cudaGetLastError());
     if (c->fuse_sub) {
         const SubTileMesh &sm = d.st;
         CUDA_TRY(c, up(sm.info, c->s_info.data(), c->s_info.size() * 4));
@@ -1581,7 +1629,21 @@ void stage_tiled_run(fblts_ctx *c, int stage, int cbegin, int cend, const StageA
             return;
         }
     }
-    launch_stage_tiled(c->dm, stage, t0, t1, hmax, emax, c->nsm, a, c->ds.err, s);
+    StageArgs g = a;
+    g.gS = c->GS;
+    if (stage > 1) {   // S's ghosts: the frozen S changes once per step, so they are refilled only for a new
+                       // step or a launch range not yet covered (always for the refresh's S^k)
+        const int32_t *r0 = &c->t_info[(size_t)t0 * TINFO], *r1 = &c->t_info[(size_t)t1 * TINFO];
+        const int nGe = (int)c->g_eidx.size();
+        const int ge0 = std::max(0, r0[7] - 1), ge1 = std::min(nGe, r1[7] + 2);
+        fblts_ctx::GhostKey &k = c->gkS;
+        const bool frozen = a.S == c->ds.S;
+        if (!(frozen && k.src == a.S && k.epoch == c->step_epoch && k.k0 <= ge0 && ge1 <= k.k1)) {
+            launch_ghost_fill(c->dGe, a.S, c->GS, ge0, ge1, s);
+            k.src = frozen ? a.S : nullptr, k.epoch = c->step_epoch, k.k0 = ge0, k.k1 = ge1;
+        }
+    }
+    launch_stage_tiled(c->dm, stage, t0, t1, hmax, emax, c->nsm, g, c->ds.err, s);
 }
 // The thin interface blocks [IF-2 .. F^5] have long, narrow tiles (more halo cells and edges per
 // cell); with FBLTS_SPLIT=1 they get their own launch so that the bulk blocks (int, F\F^5) size
@@ -1604,6 +1666,7 @@ void stage_tiled(fblts_ctx *c, int stage, const Bounds &B, int cbegin, int cend,
 // exchange (PhaseX) reads only boundary-block cells, so with several ranks it runs between the
 // two parts, overlapped with part 1.
 bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec, PhaseX *px, int part) {
+    if (ph == 0 && part == 0) c->step_epoch++;      // the S ghost cache is per enqueued step
     const DevMesh &m = c->dm;
     DevState st = c->ds;
     const StepConst &sc = c->sc;

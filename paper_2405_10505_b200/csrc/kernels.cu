@@ -341,12 +341,12 @@ struct TileShape {
 };
 
 struct TileRec {
-    int c0, c1, h0, h1, eo0, eo1, f0, f1, l0;
+    int c0, c1, h0, h1, eo0, eo1, f0, f1, l0, g0, ge0;
 };
 __device__ __forceinline__ TileRec load_rec(const TileMesh &t, int tile) {
     const int *p = t.info + (size_t)tile * TINFO;
     TileRec r;
-    r.c0 = p[0], r.h0 = p[1], r.eo0 = p[2], r.eo1 = p[3], r.f0 = p[4], r.l0 = p[5];
+    r.c0 = p[0], r.h0 = p[1], r.eo0 = p[2], r.eo1 = p[3], r.f0 = p[4], r.l0 = p[5], r.g0 = p[6], r.ge0 = p[7];
     r.c1 = p[TINFO + 0], r.h1 = p[TINFO + 1], r.f1 = p[TINFO + 4];
     return r;
 }
@@ -377,14 +377,24 @@ __device__ __forceinline__ void issue_bulk(const DevMesh &m, const StageArgs &a,
     const int nLE = r.eo1 - r.eo0 + r.f1 - r.f0;
     const int la = r.l0 & ~3, lb = (r.l0 + nLE + 3) & ~3;
     const unsigned cbytes = 8u * (cb - ca), ebytes = 8u * (eb - ea), lbytes = 4u * (lb - la);
+    // ghosts (TileMesh): the halo cells' z_b and the foreign edges' l_e, d_e, S -- values that do not change
+    // during a step -- stored per tile contiguously, so they arrive by bulk copies: halo cell q lands at
+    // local HALO0 + q, foreign edge q at nOE + FGAP + q; each ghost range starts at the parity that makes
+    // source and destination 16-byte aligned (host layout) and is copied with an even length
+    const int oc = r.c0 & 1, pe = r.eo1 & 1;
+    const int nH = r.h1 - r.h0, nF = r.f1 - r.f0;
+    const int gs = r.g0 - oc, ges = r.ge0 - pe;
+    const unsigned hbytes = (STAGE > 1 && nH) ? 8u * ((nH + oc + 1) & ~1) : 0u;
+    const unsigned fbytes = nF ? 8u * ((nF + pe + 1) & ~1) : 0u;
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic writes of the last use first
-    mbar_expect_tx(bar, NCA * cbytes + (ebytes ? NEA * ebytes : 0u) + lbytes);
+    mbar_expect_tx(bar, NCA * cbytes + hbytes + (ebytes ? NEA * ebytes : 0u) + (NEA - 1) * fbytes + lbytes);
     bulk_g2s(B, a.hprev + ca, cbytes, bar);
     if (STAGE > 1) {
         bulk_g2s(B + CS2, a.hbase + ca, cbytes, bar);
         bulk_g2s(B + 2 * CS2, m.zb + ca, cbytes, bar);
     }
     if (STAGE == 4) bulk_g2s(B + 3 * CS2, a.h2 + ca, cbytes, bar);
+    if (hbytes) bulk_g2s(B + 2 * CS2 + HALO0, m.tm.Gz + gs, hbytes, bar);
     double *E = B + NCA * CS2;
     if (ebytes) {
         bulk_g2s(E, a.ubase + ea, ebytes, bar);
@@ -392,6 +402,14 @@ __device__ __forceinline__ void issue_bulk(const DevMesh &m, const StageArgs &a,
         if (STAGE > 1) {
             bulk_g2s(E + 2 * ES2, a.S + ea, ebytes, bar);
             bulk_g2s(E + 3 * ES2, m.dc + ea, ebytes, bar);
+        }
+    }
+    if (fbytes) {
+        const int fo = (r.eo0 & 1) + (r.eo1 - r.eo0) + FGAP - pe;      // even: eo0 + nOE has the parity of eo1
+        bulk_g2s(E + ES2 + fo, m.tm.Gl + ges, fbytes, bar);
+        if (STAGE > 1) {
+            bulk_g2s(E + 2 * ES2 + fo, a.gS + ges, fbytes, bar);
+            bulk_g2s(E + 3 * ES2 + fo, m.tm.Gd + ges, fbytes, bar);
         }
     }
     bulk_g2s(E + NEA * ES2, m.tm.ecl + la, lbytes, bar);
@@ -402,22 +420,12 @@ __device__ __forceinline__ void issue_indexed(const DevMesh &m, const StageArgs 
                                               const TileBuf<STAGE> &b, int tid, const int (&hx)[HPT],
                                               const int (&fx)[FPT]) {
     const int nH = r.h1 - r.h0, nF = r.f1 - r.f0, nOE = r.eo1 - r.eo0;
-    auto halo = [&](int q, int x) {
+    auto halo = [&](int q, int x) {                       // the values that change during a step
         cp_async8(b.hp + HALO0 + q, a.hprev + x);
-        if (STAGE > 1) {
-            cp_async8(b.hb + HALO0 + q, a.hbase + x);
-            cp_async8(b.z + HALO0 + q, m.zb + x);
-        }
+        if (STAGE > 1) cp_async8(b.hb + HALO0 + q, a.hbase + x);
         if (STAGE == 4) cp_async8(b.h2 + HALO0 + q, a.h2 + x);
     };
-    auto foreign = [&](int p, int e) {
-        cp_async8(b.u + p, a.ubase + e);
-        cp_async8(b.l + p, m.dv + e);
-        if (STAGE > 1) {
-            cp_async8(b.S + p, a.S + e);
-            cp_async8(b.d + p, m.dc + e);
-        }
-    };
+    auto foreign = [&](int p, int e) { cp_async8(b.u + p, a.ubase + e); };
 #pragma unroll
     for (int k = 0; k < HPT; ++k)
         if (k * NTHR + tid < nH) halo(k * NTHR + tid, hx[k]);
@@ -1126,7 +1134,7 @@ __global__ void __launch_bounds__(TPB) k_diag_final(const double *__restrict__ p
 
 // strides of one shared tile buffer (elements, 16-byte multiples) and the dynamic smem bytes
 static void tile_strides(int hmax, int emax, int &CS2, int &ES2) {
-    CS2 = (HALO0 + hmax + 1 + 1) & ~1;     // + alignment offset, rounded to an even count
+    CS2 = (HALO0 + hmax + 3 + 1) & ~1;     // + alignment offsets and the ghost copy's slack, even
     ES2 = (emax + FGAP + 8 + 3) & ~3;       // + gap and slack; multiple of 4 (the uint32 pair array)
 }
 int stage_tiled_smem_bytes_host(int stage, int hmax, int emax) {
@@ -1838,6 +1846,18 @@ void launch_un_fstage(const DevMesh &m, const DevState &st, int stage, const dou
         else
             k_un_fstage<G, 3><<<nblocks(end - b0), TPB, 0, s>>>(m, a, U, out, st.accH, sc, pc, k, b0, end, st.err);
     });
+}
+
+// ghost fill (staged stage sweeps): dst[k] = src[idx[k]] (0 for padding slots), k in [k0, k1)
+__global__ void k_ghost_fill(const int32_t *__restrict__ idx, const double *__restrict__ src,
+                             double *__restrict__ dst, int k0, int k1) {
+    const int k = k0 + blockIdx.x * TPB + threadIdx.x;
+    if (k >= k1) return;
+    const int i = idx[k];
+    dst[k] = i >= 0 ? src[i] : 0.0;
+}
+void launch_ghost_fill(const int32_t *idx, const double *src, double *dst, int k0, int k1, cudaStream_t s) {
+    if (k1 > k0) k_ghost_fill<<<nblocks(k1 - k0), TPB, 0, s>>>(idx, src, dst, k0, k1);
 }
 
 // ---------------------------------------------------------------- prognostic absolute vorticity (N1)
