@@ -258,43 +258,6 @@ def test_sphere_with_fine_region(Solver):
     assert_parity(hg, ug, ho, uo)
 
 
-def _host_ram_gb():
-    try:
-        with open("/proc/meminfo") as f:
-            for line in f:
-                if line.startswith("MemAvailable:"):
-                    return int(line.split()[1]) / 2**20
-    except OSError:
-        pass
-    return 0.0
-
-
-def test_parity_config5_full_size(Solver):
-    """BASELINE config 5 -- the bench workload -- at full size (16,777,216 cells, 50,331,648 edges),
-    in bench.py's launch configuration (one rank, tiled stage kernels, CUDA-graph replay): one
-    coarse step (M = 4: slow terms, 3 coarse stages, 12 fine stages, 4 fine velocity sweeps, the
-    interface correction) compared element by element with the oracle, then 10 more steps checked
-    for conservation (Theorems 1-2) at full size."""
-    if _host_ram_gb() < 48:
-        pytest.skip("the full-size oracle step needs ~40 GB of host memory")
-    c = configs.config5()
-    ho, uo, lab = run_oracle(c, 1)
-    s, hg, ug, _ = run_gpu(Solver, c, 1)
-    eh, eu = assert_parity(hg, ug, ho, uo)
-    print(f"config5 full size, 1 step: eps_h={eh:.3e} eps_u={eu:.3e} bitwise={np.array_equal(hg, ho) and np.array_equal(ug, uo)}")
-    assert np.array_equal(hg, ho) and np.array_equal(ug, uo), "not bitwise (canonical arithmetic, --fmad=false)"
-    del ho, uo
-    d0 = s.diagnostics()
-    ref = dg.diagnostics(c.mesh, lab, hg, ug, c.dt, c.M, c.g)
-    assert d0[0] == pytest.approx(ref[0], rel=1e-15)
-    s.step(10)
-    d1 = s.diagnostics()
-    assert abs(d1[0] - d0[0]) <= DRIFT * d0[0]
-    fscale = float(np.sum(c.mesh.areaTriangle * np.abs(c.mesh.fVertex)))
-    assert abs(d1[1] - d0[1]) <= DRIFT * fscale
-    s.close()
-
-
 def test_parity_config4_reduced_100_steps(Solver):
     """Config-4 recipe (variable-resolution SCVT sphere, shelf disk, M = 8, full Coriolis) at
     dx_scale = 8 (~12 k cells, maxEdges 8), 100 coarse steps element by element."""
