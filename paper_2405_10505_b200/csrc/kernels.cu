@@ -334,6 +334,16 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
                  : "memory");
 }
 
+// FBLTS_CHECK=1 (debug builds): device-side bounds checks of every shared-memory index the staged
+// kernel derives from its tile tables; a violation traps (the launch fails with a CUDA error)
+#ifndef FBLTS_CHECK
+#define FBLTS_CHECK 0
+#endif
+#define FBLTS_REQUIRE(cond)                  \
+    do {                                     \
+        if (FBLTS_CHECK && !(cond)) __trap(); \
+    } while (0)
+
 template <int STAGE>
 struct TileShape {
     static constexpr int NCA = STAGE == 4 ? 4 : (STAGE > 1 ? 3 : 1);   // cell arrays: hprev (, hbase, z_b (, h2))
@@ -394,6 +404,7 @@ __device__ __forceinline__ void issue_bulk(const DevMesh &m, const StageArgs &a,
         bulk_g2s(B + 2 * CS2, m.zb + ca, cbytes, bar);
     }
     if (STAGE == 4) bulk_g2s(B + 3 * CS2, a.h2 + ca, cbytes, bar);
+    FBLTS_REQUIRE(gs >= 0 && HALO0 + (int)(hbytes / 8u) <= CS2);
     if (hbytes) bulk_g2s(B + 2 * CS2 + HALO0, m.tm.Gz + gs, hbytes, bar);
     double *E = B + NCA * CS2;
     if (ebytes) {
@@ -406,6 +417,7 @@ __device__ __forceinline__ void issue_bulk(const DevMesh &m, const StageArgs &a,
     }
     if (fbytes) {
         const int fo = (r.eo0 & 1) + (r.eo1 - r.eo0) + FGAP - pe;      // even: eo0 + nOE has the parity of eo1
+        FBLTS_REQUIRE(ges >= 0 && (fo & 1) == 0 && fo + (int)(fbytes / 8u) <= ES2);
         bulk_g2s(E + ES2 + fo, m.tm.Gl + ges, fbytes, bar);
         if (STAGE > 1) {
             bulk_g2s(E + 2 * ES2 + fo, a.gS + ges, fbytes, bar);
@@ -449,15 +461,6 @@ __device__ __forceinline__ void load_indices(const TileMesh &t, const TileRec &r
     }
 }
 
-// FBLTS_CHECK=1 (debug builds): device-side bounds checks of every shared-memory index the staged
-// kernel derives from its tile tables; a violation traps (the launch fails with a CUDA error)
-#ifndef FBLTS_CHECK
-#define FBLTS_CHECK 0
-#endif
-#define FBLTS_REQUIRE(cond)                  \
-    do {                                     \
-        if (FBLTS_CHECK && !(cond)) __trap(); \
-    } while (0)
 // development probes were removed (round 2); FBLTS_PROBE stays 0 and is reported by fblts_build_info
 #ifndef FBLTS_PROBE
 #define FBLTS_PROBE 0
