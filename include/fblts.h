@@ -133,8 +133,9 @@ typedef struct {
                             (Theorem 2; SPEC step_prognostic_vorticity S:L472-480): the PV-flux
                             term q_hat_e F_perp_e of every velocity update, integrated per edge as the velocity
                             integrates it (int_E: dt PV of coarse stage 3; F_E: sum_k dt/M PV^k; IF edges:
-                            dt/M sum_k PV^k), gives eta_v += (sum_j t_{e_j,v} d_{e_j} dP_{e_j}) / A_v.  Needs
-                            unsplit = 1 and one rank; set / read with fblts_set_vorticity / fblts_get_vorticity */
+                            dt/M sum_k PV^k), gives eta_v += (sum_j t_{e_j,v} d_{e_j} dP_{e_j}) / A_v; in split
+                            mode PV is the frozen one inside S.  One rank, FB-LTS scheme, no slow refresh;
+                            set / read with fblts_set_vorticity / fblts_get_vorticity */
 } fblts_config;
 
 #define FBLTS_SCHEME_FBLTS 0

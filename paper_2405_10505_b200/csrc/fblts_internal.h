@@ -251,6 +251,7 @@ void launch_vort_int(const DevState &st, double c3, int e1, cudaStream_t s);
 void launch_vort_fine(const DevMesh &m, const DevState &st, double c3f, int first, cudaStream_t s);
 void launch_vort_close(const DevMesh &m, const DevState &st, double c3f, cudaStream_t s);
 void launch_vort_update(const DevMesh &m, const DevState &st, cudaStream_t s);
+void launch_vort_split(const DevMesh &m, const DevState &st, const StepConst &sc, cudaStream_t s);
 // slow-term refresh views at t^{n,k} into st.hv (cells) and st.uv (edges)
 void launch_refresh_views(const DevMesh &m, const DevState &st, const double *hN, const double *hNew,
                           const double *hk, const double *uN, const double *uk, const StepConst &sc,

@@ -319,7 +319,8 @@ int fblts_create(fblts_ctx **out, const fblts_config *cfg) {
     if (cfg->unsplit && (cfg->nranks != 1 || cfg->scheme != FBLTS_SCHEME_FBLTS || cfg->slow_refresh))
         return FBLTS_ERR_INVALID_ARG;
     if (cfg->pv_energy && (cfg->nranks != 1 || cfg->slow_refresh)) return FBLTS_ERR_INVALID_ARG;
-    if (cfg->vorticity && (!cfg->unsplit || cfg->nranks != 1)) return FBLTS_ERR_INVALID_ARG;
+    if (cfg->vorticity && (cfg->nranks != 1 || cfg->slow_refresh || cfg->scheme != FBLTS_SCHEME_FBLTS))
+        return FBLTS_ERR_INVALID_ARG;
     // No CUDA call here: mesh upload, labelling and renumbering are host work, so a context
     // can be created (and its labels inspected) on a machine without a GPU.
     fblts_ctx *c = new fblts_ctx();
@@ -1728,8 +1729,10 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
             mark(K_SLOW_PRE);
             launch_slow_pre(m, st, hN, uN, s);
             mark(K_SLOW_EDGE);
-            launch_slow_edge(m, st, hN, uN, sc, s);
+            launch_slow_edge_range(m, st, hN, uN, st.S, 0, m.nOwnE, sc, s, c->cfg.vorticity ? st.Pv : nullptr);
             any = true;
+        } else if (part == 0 && c->cfg.vorticity) {
+            cudaMemsetAsync(st.Pv, 0, (size_t)std::max(1, m.nOwnE) * 8, s);   // gravity-wave model: no PV flux
         }
         cell_mark(K_COARSE_S1);
         if (T) stage_tiled(c, 1, B, B.begin, B.fl[5], StageArgs{hN, hN, uN, st.S, st.h1, 0, 0, 0, sc.c1, sc.g, K_COARSE_S1, -1}, s);
@@ -1851,6 +1854,10 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
             mark(K_COARSE_VEL);
             launch_coarse_vel(m, st, hN, uN, hNew, uNew, sc, s);
             any = true;
+        }
+        if (part == 0 && c->cfg.vorticity) {       // prognostic eta (Theorem 2), frozen PV flux
+            launch_vort_split(m, st, sc, s);
+            launch_vort_update(m, st, s);
         }
         *px = PhaseX{X_C2, hNew, X_E, uNew};
     }

@@ -1896,6 +1896,29 @@ __global__ void k_vort_update(DevMesh m, double *__restrict__ eta, const double 
     }
     eta[v] = eta[v] + acc / m.areaTri[v];
 }
+// split mode: the PV flux is frozen with S, so the per-edge integral is formed at the end of the step
+// in the oracle's operation order (F_E: ascending k, dP + dt/M PV; IF edges: dt/M (sum_k PV))
+__global__ void k_vort_split(double *__restrict__ dP, const double *__restrict__ P, double c3, double c3f, int M,
+                             int if2, int f, int end) {
+    const int e = blockIdx.x * TPB + threadIdx.x;
+    if (e >= end) return;
+    const double p = P[e];
+    if (e < if2) {
+        dP[e] = c3 * p;
+    } else if (e < f) {
+        double acc = 0.0;
+        for (int k = 0; k < M; ++k) acc = acc + p;
+        dP[e] = c3f * acc;
+    } else {
+        double acc = 0.0;
+        for (int k = 0; k < M; ++k) acc = acc + c3f * p;
+        dP[e] = acc;
+    }
+}
+void launch_vort_split(const DevMesh &m, const DevState &st, const StepConst &sc, cudaStream_t s) {
+    if (m.eb.end > 0)
+        k_vort_split<<<nblocks(m.eb.end), TPB, 0, s>>>(st.dP, st.Pv, sc.c3, sc.c3f, sc.M, m.eb.if2, m.eb.f, m.eb.end);
+}
 void launch_vort_int(const DevState &st, double c3, int e1, cudaStream_t s) {
     if (e1 > 0) k_vort_int<<<nblocks(e1), TPB, 0, s>>>(st.dP, st.Pv, c3, e1);
 }

@@ -444,9 +444,10 @@ def test_unsplit_matches_oracle(Solver, which, M):
     assert np.array_equal(hg, ho) and np.array_equal(ug, uo), "not bitwise (canonical arithmetic, --fmad=false)"
 
 
+@pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("which,M", [("config1", 4), ("shelf", 3), ("shelf", 1)])
-def test_vorticity_companion_theorem2(Solver, which, M):
-    """Prognostic absolute vorticity companion in unsplit mode (Theorem 2; SPEC
+def test_vorticity_companion_theorem2(Solver, which, M, split):
+    """Prognostic absolute vorticity companion, unsplit and split (Theorem 2; SPEC
     step_prognostic_vorticity): through the C ABI (cfg.vorticity) the eta the GPU
     advances -- the PV flux of every coarse / fine / correction velocity update, integrated per edge --
     equals the oracle's fblts_step(eta=...) bit for bit after 30 steps, and its total sum_v A_v eta_v
@@ -457,9 +458,9 @@ def test_vorticity_companion_theorem2(Solver, which, M):
     n = 30
     lab = lts.label_regions(m, c.fine_mask)
     eta0 = trisk.relative_vorticity(m, c.u0) + m.fVertex
-    ho, uo, eo = lts.run(m, lab, c.h0, c.u0, c.dt, M, phys_of(c), n, split=False, eta=eta0)
+    ho, uo, eo = lts.run(m, lab, c.h0, c.u0, c.dt, M, phys_of(c), n, split=split, eta=eta0)
     s = Solver(m, c.fine_mask, c.dt, M, g=c.g, beta=c.beta, rho0=c.rho0, slow=c.slow, tau_n=c.tau_n,
-               unsplit=True, vorticity=True)
+               unsplit=not split, vorticity=True)
     s.set_state(c.h0, c.u0)
     s.set_vorticity(eta0)
     s.step(n)
@@ -470,7 +471,7 @@ def test_vorticity_companion_theorem2(Solver, which, M):
     assert np.array_equal(eg, eo), float(np.max(np.abs(eg - eo)))
     scale = float(np.sum(m.areaTriangle * np.abs(eta0)))
     drift = abs(float(np.sum(m.areaTriangle * eg)) - float(np.sum(m.areaTriangle * eta0))) / scale
-    print(f"vorticity companion {which} M={M}: bitwise, Theorem-2 drift {drift:.2e}")
+    print(f"vorticity companion {which} M={M} split={split}: bitwise, Theorem-2 drift {drift:.2e}")
     assert drift <= 1e-13
     assert np.max(np.abs(eg - eta0)) > 0.0
 
