@@ -234,7 +234,8 @@ void launch_fine_sub(const DevMesh &m, bool vel, int nsm, const SubArgs &a, DevE
 
 void launch_stage_tiled(const DevMesh &m, int stage, int tile0, int tile1, int hmax, int emax, int nsm,
                         const StageArgs &a, DevError *err, cudaStream_t s);
-int stage_tiled_smem_bytes_host(int stage, int hmax, int emax);   // bytes for tiles with <= hmax / emax
+// bytes for tiles with <= hmax halo cells / emax local edges, and the records of nrec tiles per CTA
+int stage_tiled_smem_bytes_host(int stage, int hmax, int emax, int nrec = 0);
 int stage_tiled_configure(const DevMesh &m);      // sets the dynamic shared-memory limits (cudaError_t)
 
 // Kernel launchers (kernels.cu).  All enqueue on `s`.

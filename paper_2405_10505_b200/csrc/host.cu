@@ -1622,7 +1622,9 @@ void stage_tiled_run(fblts_ctx *c, int stage, int cbegin, int cend, const StageA
         hmax = std::max(hmax, n[1] - r[1]);
         emax = std::max(emax, r[3] - r[2] + n[4] - r[4]);
     }
-    if (stage_tiled_smem_bytes_host(stage, hmax, emax) > TILE_SMEM_MAX) {   // too large: halve the range
+    // records staged per CTA: at most ceil(tiles / nsm) (the grid is >= one CTA per SM, or one per tile)
+    const int nrec = std::max(1, (t1 - t0 + c->nsm - 1) / std::max(1, c->nsm));
+    if (stage_tiled_smem_bytes_host(stage, hmax, emax, nrec) > TILE_SMEM_MAX) {   // too large: halve the range
         if (t1 - t0 > 1) {
             const int mid = c->t_start[t0 + (t1 - t0) / 2];
             stage_tiled_run(c, stage, cbegin, mid, a, s);

@@ -43,7 +43,8 @@ constexpr int TPB = 256;
 #define FBLTS_TILE_NBUF 2
 #endif
 constexpr int NBUF = FBLTS_TILE_NBUF;   // tile buffers of the staged kernel's pipeline
-static_assert(NBUF == 2 || NBUF == 3, "k_stage_tiled pipelines 2 or 3 tile buffers");
+static_assert(NBUF == 2, "k_stage_tiled is a two-buffer pipeline (3 buffers measured slower)");
+constexpr int TREC = 16;                // ints per tile-record slot in shared memory (the record + the next one)
 #ifndef FBLTS_TILE_NTHR
 #define FBLTS_TILE_NTHR 256
 #endif
@@ -478,53 +479,63 @@ __global__ void __launch_bounds__(NTHR, FBLTS_TILE_MINB) k_stage_tiled(DevMesh m
     int tile = tile0 + blockIdx.x;
     if (tile >= tile1) return;
     const int G0 = gridDim.x;
+    // tile records in a 4-slot shared-memory ring, fetched three tiles ahead by cp.async (16 ints per slot:
+    // the tile's 8-int record and the next one's, whose c0 / h0 / f0 end the tile's ranges), so no tile
+    // waits on a dependent global load of its record and index lists can be fetched two tiles ahead
+    const int nmine = (tile1 - tile + G0 - 1) / G0;
+    const int tfirst = tile;
+    int *recs = reinterpret_cast<int *>(buf0 + NBUF * BUF);
+    auto fetch_rec = [&](int j) {                         // threads 0..3: one 16-byte copy each
+        if (tid < 4 && j < nmine) {
+            const int *src = t.info + (size_t)(tfirst + j * G0) * TINFO + tid * 4;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(recs + (j & 3) * TREC + tid * 4)),
+                         "l"(src) : "memory");
+        }
+    };
     if (tid == 0) {
         for (int k = 0; k < NBUF; ++k) mbar_init(&bar[k], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
+    fetch_rec(0);
+    fetch_rec(1);
+    fetch_rec(2);
+    cp_async_commit();
+    cp_async_wait_pending<0>();
     __syncthreads();
-    // NBUF tile buffers (2 or 3): while tile k is computed, tiles k+1 .. k+NBUF-1 are in flight.  At
-    // the top of the iteration for tile k one thread issues the bulk copies of tile k+NBUF-1 into the
-    // buffer tile k-1 just freed, and every thread issues that tile's halo / foreign gathers after the
-    // edge phase (their indices, loaded at the top, have arrived by then; issued earlier they only slow
-    // the edge phase's shared-memory traffic -- measured).  The gathers of a tile form one cp.async
-    // group, committed once per iteration (even if empty), so "all but the newest NBUF-2 groups" is
-    // exactly tile k's.  Tile records are carried in registers, loaded NBUF tiles ahead.
-    int hx[HPT], fx[FPT];
-    TileRec r0 = load_rec(t, tile), r1{}, r2{};
-    if (tile + G0 < tile1) r1 = load_rec(t, tile + G0);
-    if (NBUF == 3 && tile + 2 * G0 < tile1) r2 = load_rec(t, tile + 2 * G0);
-    for (int k = 0; k < NBUF - 1; ++k) {                  // prologue: tiles 0 .. NBUF-2
-        const TileRec &rk = k == 0 ? r0 : r1;
-        if (tile + k * G0 < tile1) {
-            double *Bk = buf0 + k * BUF;
-            if (tid == 0) issue_bulk<STAGE>(m, a, rk, Bk, CS2, ES2, &bar[k]);
-            load_indices(t, rk, tid, hx, fx);
-            issue_indexed<STAGE>(m, a, rk, TileBuf<STAGE>(Bk, CS2, ES2, rk), tid, hx, fx);
-        }
+    auto rec = [&](int j) {
+        const int *p = recs + (j & 3) * TREC;
+        TileRec r;
+        r.c0 = p[0], r.h0 = p[1], r.eo0 = p[2], r.eo1 = p[3], r.f0 = p[4], r.l0 = p[5], r.g0 = p[6], r.ge0 = p[7];
+        r.c1 = p[8], r.h1 = p[9], r.f1 = p[12];
+        return r;
+    };
+    // Two tile buffers: while tile j is computed the other buffer fills with tile j+1 -- one thread
+    // issues its bulk copies at the top of the iteration, every thread its halo / foreign gathers after
+    // the edge phase (issued earlier they only slow the edge phase's shared-memory traffic -- measured),
+    // from index lists loaded one iteration before (two tiles ahead).  The gathers of a tile form one
+    // cp.async group, committed once per iteration (even if empty).
+    int hx[HPT], fx[FPT], hx2[HPT], fx2[FPT];
+    {
+        const TileRec r0 = rec(0);
+        if (tid == 0) issue_bulk<STAGE>(m, a, r0, buf0, CS2, ES2, &bar[0]);
+        load_indices(t, r0, tid, hx, fx);
+        issue_indexed<STAGE>(m, a, r0, TileBuf<STAGE>(buf0, CS2, ES2, r0), tid, hx, fx);
         cp_async_commit();
+        if (nmine > 1) load_indices(t, rec(1), tid, hx, fx);
     }
     unsigned phase = 0u;                                   // bit b: parity of buffer b's next completion
     int buf = 0;
-    for (; tile < tile1; tile += G0, buf = (buf + 1 == NBUF ? 0 : buf + 1)) {
-        const TileRec cur = r0;
-        const TileRec nx = NBUF == 2 ? r1 : r2;            // tile + (NBUF-1) G0, issued this iteration
-        const int tn = tile + (NBUF - 1) * G0;
-        const bool more = tn < tile1;
-        TileRec rl{};
-        if (tn + G0 < tile1) rl = load_rec(t, tn + G0);    // consumed next iteration
-        r0 = r1;
-        if (NBUF == 2) r1 = rl; else r1 = r2, r2 = rl;
+    for (int j = 0; j < nmine; ++j, tile += G0, buf ^= 1) {
+        const TileRec cur = rec(j);
+        const bool more = j + 1 < nmine;
+        const TileRec nx = more ? rec(j + 1) : TileRec{};
         mbar_wait(&bar[buf], (phase >> buf) & 1u);
         phase ^= 1u << buf;
-        cp_async_wait_pending<NBUF - 2>();
-        __syncthreads();                                   // tile `cur` staged; tile k-1's buffer is free
-        const int bn = buf == 0 ? NBUF - 1 : buf - 1;
-        double *Bn = buf0 + bn * BUF;
-        if (more) {
-            if (tid == 0) issue_bulk<STAGE>(m, a, nx, Bn, CS2, ES2, &bar[bn]);
-            load_indices(t, nx, tid, hx, fx);              // consumed after the edge phase
-        }
+        cp_async_wait_pending<0>();
+        __syncthreads();                                   // tile `cur` staged; the other buffer is free
+        if (j + 2 < nmine) load_indices(t, rec(j + 2), tid, hx2, fx2);   // record j+2 arrived; used next iteration
+        double *Bn = buf0 + (buf ^ 1) * BUF;
+        if (more && tid == 0) issue_bulk<STAGE>(m, a, nx, Bn, CS2, ES2, &bar[buf ^ 1]);
         const TileBuf<STAGE> bc(buf0 + buf * BUF, CS2, ES2, cur);
         // ---- compute tile `cur`
         const int nOwn = cur.c1 - cur.c0;
@@ -574,7 +585,12 @@ __global__ void __launch_bounds__(NTHR, FBLTS_TILE_MINB) k_stage_tiled(DevMesh m
             }
         }
         if (more) issue_indexed<STAGE>(m, a, nx, TileBuf<STAGE>(Bn, CS2, ES2, nx), tid, hx, fx);
+        fetch_rec(j + 3);                                  // into the slot of tile j - 1 (read at the top)
         cp_async_commit();
+#pragma unroll
+        for (int q = 0; q < HPT; ++q) hx[q] = hx2[q];
+#pragma unroll
+        for (int q = 0; q < FPT; ++q) fx[q] = fx2[q];
         if (tid == 0) bc.u[nOE] = 0.0;                    // the gap slot: the term of an unused slot
         __syncthreads();
         if (own) {                                        // cell phase
@@ -1140,11 +1156,12 @@ static void tile_strides(int hmax, int emax, int &CS2, int &ES2) {
     CS2 = (HALO0 + hmax + 3 + 1) & ~1;     // + alignment offsets and the ghost copy's slack, even
     ES2 = (emax + FGAP + 8 + 3) & ~3;       // + gap and slack; multiple of 4 (the uint32 pair array)
 }
-int stage_tiled_smem_bytes_host(int stage, int hmax, int emax) {
+int stage_tiled_smem_bytes_host(int stage, int hmax, int emax, int nrec) {
     const int nca = stage == 4 ? 4 : (stage > 1 ? 3 : 1), nea = stage > 1 ? 4 : 2;
     int CS2, ES2;
     tile_strides(hmax, emax, CS2, ES2);
-    return 8 * (((NBUF + 1) & ~1) + NBUF * (nca * CS2 + nea * ES2 + ES2 / 2 + 2));
+    (void)nrec;                                  // records live in a fixed 4-slot ring
+    return 8 * (((NBUF + 1) & ~1) + NBUF * (nca * CS2 + nea * ES2 + ES2 / 2 + 2)) + 4 * TREC * 4;
 }
 
 #ifndef FBLTS_SUB_NTHR
@@ -1173,7 +1190,6 @@ int stage_tiled_configure(const DevMesh &m) {
 void launch_stage_tiled(const DevMesh &m, int stage, int tile0, int tile1, int hmax, int emax, int nsm,
                         const StageArgs &a, DevError *err, cudaStream_t s) {
     if (tile1 <= tile0) return;
-    const int smem = stage_tiled_smem_bytes_host(stage, hmax, emax);
     int CS, ES;
     tile_strides(hmax, emax, CS, ES);
     FBLTS_DISPATCH_G(m.ecS, {
@@ -1181,9 +1197,20 @@ void launch_stage_tiled(const DevMesh &m, int stage, int tile0, int tile1, int h
                         : stage == 2 ? (const void *)k_stage_tiled<G, 2>
                         : stage == 3 ? (const void *)k_stage_tiled<G, 3>
                                      : (const void *)k_stage_tiled<G, 4>;
-        int per = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, NTHR, smem);
-        const int grid = std::max(1, std::min(tile1 - tile0, nsm * std::max(1, per)));
+        // grid = resident CTAs; each stages the records of its ceil(tiles / grid) tiles in shared memory,
+        // which can lower the residency: settle both in at most three rounds
+        int per = 1, grid = 1, smem = stage_tiled_smem_bytes_host(stage, hmax, emax, 0);
+        for (int it = 0; it < 3; ++it) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, NTHR, smem);
+            grid = std::max(1, std::min(tile1 - tile0, nsm * std::max(1, per)));
+            const int want = stage_tiled_smem_bytes_host(stage, hmax, emax, (tile1 - tile0 + grid - 1) / grid);
+            if (want == smem) break;
+            smem = want;
+        }
+        {   // the launch must hold the records of ceil(tiles / grid) tiles per CTA
+            const int need = stage_tiled_smem_bytes_host(stage, hmax, emax, (tile1 - tile0 + grid - 1) / grid);
+            if (need > smem) smem = need;
+        }
         static const bool verbose = std::getenv("FBLTS_VERBOSE") != nullptr;
         if (verbose)
             std::fprintf(stderr, "[fblts] stage_tiled s%d tiles [%d,%d) hmax %d emax %d smem %d B, %d CTA/SM, grid %d\n",
