@@ -555,7 +555,14 @@ __global__ void __launch_bounds__(NTHR, FBLTS_TILE_MINB) k_stage_tiled(DevMesh m
 #endif
         // edge phase: T_e overwrites u_e; EU independent edges per thread in flight (fp64 latency)
         constexpr int EU = FBLTS_EDGE_UNROLL;
-        for (int p0 = tid; p0 < nLE; p0 += EU * NTHR) {
+        // edge slots are dealt from warp 1 on, warp 0 last: the partial last round of a tile's ~3.4 edges
+        // per thread falls on the low slots, so warp 0 -- which also issued the next tile's bulk copies --
+        // skips it, evening out the arrival at the barrier below
+#ifndef FBLTS_EDGE_ROTATE
+#define FBLTS_EDGE_ROTATE 1
+#endif
+        const int te = FBLTS_EDGE_ROTATE ? (tid >= 32 ? tid - 32 : tid + NTHR - 32) : tid;
+        for (int p0 = te; p0 < nLE; p0 += EU * NTHR) {
 #pragma unroll
             for (int uu = 0; uu < EU; ++uu) {
                 const int p = p0 + uu * NTHR;
