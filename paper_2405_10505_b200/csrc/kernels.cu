@@ -36,6 +36,11 @@ constexpr int TPB = 256;
 #ifndef FBLTS_MINB
 #define FBLTS_MINB 6
 #endif
+// band fine stage kernels (k_fine_s2 / k_fine_s3 BAND): 64 registers, 4 CTAs per SM (config 5: fine_s3
+// 1.795 -> 1.759 ms per step against 76 registers / 3 CTAs; 5 CTAs no better)
+#ifndef FBLTS_BAND_MINB
+#define FBLTS_BAND_MINB 4
+#endif
 #ifndef FBLTS_TILE_MINB
 #define FBLTS_TILE_MINB 2
 #endif
@@ -758,7 +763,7 @@ __global__ void __launch_bounds__(TPB) k_fine_s1(DevMesh m, FineArrays a, const 
 // Fine stage 2 (subeqn fine_s2): h_bar^{n,k+1/2} = h^{n,k} + dt/(2M) Psi(u_bar^{n,k+1/3}, h_bar^{n,k+1/3}),
 // u_bar^{n,k+1/3}_e = u^{n,k}_e + dt/(3M) (Phi^fast_e(h^{*,k}) + S_e) recomputed per edge.
 template <int G, bool BAND>
-__global__ void __launch_bounds__(TPB, BAND ? 1 : FBLTS_MINB) k_fine_s2(DevMesh m, FineArrays a, const double *__restrict__ uk,
+__global__ void __launch_bounds__(TPB, BAND ? FBLTS_BAND_MINB : FBLTS_MINB) k_fine_s2(DevMesh m, FineArrays a, const double *__restrict__ uk,
                                                  const double *__restrict__ S, double *__restrict__ out,
                                                  StepConst sc, PredConst p, int k, int begin, int end,
                                                  DevError *err) {
@@ -800,7 +805,7 @@ __global__ void __launch_bounds__(TPB, BAND ? 1 : FBLTS_MINB) k_fine_s2(DevMesh 
 // IF-1_E -> predicted (k/M) u~^{n+1} + (1/M) u~^{n+1/2} + (1-(k+1)/M) u^n with the tilde data
 // recomputed from the coarse thicknesses; IF-2_E / int_E -> coarse u~^{n+1/2}.
 template <int G, bool BAND>
-__global__ void __launch_bounds__(TPB, BAND ? 1 : FBLTS_MINB) k_fine_s3(DevMesh m, FineArrays a, const double *__restrict__ uN,
+__global__ void __launch_bounds__(TPB, BAND ? FBLTS_BAND_MINB : FBLTS_MINB) k_fine_s3(DevMesh m, FineArrays a, const double *__restrict__ uN,
                                                  const double *__restrict__ uk, const double *__restrict__ S,
                                                  double *__restrict__ hnext, double *__restrict__ accH,
                                                  StepConst sc, PredConst p, int k, int begin, int fstart, int end,
@@ -1976,7 +1981,7 @@ void launch_vort_update(const DevMesh &m, const DevState &st, cudaStream_t s) {
 extern "C" const char *fblts_build_info(void) {
     return "probe=" FBLTS_STR(FBLTS_PROBE) " check=" FBLTS_STR(FBLTS_CHECK) " tile=" FBLTS_STR(FBLTS_TILE)
            " tile_minb=" FBLTS_STR(FBLTS_TILE_MINB) " tile_nbuf=" FBLTS_STR(FBLTS_TILE_NBUF)
-           " tile_nthr=" FBLTS_STR(FBLTS_TILE_NTHR) " minb=" FBLTS_STR(FBLTS_MINB) 
+           " tile_nthr=" FBLTS_STR(FBLTS_TILE_NTHR) " minb=" FBLTS_STR(FBLTS_MINB) " band_minb=" FBLTS_STR(FBLTS_BAND_MINB) 
 #if defined(__CUDACC__)
            " fmad=off arch=sm_100a"
 #endif
