@@ -93,7 +93,8 @@ def byte_model(counts, M, fused, sub=0, maxE=6, maxE2=10):
     b["coarse_s1"] = cells(0, 7) * cell_s1 + edges(0, 7) * edge_s1
     b["coarse_s2"] = cells(0, 5) * cell_s + edges(0, 5) * edge_s
     b["coarse_s3"] = cells(0, 3) * cell_s + edges(0, 3) * edge_s
-    b["coarse_vel"] = edges(0, 0) * vel_e + cells(0, 1) * vel_c
+    # + u~^{n+1/2} (IF-2_E, IF-1_E) and u~^{n+1} (IF-1_E) for the fine stage-3 band sweeps (fine phases only)
+    b["coarse_vel"] = edges(0, 0) * vel_e + cells(0, 1) * vel_c + (edges(1, 2) * vel_e + edges(2, 2) * 8 if fused else 0)
     b["fine_s2"] = M * (cells(3, top) * (slotC + 8 + 8 + 8 + 8 + 8 - 8) + edges(3, top) * edge_s)
     b["fine_s3"] = M * (cells(1, top) * (slotC + 8 + 8 + 8 + 8 + 8 - 8) + edges(1, top) * edge_s)
     if sub:

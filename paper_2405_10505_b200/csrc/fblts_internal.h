@@ -179,6 +179,9 @@ struct DevState {
     double *qe;                         // q_hat per edge (energy-conserving PV flux only)
     double *K;                          // cells
     double *accH, *accU;                // accH indexed by owned cell (IF cells used), accU by e - eb.if2 (IF edges)
+    double *uIF2, *uIF3;                // coarse stage velocities u~^{n+1/2}, u~^{n+1} on IF-2_E u IF-1_E (by
+                                        // e - eb.if2; u~^{n+1} on IF-1_E only), written by the coarse velocity
+                                        // sweep, read by every fine stage-3 band sweep
     double *rkU[2], *rkAccU;            // RK4 scheme: stage velocities (ping-pong) and the velocity sum
     double *Sf;                         // slow tendency on F_E during the fine phase: S, or Sk (refresh)
     double *Sk, *hv, *uv;               // slow-term refresh: S^k on F_E and the t^{n,k} views;
@@ -264,8 +267,9 @@ void launch_coarse_s2(const DevMesh &m, const DevState &st, const double *hN, co
                       const StepConst &sc, cudaStream_t s, const Bounds &b);
 void launch_coarse_s3(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
                       double *hNew, const StepConst &sc, cudaStream_t s, const Bounds &b);
+// (if_edges: also u~^{n+1/2} and u~^{n+1} on the IF edges into st.uIF2 / st.uIF3, for the fine phase)
 void launch_coarse_vel(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
-                       const double *hNew, double *uNew, const StepConst &sc, cudaStream_t s);
+                       const double *hNew, double *uNew, const StepConst &sc, cudaStream_t s, bool if_edges = false);
 void launch_fine_s1(const DevMesh &m, const DevState &st, const double *hN, const double *hNew,
                     const double *hk, const double *uk, const StepConst &sc, const PredConst &pc,
                     int k, cudaStream_t s, const Bounds &b, bool deep = true);

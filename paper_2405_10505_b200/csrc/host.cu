@@ -1278,6 +1278,8 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
     put(s.qe, c->cfg.pv_energy ? (size_t)L.nE : 1);
     put(s.accH, std::max(1, L.nOwnC));
     put(s.accU, std::max(1, L.eb.f - L.eb.if2));
+    put(s.uIF2, std::max(1, L.eb.f - L.eb.if2));
+    put(s.uIF3, std::max(1, L.eb.f - L.eb.if2));
     const size_t nrk = c->cfg.scheme != FBLTS_SCHEME_FBLTS ? nE1 : 1;
     put(s.rkU[0], nrk);
     put(s.rkU[1], nrk);
@@ -1768,7 +1770,7 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
             if (part == 0) {
                 if (k == 0) {
                     mark(K_COARSE_VEL);
-                    launch_coarse_vel(m, st, hN, uN, hNew, uNew, sc, sv);
+                    launch_coarse_vel(m, st, hN, uN, hNew, uNew, sc, sv, true);
                 } else {
                     mark(K_FINE_VEL);
                     launch_fine_vel(m, st, hN, hNew, k - 1 == 0 ? hN : hb(k - 2), hb(k - 1),

@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(TPB) k_slow_pre(DevMesh m, const double *__res
     if (b < nbV) {
         const int v = v0 + b * TPB + threadIdx.x;
         if (v >= m.nV) return;
+        const double A = m.areaTri[v], fv = m.fV[v];       // independent loads first
         double circ = 0.0;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
@@ -130,19 +131,19 @@ __global__ void __launch_bounds__(TPB) k_slow_pre(DevMesh m, const double *__res
             const double t = m.dc[e] * u[e];
             circ = circ + (pos ? t : -t);
         }
-        const double A = m.areaTri[v];
         const double zeta = circ / A;
         double hv = 0.0;
 #pragma unroll
         for (int k = 0; k < 3; ++k) hv = hv + m.kite[k * m.strideV + v] * h[m.cov[k * m.strideV + v]];
         hv = hv / A;
-        q[v] = (zeta + m.fV[v]) / hv;
+        q[v] = (zeta + fv) / hv;
     } else if (b < nbV + nbC) {
         const int i = c0 + (b - nbV) * TPB + threadIdx.x;
         if (i >= m.nC) return;
         int2 r[G];
         load_row<G>(m, i, r);
         const int n = m.nEoC[i];
+        const double Ai = m.areaCell[i];
         double acc = 0.0;
 #pragma unroll
         for (int j = 0; j < G; ++j) {
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(TPB) k_slow_pre(DevMesh m, const double *__res
                 acc = acc + 0.25 * m.dv[e] * m.dc[e] * ue * ue;
             }
         }
-        K[i] = acc / m.areaCell[i];
+        K[i] = acc / Ai;
     } else {
         const int e = e0 + (b - nbV - nbC) * TPB + threadIdx.x;
         if (e >= m.nE) return;
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(TPB) k_slow_pre(DevMesh m, const double *__res
 #define FBLTS_SLOW_CHUNK 5
 #endif
 #ifndef FBLTS_SLOW_MINB
-#define FBLTS_SLOW_MINB 6
+#define FBLTS_SLOW_MINB 5
 #endif
 // PVE (energy-conserving PV flux): the term q_hat_e F_perp_e becomes
 // sum_j (W_j F_eoe_j) (0.5 (q_hat_e + q_hat_eoe_j)) with q_hat per edge from k_qhat (oracle
@@ -181,7 +182,20 @@ __global__ void __launch_bounds__(TPB, FBLTS_SLOW_MINB) k_slow_edge(DevMesh m, c
                                                    double rho0, double cd, double cw, int e0, int e1) {
     const int e = e0 + blockIdx.x * TPB + threadIdx.x;
     if (e >= e1) return;
+    const int2 c = m.coe[e];                  // issued first: its gathers (q, K, h) end the chain (measured -3 %)
     const int n = m.nEoE[e];
+#ifndef FBLTS_SLOW_HOIST
+#define FBLTS_SLOW_HOIST 1   // config 5: slow_edge 1.374 -> 1.328 ms per step (with FBLTS_SLOW_MINB 5)
+#endif
+    // FBLTS_SLOW_HOIST: the per-edge gathers (q, K, h) and streams (tau, d_e) issued before the slot loop
+    double qv0 = 0.0, qv1 = 0.0, K0 = 0.0, K1 = 0.0, h0 = 0.0, h1 = 0.0, tau = 0.0, dce = 0.0;
+    if (FBLTS_SLOW_HOIST) {
+        if (!PVE) {
+            const int2 v = m.voe[e];
+            qv0 = q[v.x], qv1 = q[v.y];
+        }
+        K0 = K[c.x], K1 = K[c.y], h0 = h[c.x], h1 = h[c.y], tau = m.tau[e], dce = m.dc[e];
+    }
     // F_perp = sum_j W_j F_eoe_j in slot order, gathered in chunks of CH slots (register budget);
     // with the hurricane terms also v_e = sum_j W_j u_eoe_j (tangential reconstruction)
     constexpr int CH = FBLTS_SLOW_CHUNK < MAXE2 ? FBLTS_SLOW_CHUNK : MAXE2;
@@ -208,19 +222,22 @@ __global__ void __launch_bounds__(TPB, FBLTS_SLOW_MINB) k_slow_edge(DevMesh m, c
                 if (HUR) vt = vt + w[j] * ut[HUR ? j : 0];
             }
     }
-    const int2 c = m.coe[e];
     double pv;
     if (PVE) {
         pv = fp;
     } else {
-        const int2 v = m.voe[e];
-        const double qh = 0.5 * (q[v.x] + q[v.y]);
+        if (!FBLTS_SLOW_HOIST) {
+            const int2 v = m.voe[e];
+            qv0 = q[v.x], qv1 = q[v.y];
+        }
+        const double qh = 0.5 * (qv0 + qv1);
         pv = qh * fp;
     }
     if (pvout) pvout[e] = pv;                 // vorticity companion: the PV-flux part alone
-    const double he = 0.5 * (h[c.x] + h[c.y]);
-    const double G = m.tau[e] / (rho0 * he);
-    double s = pv - (K[c.y] - K[c.x]) / m.dc[e] + G;
+    if (!FBLTS_SLOW_HOIST) K0 = K[c.x], K1 = K[c.y], h0 = h[c.x], h1 = h[c.y], tau = m.tau[e], dce = m.dc[e];
+    const double he = 0.5 * (h0 + h1);
+    const double G = tau / (rho0 * he);
+    double s = pv - (K1 - K0) / dce + G;
     if (HUR) {   // bottom drag and wind (eq. hurricane_model)
         const double ue = u[e];
         const double speed = sqrt(ue * ue + vt * vt);
@@ -642,13 +659,25 @@ __global__ void __launch_bounds__(TPB) k_coarse_vel(DevMesh m, const double *__r
                                                     const double *__restrict__ h2,
                                                     const double *__restrict__ h3, const double *__restrict__ uN,
                                                     const double *__restrict__ S, double *__restrict__ uNew,
-                                                    StepConst sc, int end) {
+                                                    StepConst sc, int end, double *__restrict__ u2o,
+                                                    double *__restrict__ u3o, int if1, int fend) {
     const int e = blockIdx.x * TPB + threadIdx.x;
-    if (e >= end) return;
+    if (e >= fend) return;
     const int2 c = m.coe[e];
-    const double phi = phi_fast(sc.g, hs3c(sc, h3, h2, hN, c.x), m.zb[c.x], hs3c(sc, h3, h2, hN, c.y), m.zb[c.y],
-                                m.dc[e]);
-    uNew[e] = uN[e] + sc.c3 * (phi + S[e]);
+    const double zb0 = m.zb[c.x], zb1 = m.zb[c.y], dc = m.dc[e], un = uN[e], se = S[e];
+    if (e < end || e >= if1) {      // u~^{n+1}: int_E -> u^{n+1}; IF-1_E -> u~^{n+1} for the fine phase (Q10)
+        const double phi = phi_fast(sc.g, hs3c(sc, h3, h2, hN, c.x), zb0, hs3c(sc, h3, h2, hN, c.y), zb1, dc);
+        const double v = un + sc.c3 * (phi + se);
+        if (e < end) {
+            uNew[e] = v;
+            return;
+        }
+        u3o[e - end] = v;
+    }
+    // IF-2_E u IF-1_E: u~^{n+1/2} -- the fine stage-3 band sweep's edge velocities on the IF edges (k_fine_s3),
+    // which the fine phase never changes: h2, h^n, h3 of IF cells and u^n, S stay as the coarse stages left them
+    const double phi2 = phi_fast(sc.g, hs2c(sc, h2, hN, c.x), zb0, hs2c(sc, h2, hN, c.y), zb1, dc);
+    u2o[e - end] = un + sc.c2 * (phi2 + se);
 }
 
 // ---------------------------------------------------------------- fine subcycles
@@ -658,6 +687,7 @@ __global__ void __launch_bounds__(TPB) k_coarse_vel(DevMesh m, const double *__r
 struct FineArrays {
     const double *hN, *h1, *h2, *h3, *hk;   // h3 = coarse stage-3 output (hNew before the correction)
     const double *Sf;                       // slow tendency used on F_E (S, or S^k with the refresh)
+    const double *uIF2, *uIF3;              // u~^{n+1/2}, u~^{n+1} on the IF edges (DevState)
 };
 
 __device__ __forceinline__ double pred_level(const PredConst &p, const FineArrays &a, int x) {
@@ -834,19 +864,13 @@ __global__ void __launch_bounds__(TPB, BAND ? FBLTS_BAND_MINB : FBLTS_MINB) k_fi
                 const double zbn = m.zb[nb];
                 const double phi = pos ? phi_fast(sc.g, HSi, zbi, HSn, zbn, dc) : phi_fast(sc.g, HSn, zbn, HSi, zbi, dc);
                 ue = uk[e] + sc.c2f * (phi + a.Sf[e]);
-            } else {
+            } else if (ec >= 1) {             // IF edges: the coarse stage velocities (k_coarse_vel, once per step)
+                const double u2 = a.uIF2[e - m.eb.if2];
+                ue = ec == 2 ? p.a * a.uIF3[e - m.eb.if2] + p.b * u2 + p.c * uN[e] : u2;
+            } else {                          // int_E edge of an IF-2 cell: u~^{n+1/2}
                 const int c0 = pos ? i : nb, c1 = pos ? nb : i;
-                const double zb0 = m.zb[c0], zb1 = m.zb[c1];
-                const double phi2 = phi_fast(sc.g, hs2c(sc, a.h2, a.hN, c0), zb0, hs2c(sc, a.h2, a.hN, c1), zb1, dc);
-                const double u2 = uN[e] + sc.c2 * (phi2 + S[e]);
-                if (ec == 2) {
-                    const double phi3 = phi_fast(sc.g, hs3c(sc, a.h3, a.h2, a.hN, c0), zb0,
-                                                 hs3c(sc, a.h3, a.h2, a.hN, c1), zb1, dc);
-                    const double u3 = uN[e] + sc.c3 * (phi3 + S[e]);
-                    ue = p.a * u3 + p.b * u2 + p.c * uN[e];
-                } else {
-                    ue = u2;
-                }
+                const double phi2 = phi_fast(sc.g, hs2c(sc, a.h2, a.hN, c0), m.zb[c0], hs2c(sc, a.h2, a.hN, c1), m.zb[c1], dc);
+                ue = uN[e] + sc.c2 * (phi2 + S[e]);
             }
             acc = acc + psi_term(pos, Hi, Hn, ue, m.dv[e]);
         }
@@ -1619,9 +1643,11 @@ void launch_coarse_s3(const DevMesh &m, const DevState &st, const double *hN, co
                                                                                          sc, beg, end, st.err));
 }
 void launch_coarse_vel(const DevMesh &m, const DevState &st, const double *hN, const double *uN,
-                       const double *hNew, double *uNew, const StepConst &sc, cudaStream_t s) {
-    const int end = m.eb.if2;
-    if (end > 0) k_coarse_vel<<<nblocks(end), TPB, 0, s>>>(m, hN, st.h2, hNew, uN, st.S, uNew, sc, end);
+                       const double *hNew, double *uNew, const StepConst &sc, cudaStream_t s, bool if_edges) {
+    const int end = m.eb.if2, fend = if_edges ? m.eb.f : end;
+    if (fend > 0)
+        k_coarse_vel<<<nblocks(fend), TPB, 0, s>>>(m, hN, st.h2, hNew, uN, st.S, uNew, sc, end, st.uIF2, st.uIF3,
+                                                   m.eb.if1, fend);
 }
 static FineArrays fine_arrays(const DevState &st, const double *hN, const double *hNew, const double *hk) {
     FineArrays a;
@@ -1631,6 +1657,8 @@ static FineArrays fine_arrays(const DevState &st, const double *hN, const double
     a.h2 = st.h2;
     a.h3 = hNew;
     a.hk = hk;
+    a.uIF2 = st.uIF2;
+    a.uIF3 = st.uIF3;
     return a;
 }
 
