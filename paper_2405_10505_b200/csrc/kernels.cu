@@ -596,20 +596,23 @@ __global__ void __launch_bounds__(NTHR, FBLTS_TILE_MINB) k_stage_tiled(DevMesh m
                                   (l1 < nOwn || (l1 >= HALO0 && l1 < HALO0 + cur.h1 - cur.h0)));
                     const double H0 = bc.hp[l0], H1 = bc.hp[l1];
                     double ue = bc.u[q];
+                    const double le = bc.l[q];                   // before the division (see k_fine_vel)
                     if (STAGE == 2 || STAGE == 3) {
+                        const double Se = bc.S[q];
                         const double HS0 = a.bb * H0 + a.omb * bc.hb[l0];
                         const double HS1 = a.bb * H1 + a.omb * bc.hb[l1];
                         const double phi = phi_fast(a.g, HS0, bc.z[l0], HS1, bc.z[l1], bc.d[q]);
-                        ue = ue + a.cu * (phi + bc.S[q]);
+                        ue = ue + a.cu * (phi + Se);
                     } else if (STAGE == 4) {            // u^{n,k} (fine velocity stage 3, subeqn fine_s3)
+                        const double Se = bc.S[q];
                         const double HS0 = a.bb * H0 + a.omb * bc.h2[l0] + a.bb * bc.hb[l0];
                         const double HS1 = a.bb * H1 + a.omb * bc.h2[l1] + a.bb * bc.hb[l1];
                         const double phi = phi_fast(a.g, HS0, bc.z[l0], HS1, bc.z[l1], bc.d[q]);
-                        ue = ue + a.cu * (phi + bc.S[q]);
+                        ue = ue + a.cu * (phi + Se);
                         if (p < nOE) a.unew[cur.eo0 + p] = ue;
                     }
                     const double Fe = (0.5 * (H0 + H1)) * ue;
-                    bc.u[q] = bc.l[q] * Fe;
+                    bc.u[q] = le * Fe;
                 }
             }
         }
@@ -816,9 +819,10 @@ __global__ void __launch_bounds__(TPB, BAND ? FBLTS_BAND_MINB : FBLTS_MINB) k_fi
             view1<BAND>(m, sc, p, a, nb, Hn, HSn);
             const double zbn = m.zb[nb];
             const double dc = m.dc[e];
+            const double uke = uk[e], sfe = a.Sf[e], dve = m.dv[e];  // loaded before the division
             const double phi = pos ? phi_fast(sc.g, HSi, zbi, HSn, zbn, dc) : phi_fast(sc.g, HSn, zbn, HSi, zbi, dc);
-            const double ue = uk[e] + sc.c1f * (phi + a.Sf[e]);     // every edge of a fine cell is F_E
-            acc = acc + psi_term(pos, Hi, Hn, ue, m.dv[e]);
+            const double ue = uke + sc.c1f * (phi + sfe);           // every edge of a fine cell is F_E
+            acc = acc + psi_term(pos, Hi, Hn, ue, dve);
         }
     }
     const double psi = -acc / m.areaCell[i];
@@ -858,21 +862,24 @@ __global__ void __launch_bounds__(TPB, BAND ? FBLTS_BAND_MINB : FBLTS_MINB) k_fi
             double Hn, HSn;
             view2<BAND>(m, sc, p, a, nb, Hn, HSn);
             const double dc = m.dc[e];
+            const double dve = m.dv[e];                       // loaded before any division
             double ue;
             const int ec = eclass<BAND>(m.eb, e);
             if (ec == 3) {
                 const double zbn = m.zb[nb];
+                const double uke = uk[e], sfe = a.Sf[e];
                 const double phi = pos ? phi_fast(sc.g, HSi, zbi, HSn, zbn, dc) : phi_fast(sc.g, HSn, zbn, HSi, zbi, dc);
-                ue = uk[e] + sc.c2f * (phi + a.Sf[e]);
+                ue = uke + sc.c2f * (phi + sfe);
             } else if (ec >= 1) {             // IF edges: the coarse stage velocities (k_coarse_vel, once per step)
                 const double u2 = a.uIF2[e - m.eb.if2];
                 ue = ec == 2 ? p.a * a.uIF3[e - m.eb.if2] + p.b * u2 + p.c * uN[e] : u2;
             } else {                          // int_E edge of an IF-2 cell: u~^{n+1/2}
                 const int c0 = pos ? i : nb, c1 = pos ? nb : i;
+                const double une = uN[e], se = S[e];
                 const double phi2 = phi_fast(sc.g, hs2c(sc, a.h2, a.hN, c0), m.zb[c0], hs2c(sc, a.h2, a.hN, c1), m.zb[c1], dc);
-                ue = uN[e] + sc.c2 * (phi2 + S[e]);
+                ue = une + sc.c2 * (phi2 + se);
             }
-            acc = acc + psi_term(pos, Hi, Hn, ue, m.dv[e]);
+            acc = acc + psi_term(pos, Hi, Hn, ue, dve);
         }
     }
     const double psi = -acc / m.areaCell[i];
@@ -897,15 +904,16 @@ __global__ void __launch_bounds__(TPB) k_fine_vel(DevMesh m, FineArrays a, const
     const int e = begin + blockIdx.x * TPB + threadIdx.x;
     if (e >= end) return;
     const int2 c = m.coe[e];
+    // every load before the division: the compiler does not move a load above the division's slow-path
+    // branch, so a load written after it starts only when the division is done (measured on slow_edge)
+    const bool fine = !BAND || e >= m.eb.f;
+    const int ai = e - m.eb.if2;
+    const double base = fine ? uk[e] : (k == 0 ? 0.0 : accU[ai]);
+    const double se = fine ? a.Sf[e] : S[e];
     const double phi = phi_fast(sc.g, view3<BAND>(m, sc, p, a, hnext, c.x), m.zb[c.x],
                                 view3<BAND>(m, sc, p, a, hnext, c.y), m.zb[c.y], m.dc[e]);
-    if (!BAND || e >= m.eb.f) {
-        unext[e] = uk[e] + sc.c3f * (phi + a.Sf[e]);
-    } else {
-        const int ai = e - m.eb.if2;
-        const double prev = k == 0 ? 0.0 : accU[ai];
-        accU[ai] = prev + (phi + S[e]);
-    }
+    if (fine) unext[e] = base + sc.c3f * (phi + se);
+    else accU[ai] = base + (phi + se);
 }
 
 // Interface Correction (eq. if_correction; reading Q14):
