@@ -131,10 +131,10 @@ __global__ void __launch_bounds__(TPB) k_slow_pre(DevMesh m, const double *__res
             const double t = m.dc[e] * u[e];
             circ = circ + (pos ? t : -t);
         }
-        const double zeta = circ / A;
-        double hv = 0.0;
+        double hv = 0.0;                                   // (its gathers before the first division)
 #pragma unroll
         for (int k = 0; k < 3; ++k) hv = hv + m.kite[k * m.strideV + v] * h[m.cov[k * m.strideV + v]];
+        const double zeta = circ / A;
         hv = hv / A;
         q[v] = (zeta + fv) / hv;
     } else if (b < nbV + nbC) {
@@ -282,6 +282,7 @@ __global__ void __launch_bounds__(TPB, FBLTS_MINB) k_coarse_stage(DevMesh m, con
             const int e = decode(r[j].x, pos);
             const int nb = r[j].y;
             double ue, Hn;
+            const double dve = m.dv[e];
             if (STAGE == 1) {
                 Hn = hN[nb];
                 ue = uN[e];
@@ -290,10 +291,11 @@ __global__ void __launch_bounds__(TPB, FBLTS_MINB) k_coarse_stage(DevMesh m, con
                 const double HSn = bb * Hn + omb * hN[nb];
                 const double zbn = m.zb[nb];
                 const double dc = m.dc[e];
+                const double une = uN[e], se = S[e];        // loaded before the division
                 const double phi = pos ? phi_fast(sc.g, HSi, zbi, HSn, zbn, dc) : phi_fast(sc.g, HSn, zbn, HSi, zbi, dc);
-                ue = uN[e] + cu * (phi + S[e]);
+                ue = une + cu * (phi + se);
             }
-            acc = acc + psi_term(pos, Hi, Hn, ue, m.dv[e]);
+            acc = acc + psi_term(pos, Hi, Hn, ue, dve);
         }
     }
     const double ch = STAGE == 1 ? sc.c1 : (STAGE == 2 ? sc.c2 : sc.c3);
@@ -946,12 +948,14 @@ __global__ void __launch_bounds__(TPB) k_rk4_stage(DevMesh m, int stage, const d
                                                    double *__restrict__ accH, double *__restrict__ accU,
                                                    double *__restrict__ hout, double *__restrict__ uout,
                                                    double cnext, double dt6, double g, unsigned nbC, DevError *err) {
-    double kx, base;
+    double kx, base, accv = 0.0;          // base and the running sum loaded before the division (k_fine_vel)
     double *acc, *out;
     int x;
     if (blockIdx.x < nbC) {
         x = blockIdx.x * TPB + threadIdx.x;
         if (x >= m.nOwnC) return;
+        base = hN[x];
+        if (stage >= 2) accv = accH[x];
         int2 r[G];
         load_row<G>(m, x, r);
         const int n = m.nEoC[x];
@@ -966,15 +970,16 @@ __global__ void __launch_bounds__(TPB) k_rk4_stage(DevMesh m, int stage, const d
             }
         }
         kx = -a / m.areaCell[x];
-        base = hN[x];
         acc = accH;
         out = hout;
     } else {
         x = (blockIdx.x - nbC) * TPB + threadIdx.x;
         if (x >= m.nOwnE) return;
         const int2 c = m.coe[x];
-        kx = phi_fast(g, hs[c.x], m.zb[c.x], hs[c.y], m.zb[c.y], m.dc[x]) + S[x];
         base = uN[x];
+        if (stage >= 2) accv = accU[x];
+        const double sx = S[x];
+        kx = phi_fast(g, hs[c.x], m.zb[c.x], hs[c.y], m.zb[c.y], m.dc[x]) + sx;
         acc = accU;
         out = uout;
     }
@@ -986,8 +991,8 @@ __global__ void __launch_bounds__(TPB) k_rk4_stage(DevMesh m, int stage, const d
     }
     double sum;
     if (stage == 1) sum = kx;
-    else if (stage == 4) sum = acc[x] + kx;
-    else sum = acc[x] + 2.0 * kx;
+    else if (stage == 4) sum = accv + kx;
+    else sum = accv + 2.0 * kx;
     if (stage < 4) {
         acc[x] = sum;
         const double v = base + cnext * kx;
@@ -1780,6 +1785,7 @@ __global__ void __launch_bounds__(TPB) k_un_cstage(DevMesh m, const double *__re
     load_row<G>(m, i, r);
     const int n = m.nEoC[i];
     const double Hi = H[i];
+    const double hn = hN[i];                          // before the division
     double acc = 0.0;
 #pragma unroll
     for (int j = 0; j < G; ++j) {
@@ -1791,9 +1797,8 @@ __global__ void __launch_bounds__(TPB) k_un_cstage(DevMesh m, const double *__re
     }
     const double c = STAGE == 1 ? sc.c1 : (STAGE == 2 ? sc.c2 : sc.c3);
     const double psi = -acc / m.areaCell[i];
-    const double v = hN[i] + c * psi;
+    const double v = hn + c * psi;
     out[i] = v;
-    const double hn = hN[i];
     hsv[i] = STAGE == 1 ? sc.b1 * v + sc.omb1 * hn
                         : (STAGE == 2 ? sc.b2 * v + sc.omb2 * hn : sc.b3 * v + sc.om2b3 * Hi + sc.b3 * hn);
     if (!(v > 0.0)) report(err, STAGE == 1 ? K_COARSE_S1 : (STAGE == 2 ? K_COARSE_S2 : K_COARSE_S3), -1, i, v);
@@ -1808,13 +1813,11 @@ __global__ void __launch_bounds__(TPB) k_un_vel(DevMesh m, const double *__restr
     const int e = e0 + blockIdx.x * TPB + threadIdx.x;
     if (e >= e1) return;
     const int2 cc = m.coe[e];
+    const bool ia = acc && e >= a0 && e < a1;
+    const double b0 = ia ? (first ? 0.0 : acc[e - a0]) : base[e], se = S[e];   // loads before the division
     const double phi = phi_fast(g, HS[cc.x], m.zb[cc.x], HS[cc.y], m.zb[cc.y], m.dc[e]);
-    if (acc && e >= a0 && e < a1) {
-        const double prev = first ? 0.0 : acc[e - a0];
-        acc[e - a0] = prev + (phi + S[e]);
-    } else {
-        out[e] = base[e] + c * (phi + S[e]);
-    }
+    if (ia) acc[e - a0] = b0 + (phi + se);
+    else out[e] = b0 + c * (phi + se);
 }
 
 // fine-phase views of stage s (1..3) at subcycle k: HS view on every owned cell (view1/2/3: fine
@@ -1875,14 +1878,15 @@ __global__ void __launch_bounds__(TPB) k_un_fstage(DevMesh m, FineArrays a, cons
             acc = acc + psi_term(pos, Hi, Hn, U[e], m.dv[e]);
         }
     }
+    const bool fine = i >= m.cb.f;
+    const double b0 = fine ? a.hk[i] : (k == 0 ? 0.0 : accH[i]);   // loaded before the division
     const double psi = -acc / m.areaCell[i];
-    if (i >= m.cb.f) {
-        const double v = a.hk[i] + (STAGE == 2 ? sc.c2f : sc.c3f) * psi;
+    if (fine) {
+        const double v = b0 + (STAGE == 2 ? sc.c2f : sc.c3f) * psi;
         out[i] = v;
         if (!(v > 0.0)) report(err, STAGE == 2 ? K_FINE_S2 : K_FINE_S3, k, i, v);
     } else {
-        const double prev = k == 0 ? 0.0 : accH[i];
-        accH[i] = prev + psi;
+        accH[i] = b0 + psi;
     }
 }
 
