@@ -129,7 +129,9 @@ def unsplit_byte_model(counts, M, maxE=6, maxE2=10):
     every velocity update is preceded by a slow sweep (slow_pre over the mesh -- or, for fine stages 1-2,
     over the F_E stencil -- and slow_edge over the update's edge range); the thickness sweeps read the
     stored stage velocity instead of recomputing it (cell row + h_prev, h_base, A, write; per edge U, l);
-    the view kernels write the HS / U views of the stage's stencil (8 B per cell and per edge each way)."""
+    the view kernels write the HS / U views of the stage's stencil (8 B per cell and per edge each way).
+    The velocity update runs inside the slow edge sweep (VelFuse): + u_base, z_b, the write of u, - the
+    store of S (16 B per edge); the coarse_vel / fine_vel kinds are then empty."""
     C, E = counts["owned_cells"], counts["owned_edges"]
     V = counts["nVertices"] * C // max(1, counts["nCells"])
     cc, ec = counts["cells_by_region"], counts["edges_by_region"]
@@ -141,7 +143,6 @@ def unsplit_byte_model(counts, M, maxE=6, maxE2=10):
     pre_fine = pre_full * fstencil
     edge_b = 4 + 4 * maxE2 + 8 * maxE2 + 8 * 5 + 8 * 2              # slow_edge per edge (+ q, K, h gathers)
     th = lambda n_c, n_e: n_c * (slotC + 8 * 4) + n_e * 16             # thickness sweep with stored U
-    vel = lambda n_e: n_e * (8 * 4 + 8) + n_e * 8                       # un_vel: coe, S, base, d, write (+ HS)
     view = lambda n_c, n_e: (n_c + n_e) * 16
     b = {}
     yE = [edges(0, 6), edges(0, 4), edges(0, 2)]                       # Y1 = C_E u F^4_E, Y2, Y3
@@ -149,12 +150,12 @@ def unsplit_byte_model(counts, M, maxE=6, maxE2=10):
     b["coarse_s1"], b["coarse_s2"], b["coarse_s3"] = (th(xC[q], yE[q]) for q in range(3))
     b["slow_pre"] = 3 * pre_full + M * (2 * pre_fine + pre_full)
     fE, ifE = edges(3, 8), edges(1, 8)
-    b["slow_edge"] = edge_b * (sum(yE) + M * (2 * fE + ifE))
-    b["coarse_vel"] = sum(vel(n) for n in yE)
+    b["slow_edge"] = (edge_b + 16) * (sum(yE) + M * (2 * fE + ifE))
+    b["coarse_vel"] = 0
     b["fine_s1"] = M * (th(cells(3, 8), fE) + view(cells(1, 8), ifE))
     b["fine_s2"] = M * (th(cells(3, 8), fE) + view(cells(1, 8), ifE))
-    b["fine_s3"] = M * (th(cells(1, 8), ifE) + 2 * view(cells(1, 8), ifE))
-    b["fine_vel"] = M * (2 * vel(fE) + vel(ifE))
+    b["fine_s3"] = M * (th(cells(1, 8), ifE) + view(cells(1, 8), ifE) + view(0, ifE))
+    b["fine_vel"] = 0
     b["correct_if"] = cells(1, 2) * 24 + edges(1, 2) * 24
     return b
 
@@ -408,6 +409,14 @@ def arm_native(args):
     launches_per_step = s.counts()["kernels_per_step"]         # nodes of the captured step graph
     step_bytes = sum(bm[k] for k in t_step)
     prof_total = sum(t_step.values())
+    # the dominant stage sweep against SURVEY 8(d)'s flat 188 B per cell-update (s >= 2) as well: cells
+    # per launch = the sweep's extent (fine s3: IF-2 u IF-1 u F, fine s2: F; the split step only)
+    survey = None
+    if dom in ("fine_s2", "fine_s3") and not args.unsplit and not args.slow_refresh:
+        cc = counts["cells_by_region"]
+        n_cells = sum(cc[1:]) if dom == "fine_s3" else sum(cc[3:])
+        ach = n_cells * 188 / (dom_ms * 1e-3) / 1e9
+        survey = {"bytes_per_cell": 188, "cells_per_launch": n_cells, "achieved": ach, "frac": ach / peak}
 
     # ---------------- end to end through the public API with HOST buffers
     e2e = None
@@ -521,7 +530,7 @@ def arm_native(args):
                      "frac": achieved / peak, "traffic": traffic, "bytes_per_launch": bm[dom] / launches_dom,
                      "launch_ms": dom_ms, "share_of_step": t_step[dom] / prof_total, "peak_source": peak_src,
                      "step_achieved": step_bytes / (ms_step * 1e-3) / 1e9,
-                     "step_frac": step_bytes / (ms_step * 1e-3) / 1e9 / peak},
+                     "step_frac": step_bytes / (ms_step * 1e-3) / 1e9 / peak, "survey_8d_model": survey},
         "kernels": {k: {"ms_per_launch": tms / n, "launches_per_step": n / n_prof, "ms_per_step": tms / n_prof,
                         "GBps": bm[k] / (tms / n_prof * 1e-3) / 1e9}
                     for k, (tms, n) in prof.items() if n},

@@ -131,6 +131,10 @@ struct DevMesh {
     // [nB, nOwnC), so that a stage can compute the boundary block, hand it to the halo exchange
     // and compute the interior block while the exchange is in flight.
     int32_t nB;
+    // 1: the edge e = eov[k][v] with v = voe[e][1] joins cov[k][v] and cov[(k+1)%3][v], for every local
+    // edge exactly once -- the full slow_pre sweep then forms F_e in the vertex role (its h and u are
+    // already loaded there) and runs no edge role
+    int32_t vF;
     Bounds cb, cbI;                    // boundary / interior cell blocks (absolute indices)
     Bounds eb;                         // edges touching owned cells (eb.end = nOwnE)
     Bounds cbh;                        // halo cell block [nOwnC, nC), region-major, absolute indices
@@ -247,9 +251,21 @@ void launch_slow_edge(const DevMesh &m, const DevState &st, const double *h, con
                       cudaStream_t s);
 // restricted slow sweeps (vertices >= v0, cells >= c0, edges >= e0; S on edges [e0, e1) into out)
 void launch_slow_pre_range(const DevMesh &m, const DevState &st, const double *h, const double *u, int v0, int c0,
-                           int e0, cudaStream_t s);
+                           int e0, cudaStream_t s,
+                           int v0vf = -1);
+// Unsplit velocity update fused into the slow edge sweep (k_slow_edge<..., VEL = true>): instead of
+// writing S_e, out_e = base_e + c (Phi^fast_e(h) + S_e), or on edges [a0, a1) with acc != nullptr
+// acc[e - a0] = (first ? 0 : acc[e - a0]) + (Phi^fast_e(h) + S_e) -- k_un_vel's arithmetic, same bits.
+struct VelFuse {
+    const double *base = nullptr;
+    double *out = nullptr;
+    double c = 0.0;
+    double *acc = nullptr;
+    int a0 = 0, a1 = 0, first = 0;
+};
 void launch_slow_edge_range(const DevMesh &m, const DevState &st, const double *h, const double *u, double *out,
-                            int e0, int e1, const StepConst &sc, cudaStream_t s, double *pvout = nullptr);
+                            int e0, int e1, const StepConst &sc, cudaStream_t s, double *pvout = nullptr,
+                            const VelFuse *vel = nullptr);
 // prognostic absolute vorticity companion (unsplit, config vorticity): kernels.cu
 void launch_vort_int(const DevState &st, double c3, int e1, cudaStream_t s);
 void launch_vort_fine(const DevMesh &m, const DevState &st, double c3f, int first, cudaStream_t s);
@@ -299,7 +315,7 @@ void launch_un_vel(const DevMesh &m, const DevState &st, const double *base, dou
                    double *acc, int a0, int a1, int first, const StepConst &sc, cudaStream_t s);
 void launch_un_views(const DevMesh &m, const DevState &st, int stage, const double *hN, const double *hNew,
                      const double *hk, const double *hnext, const double *uN, const double *ufine,
-                     const StepConst &sc, const PredConst &pc, cudaStream_t s);
+                     const StepConst &sc, const PredConst &pc, cudaStream_t s, int c0 = 0, int e0 = 0);
 void launch_un_fstage(const DevMesh &m, const DevState &st, int stage, const double *hN, const double *hNew,
                       const double *hk, const double *U, double *out, const StepConst &sc, const PredConst &pc,
                       int k, cudaStream_t s);

@@ -130,6 +130,12 @@ struct fblts_ctx {
     size_t t_nHalo = 0, t_nFedge = 0, t_nEcl = 0;
     bool deep_runs_ok = false;
     int vminF = 0;
+    int vminF1 = -1;           // vF: first vertex owning an edge of IF-1_E .. F_E (-1: vF off)
+    // unsplit fine views (enqueue_unsplit_step): first cell / edge the HS / U views of fine stages 1-2 are
+    // read at (the F_E slow stencil), first edge the stage-3 thickness sweep reads U at (cells from IF-2)
+    int un_c12 = 0, un_e12 = 0, un_e3 = 0;
+    bool vF = false;           // DevMesh::vF (FBLTS_VF=0: off)
+    bool un_fuse = true;       // unsplit: velocity update inside the slow edge sweep (FBLTS_UNFUSE=0: off)
     std::vector<int32_t> e_owner;          // local owner cell of every local edge (build_local)
     bool tiled = true;
     bool split = false;        // FBLTS_SPLIT=1: separate launches for the thin interface blocks
@@ -1006,6 +1012,71 @@ int build_local(fblts_ctx *c, const std::vector<int32_t> &coc) {
             c->d_kite[(size_t)k * sV + v] = m.kite[3 * o + k];
         }
     }
+    {   // F_e in slow_pre's vertex role: every local edge met exactly once as a positive eov slot whose
+        // two kite cells (slots k, k+1) are the edge's cells
+        const char *ev = getenv("FBLTS_VF");
+        std::vector<uint8_t> seen(L.nE, 0);
+        bool ok = !(ev && ev[0] == '0');
+        for (int v = 0; ok && v < L.nV; ++v)
+            for (int k = 0; k < 3; ++k) {
+                const int es = c->d_eov[(size_t)k * sV + v];
+                if (es < 0) continue;
+                const int a = c->d_cov[(size_t)k * sV + v], b = c->d_cov[(size_t)((k + 1) % 3) * sV + v];
+                if (es >= L.nE || seen[es] || a < 0 || b < 0 ||
+                    !((c->d_coe[2 * es] == a && c->d_coe[2 * es + 1] == b) ||
+                      (c->d_coe[2 * es] == b && c->d_coe[2 * es + 1] == a))) {
+                    ok = false;
+                    break;
+                }
+                seen[es] = 1;
+            }
+        for (int e = 0; ok && e < L.nE; ++e) ok = seen[e] != 0;
+        c->vF = ok;
+        c->vminF1 = -1;
+        for (int v = 0; ok && v < L.nV && c->vminF1 < 0; ++v)
+            for (int k = 0; k < 3; ++k)
+                if (c->d_eov[(size_t)k * sV + v] >= L.eb.if1) {
+                    c->vminF1 = v;
+                    break;
+                }
+        if (ok && c->vminF1 < 0) c->vminF1 = L.nV;
+    }
+    c->un_c12 = L.nOwnC, c->un_e12 = L.nOwnE, c->un_e3 = L.nOwnE;
+    {
+        const char *uf = getenv("FBLTS_UNFUSE");
+        c->un_fuse = !(uf && uf[0] == '0');
+    }
+    if (c->cfg.unsplit) {
+        auto ce = [&](int e) {
+            if (e >= 0) c->un_e12 = std::min(c->un_e12, e);
+        };
+        auto cc = [&](int i) {
+            if (i >= 0) c->un_c12 = std::min(c->un_c12, i);
+        };
+        for (int v = c->vminF; v < L.nV; ++v)       // slow_pre vertex role: kite h, circulation u
+            for (int k = 0; k < 3; ++k) {
+                const int es = c->d_eov[(size_t)k * sV + v];
+                cc(c->d_cov[(size_t)k * sV + v]);
+                ce(es >= 0 ? es : ~es);
+            }
+        for (int i = L.cb.if1; i < L.nOwnC; ++i)   // cell role: u on the cell's edges
+            for (int j = 0; j < c->d_nEoC[i]; ++j) {
+                const int es = c->d_ec[((size_t)i * G + j) * 2];
+                ce(es >= 0 ? es : ~es);
+            }
+        for (int e = L.eb.if1; e < L.nOwnE; ++e) {  // edge role (h, u) and slow_edge on F_E (h, u, eoe's u)
+            ce(e);
+            cc(c->d_coe[2 * e]);
+            cc(c->d_coe[2 * e + 1]);
+            if (e >= L.eb.f)
+                for (int j = 0; j < c->d_nEoE[e]; ++j) ce(c->d_eoe[(size_t)j * sE + e]);
+        }
+        for (int i = L.cb.if2; i < L.nOwnC; ++i)
+            for (int j = 0; j < c->d_nEoC[i]; ++j) {
+                const int es = c->d_ec[((size_t)i * G + j) * 2];
+                c->un_e3 = std::min(c->un_e3, es >= 0 ? es : ~es);
+            }
+    }
     // ---- halo exchanges (nranks > 1)
     for (int x = 0; x < X_NUM; ++x) {
         L.x[x] = Xchg();
@@ -1365,6 +1436,7 @@ size_t plan_workspace(fblts_ctx *c, char *base) {
         d.eov = eov, d.cov = cov, d.kite = kite, d.areaTri = areaTri, d.fV = fV;
         d.vOwn = vOwn, d.eOwn = eOwn;
         d.nB = L.nB, d.cb = L.cb, d.cbI = L.cbI, d.eb = L.eb, d.cbh = L.cbh;
+        d.vF = c->vF ? 1 : 0;
         c->hbuf[0] = hA, c->hbuf[1] = hB, c->ubuf[0] = uA, c->ubuf[1] = uB;
         s.hN = hA, s.hNew = hB, s.uN = uA, s.uNew = uB;
         c->diag_out = s.diag + DIAG_BLOCKS * 6;
@@ -1818,7 +1890,7 @@ bool enqueue_phase(fblts_ctx *c, int par, int ph, cudaStream_t s, Recorder *rec,
                                         cudaMemcpyDeviceToDevice, s);
                 } else {
                     launch_refresh_views(m, st, hN, hNew, hk, uN, uk, sc, pred(k), s);
-                    launch_slow_pre_range(m, st, st.hv, st.uv, c->vminF, m.cb.if1, m.eb.if1, s);
+                    launch_slow_pre_range(m, st, st.hv, st.uv, c->vminF, m.cb.if1, m.eb.if1, s, c->vminF1);
                     launch_slow_edge_range(m, st, st.hv, st.uv, st.Sk, m.eb.f, m.eb.end, sc, s);
                 }
                 any = true;
@@ -1996,21 +2068,42 @@ int enqueue_unsplit_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
         return pc;
     };
     const bool vort = c->cfg.vorticity != 0;
-    auto slow = [&](const double *U, int e0, int e1, double *pvout = nullptr) {   // Phi^slow(U, st.hv) on [e0, e1) -> st.Sk
-        if (!c->cfg.slow) {
+    // slow sweeps + velocity update on [e0, e1): with the slow terms on, the update runs inside the
+    // slow edge sweep (VelFuse: no S store, no separate velocity sweep; the same bits as k_un_vel)
+    auto slow_vel = [&](const double *U, int e0, int e1, double *pvout, int vkind, const double *base, double *out,
+                        double cc, double *acc, int a0, int a1, int first) {
+        if (!c->cfg.slow) {                                 // S = 0 (and the PV flux part)
             if (e1 > e0) cudaMemsetAsync(st.Sk + e0, 0, (size_t)(e1 - e0) * 8, s);
             if (pvout && e1 > e0) cudaMemsetAsync(pvout + e0, 0, (size_t)(e1 - e0) * 8, s);
+            mark(vkind);
+            launch_un_vel(m, st, base, out, cc, e0, e1, acc, a0, a1, first, sc, s);
             return;
         }
         mark(K_SLOW_PRE);
         // S on F_E needs q, K, F only on its stencil (vertices of F_E edges, cells from IF-1, edges
         // from IF-1_E; the slow-term refresh's range); wider extents and the energy-conserving PV
         // flux (q_hat on the edges of the cells of F_E edges: one more vertex ring) take the whole mesh
-        if (e0 >= m.eb.f && !sc.pve) launch_slow_pre_range(m, st, st.hv, U, c->vminF, m.cb.if1, m.eb.if1, s);
+        if (e0 >= m.eb.f && !sc.pve) launch_slow_pre_range(m, st, st.hv, U, c->vminF, m.cb.if1, m.eb.if1, s, c->vminF1);
         else launch_slow_pre_range(m, st, st.hv, U, 0, 0, 0, s);
         mark(K_SLOW_EDGE);
-        launch_slow_edge_range(m, st, st.hv, U, st.Sk, e0, e1, sc, s, pvout);
+        if (!c->un_fuse) {                                  // FBLTS_UNFUSE=0: S stored, separate velocity sweep
+            launch_slow_edge_range(m, st, st.hv, U, st.Sk, e0, e1, sc, s, pvout);
+            mark(vkind);
+            launch_un_vel(m, st, base, out, cc, e0, e1, acc, a0, a1, first, sc, s);
+            return;
+        }
+        VelFuse vf;
+        vf.base = base;
+        vf.out = out;
+        vf.c = cc;
+        vf.acc = acc;
+        vf.a0 = a0;
+        vf.a1 = a1;
+        vf.first = first;
+        launch_slow_edge_range(m, st, st.hv, U, nullptr, e0, e1, sc, s, pvout, &vf);
     };
+    // fine views of stages 1-2 on the F_E slow stencil only (the energy-conserving PV flux reads the whole mesh)
+    const int v12c = sc.pve ? 0 : c->un_c12, v12e = sc.pve ? 0 : c->un_e12;
     // ---- coarse phase: extents X1 = C u F^5, Y1 = C_E u F^4_E, X2 = C u F^3, Y2 = C_E u F^2_E,
     //      X3 = C u F^1, Y3 = IF-1_E u int_E (IF-2_E computed as scratch)
     const double *Hs[3] = {hN, st.h1, st.h2};
@@ -2022,9 +2115,8 @@ int enqueue_unsplit_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
     for (int q = 0; q < 3; ++q) {
         mark(kinds[q]);
         launch_un_cstage(m, st, q + 1, hN, Hs[q], Us[q], Hout[q], sc, Xend[q], s);
-        slow(Us[q], 0, Yend[q], vort && q == 2 ? st.Pv : nullptr);
-        mark(K_COARSE_VEL);
-        launch_un_vel(m, st, uN, st.un[q], cs[q], 0, Yend[q], nullptr, 0, 0, 0, sc, s);
+        slow_vel(Us[q], 0, Yend[q], vort && q == 2 ? st.Pv : nullptr, K_COARSE_VEL, uN, st.un[q], cs[q], nullptr, 0, 0,
+                 0);
         if (vort && q == 2) launch_vort_int(st, sc.c3, m.eb.if2, s);     // eta companion: int_E, dt PV
     }
     if (m.eb.if2 > 0) CUDA_TRY(c, cudaMemcpyAsync(uNew, st.un[2], (size_t)m.eb.if2 * 8, cudaMemcpyDeviceToDevice, s));
@@ -2035,23 +2127,18 @@ int enqueue_unsplit_step(fblts_ctx *c, int par, cudaStream_t s, Recorder *rec) {
             const PredConst pc = pred(k);
             mark(K_FINE_S1);                                         // stage 1: thickness (U0 = u^{n,k} on F_E)
             launch_fine_s1(m, st, hN, hNew, hk, uk, sc, pc, k, s, m.cb, true);
-            launch_un_views(m, st, 1, hN, hNew, hk, nullptr, uN, uk, sc, pc, s);
-            slow(st.uv, m.eb.f, m.eb.end);
-            mark(K_FINE_VEL);
-            launch_un_vel(m, st, uk, st.unk[0], sc.c1f, m.eb.f, m.eb.end, nullptr, 0, 0, 0, sc, s);
+            launch_un_views(m, st, 1, hN, hNew, hk, nullptr, uN, uk, sc, pc, s, v12c, v12e);
+            slow_vel(st.uv, m.eb.f, m.eb.end, nullptr, K_FINE_VEL, uk, st.unk[0], sc.c1f, nullptr, 0, 0, 0);
             mark(K_FINE_S2);                                         // stage 2
             launch_un_fstage(m, st, 2, hN, hNew, hk, st.unk[0], st.h2, sc, pc, k, s);
-            launch_un_views(m, st, 2, hN, hNew, hk, nullptr, uN, st.unk[0], sc, pc, s);
-            slow(st.uv, m.eb.f, m.eb.end);
-            mark(K_FINE_VEL);
-            launch_un_vel(m, st, uk, st.unk[1], sc.c2f, m.eb.f, m.eb.end, nullptr, 0, 0, 0, sc, s);
+            launch_un_views(m, st, 2, hN, hNew, hk, nullptr, uN, st.unk[0], sc, pc, s, v12c, v12e);
+            slow_vel(st.uv, m.eb.f, m.eb.end, nullptr, K_FINE_VEL, uk, st.unk[1], sc.c2f, nullptr, 0, 0, 0);
             mark(K_FINE_S3);                                         // stage 3 + correction summands
-            launch_un_views(m, st, 3, hN, hNew, hk, hk, uN, st.unk[1], sc, pc, s);   // U2 view for the sweep
+            launch_un_views(m, st, 3, hN, hNew, hk, hk, uN, st.unk[1], sc, pc, s, m.nOwnC, c->un_e3);   // U2 view for the sweep
             launch_un_fstage(m, st, 3, hN, hNew, hk, st.uv, hb(k), sc, pc, k, s);
-            launch_un_views(m, st, 3, hN, hNew, hk, hb(k), uN, st.unk[1], sc, pc, s);
-            slow(st.uv, m.eb.if2, m.eb.end, vort ? st.Pv : nullptr);
-            mark(K_FINE_VEL);
-            launch_un_vel(m, st, uk, ub(k), sc.c3f, m.eb.if2, m.eb.end, st.accU, m.eb.if2, m.eb.f, k == 0, sc, s);
+            launch_un_views(m, st, 3, hN, hNew, hk, hb(k), uN, st.unk[1], sc, pc, s, 0, 0);
+            slow_vel(st.uv, m.eb.if2, m.eb.end, vort ? st.Pv : nullptr, K_FINE_VEL, uk, ub(k), sc.c3f, st.accU, m.eb.if2,
+                     m.eb.f, k == 0);
             if (vort) launch_vort_fine(m, st, sc.c3f, k == 0, s);   // F_E: += dt/M PV^k; IF edges: sum_k PV^k
         }
         mark(K_CORRECT);

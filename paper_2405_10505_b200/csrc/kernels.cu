@@ -113,7 +113,10 @@ __device__ __forceinline__ void load_row(const DevMesh &m, int i, int2 (&r)[G]) 
 // One launch, three index spaces: vertices (q_v), cells (K_i), edges (F_e).
 // q_v = (zeta_v + f_v) / h_v,  zeta_v = (sum t d u)/A_v,  h_v = (sum kite h)/A_v
 // K_i = (sum 0.25 l d u u) / A_i   (Q18);   F_e = (0.5 (h_c0 + h_c1)) u_e   (Q1)
-template <int G>
+// VF (DevMesh::vF, full sweeps): the vertex role also writes F_e for the edges e = eov[k][v] with
+// v = voe[e][1]; their cells are the kite cells k, k+1 whose h it has loaded, so F costs no extra
+// reads and the edge role is not launched ((0.5 (h_a + h_b)) u_e: the same bits in either cell order).
+template <int G, bool VF>
 __global__ void __launch_bounds__(TPB) k_slow_pre(DevMesh m, const double *__restrict__ h,
                                                   const double *__restrict__ u, double *__restrict__ q,
                                                   double *__restrict__ K, double *__restrict__ F,
@@ -123,17 +126,27 @@ __global__ void __launch_bounds__(TPB) k_slow_pre(DevMesh m, const double *__res
         const int v = v0 + b * TPB + threadIdx.x;
         if (v >= m.nV) return;
         const double A = m.areaTri[v], fv = m.fV[v];       // independent loads first
-        double circ = 0.0;
+        int ev[3];
+        bool pv[3];
+        double uk[3], hk[3], circ = 0.0;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            bool pos;
-            const int e = decode(m.eov[k * m.strideV + v], pos);
-            const double t = m.dc[e] * u[e];
-            circ = circ + (pos ? t : -t);
+            ev[k] = decode(m.eov[k * m.strideV + v], pv[k]);
+            uk[k] = u[ev[k]];
+            const double t = m.dc[ev[k]] * uk[k];
+            circ = circ + (pv[k] ? t : -t);
         }
         double hv = 0.0;                                   // (its gathers before the first division)
 #pragma unroll
-        for (int k = 0; k < 3; ++k) hv = hv + m.kite[k * m.strideV + v] * h[m.cov[k * m.strideV + v]];
+        for (int k = 0; k < 3; ++k) {
+            hk[k] = h[m.cov[k * m.strideV + v]];
+            hv = hv + m.kite[k * m.strideV + v] * hk[k];
+        }
+        if (VF) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                if (pv[k]) F[ev[k]] = (0.5 * (hk[k] + hk[(k + 1) % 3])) * uk[k];
+        }
         const double zeta = circ / A;
         hv = hv / A;
         q[v] = (zeta + fv) / hv;
@@ -173,13 +186,16 @@ __global__ void __launch_bounds__(TPB) k_slow_pre(DevMesh m, const double *__res
 // PVE (energy-conserving PV flux): the term q_hat_e F_perp_e becomes
 // sum_j (W_j F_eoe_j) (0.5 (q_hat_e + q_hat_eoe_j)) with q_hat per edge from k_qhat (oracle
 // trisk.pv_flux_energy); it does no work on the flow (sum_e l_e d_e F_e PV_e = 0).
-template <int MAXE2, bool HUR, bool PVE>
+// VEL (unsplit FB-LTS): the stage's velocity update follows in the same thread (see
+// VelFuse) instead of a store of S_e and a separate k_un_vel sweep; h is then the stage's HS view.
+template <int MAXE2, bool HUR, bool PVE, bool VEL>
 __global__ void __launch_bounds__(TPB, FBLTS_SLOW_MINB) k_slow_edge(DevMesh m, const double *__restrict__ h,
                                                    const double *__restrict__ q, const double *__restrict__ K,
                                                    const double *__restrict__ F, const double *__restrict__ u,
                                                    const double *__restrict__ qe,
                                                    double *__restrict__ S, double *__restrict__ pvout,
-                                                   double rho0, double cd, double cw, int e0, int e1) {
+                                                   double rho0, double cd, double cw, int e0, int e1,
+                                                   VelFuse vf, double g) {
     const int e = e0 + blockIdx.x * TPB + threadIdx.x;
     if (e >= e1) return;
     const int2 c = m.coe[e];                  // issued first: its gathers (q, K, h) end the chain (measured -3 %)
@@ -196,6 +212,7 @@ __global__ void __launch_bounds__(TPB, FBLTS_SLOW_MINB) k_slow_edge(DevMesh m, c
         }
         K0 = K[c.x], K1 = K[c.y], h0 = h[c.x], h1 = h[c.y], tau = m.tau[e], dce = m.dc[e];
     }
+
     // F_perp = sum_j W_j F_eoe_j in slot order, gathered in chunks of CH slots (register budget);
     // with the hurricane terms also v_e = sum_j W_j u_eoe_j (tangential reconstruction)
     constexpr int CH = FBLTS_SLOW_CHUNK < MAXE2 ? FBLTS_SLOW_CHUNK : MAXE2;
@@ -222,6 +239,14 @@ __global__ void __launch_bounds__(TPB, FBLTS_SLOW_MINB) k_slow_edge(DevMesh m, c
                 if (HUR) vt = vt + w[j] * ut[HUR ? j : 0];
             }
     }
+    // VEL: the update's own loads (z_b, base / accumulator) after the slot loop (not live in it: no
+    // spills at 5 CTAs per SM) but before the divisions
+    const bool ia = VEL && vf.acc && e >= vf.a0 && e < vf.a1;
+    double zb0 = 0.0, zb1 = 0.0, b0 = 0.0;
+    if (VEL) {
+        zb0 = m.zb[c.x], zb1 = m.zb[c.y];
+        b0 = ia ? (vf.first ? 0.0 : vf.acc[e - vf.a0]) : vf.base[e];
+    }
     double pv;
     if (PVE) {
         pv = fp;
@@ -247,7 +272,13 @@ __global__ void __launch_bounds__(TPB, FBLTS_SLOW_MINB) k_slow_edge(DevMesh m, c
         const double Wd = cw * ws * dn / he;
         s = s - D + Wd;
     }
-    S[e] = s;
+    if (VEL) {
+        const double phi = phi_fast(g, h0, zb0, h1, zb1, dce);
+        if (ia) vf.acc[e - vf.a0] = b0 + (phi + s);
+        else vf.out[e] = b0 + vf.c * (phi + s);
+    } else {
+        S[e] = s;
+    }
 }
 
 // ---------------------------------------------------------------- coarse stages
@@ -1586,12 +1617,18 @@ __global__ void __launch_bounds__(TPB) k_refresh_views(DevMesh m, FineArrays a, 
 
 
 void launch_slow_pre_range(const DevMesh &m, const DevState &st, const double *h, const double *u, int v0, int c0,
-                           int e0, cudaStream_t s) {
+                           int e0, cudaStream_t s, int v0vf) {
+    // F_e in the vertex role: full sweeps, or a range sweep whose caller passes v0vf = the first vertex
+    // that owns an edge >= e0 (<= v0; the extra vertices' q is recomputed, not used)
+    const bool vf = m.vF && ((v0 == 0 && e0 == 0) || v0vf >= 0);
+    if (vf && v0vf >= 0) v0 = std::min(v0, v0vf);
     const unsigned nbV = nblocks(std::max(0, m.nV - v0)), nbC = nblocks(std::max(0, m.nC - c0)),
-                   nbE = nblocks(std::max(0, m.nE - e0));
+                   nbE = vf ? 0u : nblocks(std::max(0, m.nE - e0));
     if (nbV + nbC + nbE == 0) return;
-    FBLTS_DISPATCH_G(m.ecS, k_slow_pre<G><<<nbV + nbC + nbE, TPB, 0, s>>>(m, h, u, st.q, st.K, st.F, nbV, nbC, v0, c0,
-                                                                           e0));
+    FBLTS_DISPATCH_G(m.ecS, {
+        if (vf) k_slow_pre<G, true><<<nbV + nbC + nbE, TPB, 0, s>>>(m, h, u, st.q, st.K, st.F, nbV, nbC, v0, c0, e0);
+        else k_slow_pre<G, false><<<nbV + nbC + nbE, TPB, 0, s>>>(m, h, u, st.q, st.K, st.F, nbV, nbC, v0, c0, e0);
+    });
 }
 void launch_slow_pre(const DevMesh &m, const DevState &st, const double *h, const double *u, cudaStream_t s) {
     launch_slow_pre_range(m, st, h, u, 0, 0, 0, s);
@@ -1605,12 +1642,19 @@ __global__ void __launch_bounds__(TPB) k_qhat(DevMesh m, const double *__restric
 }
 
 void launch_slow_edge_range(const DevMesh &m, const DevState &st, const double *h, const double *u, double *out,
-                            int e0, int e1, const StepConst &sc, cudaStream_t s, double *pvout) {
+                            int e0, int e1, const StepConst &sc, cudaStream_t s, double *pvout, const VelFuse *vel) {
     if (e1 <= e0) return;
     const unsigned nb = nblocks(e1 - e0);
     if (sc.pve) k_qhat<<<nblocks(m.nE), TPB, 0, s>>>(m, st.q, st.qe);
+    const VelFuse vf = vel ? *vel : VelFuse();
+#define FBLTS_SLOW_EDGE4(ME2, HU, PV, VL)                                                                          \
+    k_slow_edge<ME2, HU, PV, VL><<<nb, TPB, 0, s>>>(m, h, st.q, st.K, st.F, u, st.qe, out, pvout, sc.rho0, sc.cd,  \
+                                                    sc.cw, e0, e1, vf, sc.g)
 #define FBLTS_SLOW_EDGE3(ME2, HU, PV)                                                                              \
-    k_slow_edge<ME2, HU, PV><<<nb, TPB, 0, s>>>(m, h, st.q, st.K, st.F, u, st.qe, out, pvout, sc.rho0, sc.cd, sc.cw, e0, e1)
+    do {                                                                                                         \
+        if (vel) FBLTS_SLOW_EDGE4(ME2, HU, PV, true);                                                            \
+        else FBLTS_SLOW_EDGE4(ME2, HU, PV, false);                                                               \
+    } while (0)
 #define FBLTS_SLOW_EDGE(ME2)                                                                                     \
     do {                                                                                                         \
         if (sc.pve) {                                                                                            \
@@ -1629,6 +1673,7 @@ void launch_slow_edge_range(const DevMesh &m, const DevState &st, const double *
         FBLTS_SLOW_EDGE(30);
 #undef FBLTS_SLOW_EDGE
 #undef FBLTS_SLOW_EDGE3
+#undef FBLTS_SLOW_EDGE4
 }
 void launch_slow_edge(const DevMesh &m, const DevState &st, const double *h, const double *u, const StepConst &sc,
                       cudaStream_t s) {
@@ -1828,9 +1873,10 @@ __global__ void __launch_bounds__(TPB) k_un_views(DevMesh m, FineArrays a, const
                                                   const double *__restrict__ uN, const double *__restrict__ ufine,
                                                   const double *__restrict__ u1c, const double *__restrict__ u2c,
                                                   const double *__restrict__ u3c, double *__restrict__ hsv,
-                                                  double *__restrict__ uv, StepConst sc, PredConst p, unsigned nbC) {
+                                                  double *__restrict__ uv, StepConst sc, PredConst p, unsigned nbC,
+                                                  int c0, int e0) {
     if (blockIdx.x < nbC) {
-        const int i = blockIdx.x * TPB + threadIdx.x;
+        const int i = c0 + blockIdx.x * TPB + threadIdx.x;
         if (i >= m.nOwnC) return;
         double H, HS;
         if (S == 1) view1<true>(m, sc, p, a, i, H, HS);
@@ -1838,7 +1884,7 @@ __global__ void __launch_bounds__(TPB) k_un_views(DevMesh m, FineArrays a, const
         else HS = view3<true>(m, sc, p, a, hnext, i);
         hsv[i] = HS;
     } else {
-        const int e = (blockIdx.x - nbC) * TPB + threadIdx.x;
+        const int e = e0 + (blockIdx.x - nbC) * TPB + threadIdx.x;
         if (e >= m.nOwnE) return;
         const int ec = ecls(m.eb, e);
         double v;
@@ -1906,15 +1952,17 @@ void launch_un_vel(const DevMesh &m, const DevState &st, const double *base, dou
 }
 void launch_un_views(const DevMesh &m, const DevState &st, int stage, const double *hN, const double *hNew,
                      const double *hk, const double *hnext, const double *uN, const double *ufine,
-                     const StepConst &sc, const PredConst &pc, cudaStream_t s) {
+                     const StepConst &sc, const PredConst &pc, cudaStream_t s, int c0, int e0) {
     const FineArrays a = fine_arrays(st, hN, hNew, hk);
-    const unsigned nbC = nblocks(m.nOwnC), nbE = nblocks(m.nOwnE);
-    if (stage == 1)
-        k_un_views<1><<<nbC + nbE, TPB, 0, s>>>(m, a, hnext, uN, ufine, st.un[0], st.un[1], st.un[2], st.hv, st.uv, sc, pc, nbC);
-    else if (stage == 2)
-        k_un_views<2><<<nbC + nbE, TPB, 0, s>>>(m, a, hnext, uN, ufine, st.un[0], st.un[1], st.un[2], st.hv, st.uv, sc, pc, nbC);
-    else
-        k_un_views<3><<<nbC + nbE, TPB, 0, s>>>(m, a, hnext, uN, ufine, st.un[0], st.un[1], st.un[2], st.hv, st.uv, sc, pc, nbC);
+    const unsigned nbC = c0 < m.nOwnC ? nblocks(m.nOwnC - c0) : 0u, nbE = e0 < m.nOwnE ? nblocks(m.nOwnE - e0) : 0u;
+    if (nbC + nbE == 0) return;
+#define FBLTS_UN_VIEWS(S)                                                                                         \
+    k_un_views<S><<<nbC + nbE, TPB, 0, s>>>(m, a, hnext, uN, ufine, st.un[0], st.un[1], st.un[2], st.hv, st.uv, sc, \
+                                            pc, nbC, c0, e0)
+    if (stage == 1) FBLTS_UN_VIEWS(1);
+    else if (stage == 2) FBLTS_UN_VIEWS(2);
+    else FBLTS_UN_VIEWS(3);
+#undef FBLTS_UN_VIEWS
 }
 void launch_un_fstage(const DevMesh &m, const DevState &st, int stage, const double *hN, const double *hNew,
                       const double *hk, const double *U, double *out, const StepConst &sc, const PredConst &pc,

@@ -444,6 +444,32 @@ def test_unsplit_matches_oracle(Solver, which, M):
     assert np.array_equal(hg, ho) and np.array_equal(ug, uo), "not bitwise (canonical arithmetic, --fmad=false)"
 
 
+@pytest.mark.parametrize("vort", [False, True])
+def test_unsplit_config5_block(Solver, vort):
+    """Unsplit FB-LTS on a 256 x 256 block of the config-5 recipe (M = 4; int, IF and F regions all
+    thousands of cells wide): the velocity update fused into the slow edge sweep and the fine views
+    restricted to the F_E slow stencil (host.cu enqueue_unsplit_step) give the oracle's
+    fblts_step(split=False) bit for bit, h, u and (with the companion) eta, after 4 steps."""
+    c = configs.config5(nx=256, ny=256)
+    m, n = c.mesh, 4
+    lab = lts.label_regions(m, c.fine_mask)
+    eta0 = trisk.relative_vorticity(m, c.u0) + m.fVertex
+    out = lts.run(m, lab, c.h0, c.u0, c.dt, c.M, phys_of(c), n, split=False, eta=eta0 if vort else None)
+    ho, uo = out[0], out[1]
+    s = Solver(m, c.fine_mask, c.dt, c.M, g=c.g, beta=c.beta, rho0=c.rho0, slow=c.slow, tau_n=c.tau_n,
+               unsplit=True, vorticity=vort)
+    s.set_state(c.h0, c.u0)
+    if vort:
+        s.set_vorticity(eta0)
+    s.step(n)
+    hg, ug, _ = s.state()
+    eg = s.vorticity() if vort else None
+    s.close()
+    assert np.array_equal(hg, ho) and np.array_equal(ug, uo), "not bitwise (canonical arithmetic, --fmad=false)"
+    if vort:
+        assert np.array_equal(eg, out[2]), float(np.max(np.abs(eg - out[2])))
+
+
 @pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("which,M", [("config1", 4), ("shelf", 3), ("shelf", 1)])
 def test_vorticity_companion_theorem2(Solver, which, M, split):
