@@ -88,7 +88,10 @@ def byte_model(counts, M, fused, sub=0, maxE=6, maxE2=10):
     fs1 = lambda lo: cells(lo, top) * (slotC + 8 + 8 + 8) + edges(lo, top) * edge_s1
     fvel = lambda lo: edges(lo, 8) * vel_e + cells(lo, 8) * vel_c
     b = {}
-    b["slow_pre"] = V * (12 + 12 + 24 + 8 + 8) + C * (4 + 4 * maxE + 8 + 8) + E * (8 + 8 + 8 + 8)
+    # per edge: cellsOnEdge, u, d_e, write F -- cellsOnEdge not read when F_e is formed in the vertex
+    # role (DevMesh::vF, every mesh here; FBLTS_VF=0 turns it off)
+    coe_b = 0 if os.environ.get("FBLTS_VF", "1") != "0" else 8
+    b["slow_pre"] = V * (12 + 12 + 24 + 8 + 8) + C * (4 + 4 * maxE + 8 + 8) + E * (coe_b + 8 + 8 + 8)
     b["slow_edge"] = E * (4 + 4 * maxE2 + 8 * maxE2 + 8 + 8 + 8 + 8 + 8) + V * 8 + C * 8 + C * 8
     b["coarse_s1"] = cells(0, 7) * cell_s1 + edges(0, 7) * edge_s1
     b["coarse_s2"] = cells(0, 5) * cell_s + edges(0, 5) * edge_s
@@ -138,7 +141,8 @@ def unsplit_byte_model(counts, M, maxE=6, maxE2=10):
     cells = lambda lo, hi: sum(cc[lo:hi + 1])
     edges = lambda lo, hi: sum(ec[lo:hi + 1])
     slotC = 4 + 4 * maxE + 4 * maxE
-    pre_full = V * (12 + 12 + 24 + 8 + 8) + C * (4 + 4 * maxE + 8 + 8) + E * (8 + 8 + 8 + 8)
+    coe_b = 0 if os.environ.get("FBLTS_VF", "1") != "0" else 8     # as in byte_model
+    pre_full = V * (12 + 12 + 24 + 8 + 8) + C * (4 + 4 * maxE + 8 + 8) + E * (coe_b + 8 + 8 + 8)
     fstencil = cells(2, 8) / max(1, C)                              # F u IF-1 share of the mesh
     pre_fine = pre_full * fstencil
     edge_b = 4 + 4 * maxE2 + 8 * maxE2 + 8 * 5 + 8 * 2              # slow_edge per edge (+ q, K, h gathers)
